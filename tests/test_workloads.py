@@ -1,0 +1,72 @@
+"""Pins of the workload generator (synthetic objectives of Fig. 1 / Table I, config shapes)."""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import gen, synthetic as syn
+
+
+def test_p11_case3_all_ones():
+    """P11 / SPEC S:L121: Case 3, eps = 0, all x = 1 -> log 50 + log 50 + log 10 + log 5
+    = 11.736 (re-derived to full precision in SURVEY.md §4: 11.736069016284778)."""
+    x = np.ones((1, 20))
+    assert abs(syn.f20(x, 3)[0] - 11.736069016284778) < 1e-12
+    g = syn.f20_groups(x, 3)
+    assert abs(g[0][0] - math.log(50)) < 1e-12 and abs(g[2][0] - math.log(10)) < 1e-12
+    assert abs(g[3][0] - math.log(5)) < 1e-12
+
+
+def test_p11_case4_group3():
+    """Case 4, x_10..14 = 2, x_15..19 = 1 -> raw G3 = 5 (2 * 1)^2 = 20."""
+    x = np.ones((1, 20))
+    x[:, 10:15] = 2.0
+    assert abs(syn.group3(x, 4)[0] - 20.0) < 1e-12
+    assert abs(syn.f20_groups(x, 4)[2][0] - math.log(20.0)) < 1e-12
+
+
+def test_p12_group_minimum():
+    """P12: each raw Group-1 term has minimum -50 at x_0 = ... = x_4 = k + 1/2."""
+    for k in (-3, 0, 7):
+        x = np.full((1, 20), k + 0.5)
+        assert abs(syn.group1(x)[0] + 50.0) < 1e-9
+    rng = np.random.default_rng(0)
+    assert syn.group1(rng.uniform(-50, 50, (10000, 20))).min() > -50.0
+
+
+@pytest.mark.parametrize("case,paper", [(1, 19.4), (2, 25.8), (3, 27.7), (4, 53.2), (5, 74.4)])
+def test_table3_random_search_column(case, paper):
+    """Coarse pin of the synthetic functions: the mean over 5 repeats
+    of the minimum of 200 uniform samples on [-50, 50]^20 with sigma = 0.1 matches the
+    Random-Search column of Table III within a few units."""
+    mins = []
+    for rep in range(5):
+        g = np.random.default_rng(100 * case + rep)
+        x = g.uniform(-50, 50, (200, 20))
+        eps = 0.1 * g.standard_normal((200, syn.N_EPS))
+        mins.append(syn.f20(x, case, eps).min())
+    assert abs(np.mean(mins) - paper) < 6.0
+
+
+def test_config_shapes_and_determinism():
+    w1 = gen.make(3, M=64, n=10)
+    w2 = gen.make(3, M=64, n=10)
+    assert w1.S == 64
+    for a, b in zip(w1.searches, w2.searches):
+        assert np.array_equal(a.X, b.X) and np.array_equal(a.y, b.y)
+    assert all(np.array_equal(a, b) for a, b in zip(w1.Xstar, w2.Xstar))
+    w = gen.make(1)
+    assert w.Xstar[0].shape == (4096, 2) and w.searches[0].X.shape == (20, 2)
+    assert w.Xstar[0][64 * 5 + 7, 0] == np.float32(5 / 63) and w.Xstar[0][64 * 5 + 7, 1] == np.float32(7 / 63)
+
+
+def test_sharding_reproduces_global_rows():
+    """rank r's contiguous shard holds exactly the global rows of X*."""
+    full = gen.make(2, n=8, M=1000)
+    for world in (2, 3, 8):
+        rows = []
+        for r in range(world):
+            w = gen.make(2, n=8, M=1000, rank=r, world=world)
+            assert w.m_global_base[0] == min(1000, r * -(-1000 // world))
+            rows.append(w.Xstar[0])
+        assert np.array_equal(np.concatenate(rows), full.Xstar[0])
