@@ -1,0 +1,164 @@
+/*
+ * gpbo.h -- C ABI of libgpbo.so, the B200 (sm_100a) GP-surrogate + Expected-Improvement hot path
+ * of arXiv 2403.08131 ("Cost-Effective Methodology for Complex Tuning Searches in HPC").
+ *
+ * The paper's BO searches (§III.A) train a surrogate on the observed
+ * configurations and let "an acquisition function guide the selection of the next
+ * configuration"; their cost is "the training complexity of Gaussian Processes ... O(N^3)"
+ * (L249, L256, §IV.D).  This library is that step, batched over the many sub-searches the
+ * interdependence analysis produces (L163-173, L245-256) and sharded over GPUs:
+ *
+ *   gp_fit           H1-H4  standardise y, Gram matrix, jittered Cholesky, L^-1, alpha
+ *   gp_posterior     H6-H8  posterior mean / latent variance / EI of caller candidates
+ *   ei_score_argmax  H6-H10 EI of caller candidates, per-search argmax, cross-GPU max
+ *
+ * (H* = the step rows of SURVEY.md §8(a); readings R* = SURVEY.md §8(c), listed in DESIGN.md.)
+ * The paper names neither kernel nor acquisition (GPTune internals, L77): GP with ARD RBF or
+ * Matern-5/2 kernel (reading R1/R2), EI for minimisation with xi = 0
+ * (readings R3-R5), ties to the lowest global candidate index.
+ *
+ * Conventions for every entry point
+ *  - Every call returns gpbo_status; no C++ exception crosses the ABI.  On error the message
+ *    is available from gpbo_last_error(ctx).
+ *  - Calls are ordered on the ctx's CUDA stream and are synchronous on return (they end with
+ *    a stream synchronisation because they return host-side results).
+ *  - Inputs are read only during the call and remain owned by the caller.  "mem" selects
+ *    whether the caller's array pointers are host (GPBO_HOST, any host memory; pinned is
+ *    faster) or device (GPBO_DEVICE, on ctx's device) addresses.  Shape arrays (n, d, m_off,
+ *    m_global_base) are always host arrays.
+ *  - A gpbo_model is library-owned device state until gp_model_free.  A ctx is bound to one
+ *    device and stream and is NOT thread-safe.
+ *  - Layouts: X and X* are row-major float32 with d_s contiguous encoded coordinates per row,
+ *    concatenated over the S searches; y is float64.  Encoded coordinates are expected in
+ *    [0, 1] (reading R8) but any finite value is accepted.
+ *  - Limits (v1): 1 <= S, 1 <= n_s <= GPBO_MAX_N, 1 <= d_s <= GPBO_MAX_D, M_s < 2^32 - 1.
+ *  - Non-finite inputs (X, y, lengthscale, variances) -> GPBO_EINVAL.
+ */
+#ifndef GPBO_H
+#define GPBO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPBO_MAX_N 512
+#define GPBO_MAX_D 64
+#define GPBO_NCCL_ID_BYTES 128
+
+typedef enum {
+  GPBO_OK = 0,
+  GPBO_EINVAL = 1,        /* bad shape / pointer / non-finite input                        */
+  GPBO_ENOTPD = 2,        /* Cholesky failed even at the largest jitter (reading R9)       */
+  GPBO_WDEGENERATE = 3,   /* warning: constant y; model built with y~ = 0     */
+  GPBO_ESAMPLING = 4,     /* candidate generation exhausted (reserved for bo_suggest)     */
+  GPBO_ECUDA = 5,         /* CUDA runtime error                                           */
+  GPBO_ENCCL = 6,         /* NCCL error                                                   */
+  GPBO_ENOMEM = 7,        /* device or pinned host allocation failed                      */
+  GPBO_ENOTSUP = 8        /* valid request outside this build's supported envelope        */
+} gpbo_status;
+
+typedef enum { GPBO_RBF = 0, GPBO_MATERN52 = 1 } gpbo_kernel;
+typedef enum { GPBO_HOST = 0, GPBO_DEVICE = 1 } gpbo_mem;
+
+typedef struct gpbo_ctx gpbo_ctx;
+typedef struct gpbo_model gpbo_model;
+
+/* ---------------------------------------------------------------- context
+ * gpbo_nccl_unique_id: writes a fresh NCCL unique id (GPBO_NCCL_ID_BYTES bytes) to out; call on
+ *   rank 0 and broadcast it (e.g. torch.distributed.broadcast_object_list) to the other ranks.
+ * gpbo_ctx_create: binds to CUDA device `device` and stream `cuda_stream` (a cudaStream_t; NULL
+ *   = the legacy default stream).  nranks > 1 creates an NCCL communicator from
+ *   `nccl_unique_id` (must be non-NULL then; NULL is required when nranks == 1).  All ranks
+ *   must call it collectively.  On success *out owns the communicator and scratch buffers. */
+gpbo_status gpbo_nccl_unique_id(void *out);
+gpbo_status gpbo_ctx_create(int device, void *cuda_stream, int nranks, int rank,
+                            const void *nccl_unique_id, gpbo_ctx **out);
+gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx);
+/* Last error message of this ctx ("" if none).  Valid until the next call on ctx. */
+const char *gpbo_last_error(const gpbo_ctx *ctx);
+/* Library build string (compile flags, arch) for logs. */
+const char *gpbo_version(void);
+
+/* ---------------------------------------------------------------- fit (H1-H4)
+ * Ragged batch of S sub-searches.  Search s has n[s] observations of d[s] encoded parameters:
+ *   X            float32 [sum n_s d_s]  rows of search s start at sum_{t<s} n_t d_t
+ *   y            float64 [sum n_s]      raw objective values, minimised (P L72)
+ *   lengthscale  float32 [sum d_s]      ARD lengthscales l > 0 (reading R2: k depends on
+ *                                       sum_j ((x_j - x'_j) / l_j)^2)
+ *   signal_var   float32 [S]            sf2 > 0, kernel amplitude in standardised units
+ *   noise_var    float32 [S]            sn2 >= 0, observation noise in standardised units
+ * The fit standardises y (ddof = 0; reading R7), builds K = k(X, X) + (sn2 + j_k) I with the
+ * jitter ladder j_k = 1e-8 10^k sf2, k = 0..6 (reading R9), factors K = L L^T in
+ * float64 (one CTA per sub-search), forms L^-1 and alpha = K^-1 y~, and stores the scoring
+ * operands on the device.  Outputs (host arrays, may be NULL):
+ *   status[S]   GPBO_OK | GPBO_ENOTPD | GPBO_WDEGENERATE per search
+ *   jitter_k[S] the k that succeeded, -1 on ENOTPD
+ * Returns GPBO_ENOTPD if any search failed (the model is still returned; failed searches
+ * score no candidate), GPBO_WDEGENERATE if any search is degenerate, else GPBO_OK. */
+typedef struct {
+  int32_t S;
+  const int32_t *n;
+  const int32_t *d;
+  const float *X;
+  const double *y;
+  const float *lengthscale;
+  const float *signal_var;
+  const float *noise_var;
+  gpbo_kernel kernel;
+  gpbo_mem mem;
+} gpbo_fit_args;
+
+gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *args, gpbo_model **out,
+                   int32_t *status, int32_t *jitter_k);
+void gp_model_free(gpbo_model *model);
+
+/* Fitted per-search statistics (host copies, any may be NULL): y mean and std (raw units),
+ * best = min y~ (standardised), alpha_l1 = ||alpha||_1 (the mu-tier diagnostic, reading R13). */
+gpbo_status gp_model_stats(const gpbo_model *model, int32_t s, double *mean, double *std,
+                           double *best, double *alpha_l1);
+
+/* Test/diagnostic export of the float64 fit of search s into caller host buffers of n_s*n_s
+ * (L, Linv: row-major, lower triangle, upper zero) and n_s (alpha) doubles; any may be NULL. */
+gpbo_status gp_model_export(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, double *L,
+                            double *Linv, double *alpha);
+
+/* ---------------------------------------------------------------- posterior (H6-H8, H11)
+ * Scores M candidates X* (float32 [M d_s], row-major) of search s and writes, per candidate,
+ *   mu  = mean + std mu~       (raw units; mu~ = k*^T alpha)
+ *   var = std^2 s2~            (latent variance, raw units^2; s2~ = max(sf2 - |L^-1 k*|^2, 0))
+ *   ei  = std EI(mu~, s2~, best)  (raw units; best = min y~)
+ * to float32 arrays in `mem` space (any may be NULL).  Same kernel as ei_score_argmax. */
+gpbo_status gp_posterior(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, const float *Xstar,
+                         int64_t M, gpbo_mem mem, float *mu, float *var, float *ei);
+
+/* ---------------------------------------------------------------- EI + argmax (H6-H10)
+ * Scores this rank's shard of every search's candidate pool and returns the global argmax.
+ *   Xstar          float32, concatenation over s of this rank's rows of search s (M_s_local x d_s)
+ *   m_off          int64 [S+1] host: rows of search s are Xstar rows [m_off[s], m_off[s+1])
+ *   m_global_base  int64 [S] host: global candidate index of this rank's first row of search s
+ *                  (NULL = 0); ties resolve to the lowest GLOBAL index (reading R10)
+ *   best           float64 [S] host: incumbent in raw units (NULL = min observed y; R3)
+ * Outputs (host, any may be NULL):
+ *   idx[S]  global index of the suggestion, -1 if search s had no scorable candidate
+ *   ei[S]   its EI in raw units (std * EI~)
+ * With nranks > 1 every rank returns the same result: the per-search 64-bit keys
+ * (EI~ bits << 32 | (2^32 - 1 - idx)) are combined with one ncclAllReduce(max) on ctx's
+ * communicator (H10). */
+gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float *Xstar,
+                            const int64_t *m_off, const int64_t *m_global_base,
+                            const double *best, gpbo_mem mem, int64_t *idx, float *ei);
+
+/* Number of CUDA kernels the library launched on ctx since creation (for bench accounting). */
+int64_t gpbo_launch_count(const gpbo_ctx *ctx);
+
+/* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
+ * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,
+ * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP).  Diagnostic/testing. */
+gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPBO_H */

@@ -1,0 +1,538 @@
+// Host side of the C ABI declared in include/gpbo.h: argument validation, model/ctx lifecycle,
+// stream-ordered staging of host inputs, kernel launches and the NCCL max-all-reduce of the
+// per-search argmax keys (H10).  No numerical work happens here: every step of the path runs in
+// the CUDA kernels of fit.cu / score_*.cu.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gpbo_internal.cuh"
+#include "score_tc.cuh"
+
+using gpbo::SearchMeta;
+
+struct gpbo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  unsigned long long *keys_d = nullptr;
+  unsigned long long *keys_h = nullptr;
+  int keys_cap = 0;
+  void *stage_d = nullptr;  // device staging of host-resident candidates / outputs
+  size_t stage_cap = 0;
+  void *aux_d = nullptr;    // per-call small arrays (offsets, bases, best, tile prefix)
+  void *aux_h = nullptr;    // pinned mirror
+  size_t aux_cap = 0;
+  int64_t launches = 0;
+  int num_sms = 148;
+  int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05
+};
+
+struct gpbo_model {
+  int S = 0;
+  int kernel = 0;
+  int device = 0;
+  int nmax = 0, dmax = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<SearchMeta> meta;  // host copy (after the fit)
+  SearchMeta *meta_d = nullptr;
+  char *block = nullptr;         // one cudaMallocAsync block, sub-allocated below
+  float *X32 = nullptr, *ls32 = nullptr, *Xs32 = nullptr, *LT32 = nullptr;
+  double *y64 = nullptr, *L64 = nullptr, *Linv64 = nullptr, *alpha64 = nullptr;
+  unsigned char *img = nullptr;  // tcgen05 operand images
+  int64_t img_bytes = 0;
+};
+
+namespace {
+
+gpbo_status fail(gpbo_ctx *ctx, gpbo_status st, const std::string &msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? GPBO_ENOMEM : GPBO_ECUDA,    \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+#define NK(x)                                                                         \
+  do {                                                                                \
+    ncclResult_t r_ = (x);                                                            \
+    if (r_ != ncclSuccess)                                                            \
+      return fail(ctx, GPBO_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));  \
+  } while (0)
+
+inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+gpbo_status ensure_stage(gpbo_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->stage_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->stage_d) CK(cudaFree(ctx->stage_d));
+  ctx->stage_d = nullptr;
+  ctx->stage_cap = 0;
+  CK(cudaMalloc(&ctx->stage_d, bytes));
+  ctx->stage_cap = bytes;
+  return GPBO_OK;
+}
+
+gpbo_status ensure_aux(gpbo_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->aux_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->aux_d) CK(cudaFree(ctx->aux_d));
+  if (ctx->aux_h) CK(cudaFreeHost(ctx->aux_h));
+  ctx->aux_d = ctx->aux_h = nullptr;
+  size_t cap = std::max<size_t>(bytes, 1 << 16);
+  CK(cudaMalloc(&ctx->aux_d, cap));
+  CK(cudaMallocHost(&ctx->aux_h, cap));
+  ctx->aux_cap = cap;
+  return GPBO_OK;
+}
+
+gpbo_status ensure_keys(gpbo_ctx *ctx, int S) {
+  if (S <= ctx->keys_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->keys_d) CK(cudaFree(ctx->keys_d));
+  if (ctx->keys_h) CK(cudaFreeHost(ctx->keys_h));
+  int cap = std::max(S, 64);
+  CK(cudaMalloc(&ctx->keys_d, cap * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&ctx->keys_h, cap * sizeof(unsigned long long)));
+  ctx->keys_cap = cap;
+  return GPBO_OK;
+}
+
+// Shared scoring launch used by gp_posterior and ei_score_argmax.
+gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S,
+                      const float *Xstar_dev, const int64_t *m_off, const int64_t *m_base,
+                      const double *best_std, float *out_mu, float *out_var, float *out_ei) {
+  // aux layout: m_off[S+1] i64 | m_base[S] i64 | x_off[S] i64 | best[S] f64 | tile_first[S+1] i32
+  const size_t bytes = (size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4;
+  gpbo_status st = ensure_aux(ctx, bytes + 64);
+  if (st) return st;
+  st = ensure_keys(ctx, S);
+  if (st) return st;
+  CK(cudaStreamSynchronize(ctx->stream));  // aux_h may still feed an earlier copy
+  char *h = (char *)ctx->aux_h;
+  int64_t *h_off = (int64_t *)h;
+  int64_t *h_base = h_off + (S + 1);
+  int64_t *h_xoff = h_base + S;
+  double *h_best = (double *)(h_xoff + S);
+  int32_t *h_tiles = (int32_t *)(h_best + S);
+  // pick the implementation: tcgen05 when every search fits its envelope
+  bool use_tc = ctx->score_impl != 1;
+  int nmax = 0, dmax = 0;
+  for (int i = 0; i < S; ++i) {
+    const SearchMeta &m = model->meta[s_first + i];
+    nmax = std::max(nmax, m.n);
+    dmax = std::max(dmax, m.d_pad);
+    if (!gpbo::tc_supported(m)) use_tc = false;
+  }
+  if (ctx->score_impl == 2 && !use_tc)
+    return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
+  const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;
+  h_tiles[0] = 0;
+  int64_t xo = 0;
+  for (int i = 0; i < S; ++i) {
+    h_xoff[i] = xo;
+    xo += (m_off[i + 1] - m_off[i]) * model->meta[s_first + i].d;
+    h_off[i] = m_off[i] - m_off[0];
+    h_base[i] = m_base ? m_base[i] : 0;
+    h_best[i] = best_std[i];
+    const int64_t Ms = m_off[i + 1] - m_off[i];
+    if (Ms < 0 || h_base[i] < 0 || h_base[i] + Ms >= 0xFFFFFFFFll)
+      return fail(ctx, GPBO_EINVAL, "candidate offsets out of range (M_s must be < 2^32-1)");
+    const int64_t t = (Ms + tile - 1) / tile;
+    if ((int64_t)h_tiles[i] + t > (1ll << 30))
+      return fail(ctx, GPBO_EINVAL, "too many candidates in one call");
+    h_tiles[i + 1] = h_tiles[i] + (int32_t)t;
+  }
+  h_off[S] = m_off[S] - m_off[0];
+  CK(cudaMemcpyAsync(ctx->aux_d, ctx->aux_h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->keys_d, 0, S * sizeof(unsigned long long), ctx->stream));
+  char *dptr = (char *)ctx->aux_d;
+  gpbo::ScoreLaunch p{};
+  p.meta = model->meta_d + s_first;
+  p.Xstar = Xstar_dev;
+  p.m_off = (const int64_t *)dptr;
+  p.m_base = p.m_off + (S + 1);
+  p.x_off = p.m_base + S;
+  p.best = (const double *)(p.x_off + S);
+  p.tile_first = (const int32_t *)(p.best + S);
+  p.S = S;
+  p.Xs32 = model->Xs32;
+  p.LT32 = model->LT32;
+  p.alpha64 = model->alpha64;
+  p.ls32 = model->ls32;
+  p.img = model->img;
+  p.keys = ctx->keys_d;
+  p.out_mu = out_mu;
+  p.out_var = out_var;
+  p.out_ei = out_ei;
+  const int tiles = h_tiles[S];
+  if (tiles > 0) {
+    if (use_tc)
+      CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
+    else
+      CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
+    ctx->launches += 1;
+  }
+  return GPBO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *gpbo_version(void) {
+  return "libgpbo 0.1 (sm_100a; fit fp64 1 CTA/search; score: tcgen05 fp16x3 + SIMT fallback)";
+}
+
+gpbo_status gpbo_nccl_unique_id(void *out) {
+  if (!out) return GPBO_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return GPBO_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return GPBO_OK;
+}
+
+gpbo_status gpbo_ctx_create(int device, void *cuda_stream, int nranks, int rank,
+                            const void *nccl_unique_id, gpbo_ctx **out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return GPBO_EINVAL;
+  if ((nranks > 1) != (nccl_unique_id != nullptr)) return GPBO_EINVAL;
+  *out = nullptr;
+  gpbo_ctx *ctx = new gpbo_ctx();
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return GPBO_ECUDA; }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess)
+    ctx->num_sms = sms;
+  // keep freed model blocks cached in the stream-ordered pool (no device-wide sync per fit)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (const char *e = getenv("GPBO_SCORE_IMPL")) {
+    if (!strcmp(e, "simt")) ctx->score_impl = 1;
+    if (!strcmp(e, "tc")) ctx->score_impl = 2;
+  }
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&ctx->comm, nranks, id, rank) != ncclSuccess) {
+      delete ctx;
+      return GPBO_ENCCL;
+    }
+  }
+  *out = ctx;
+  return GPBO_OK;
+}
+
+gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
+  if (!ctx) return GPBO_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->stage_d) cudaFree(ctx->stage_d);
+  if (ctx->aux_d) cudaFree(ctx->aux_d);
+  if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
+  if (ctx->keys_d) cudaFree(ctx->keys_d);
+  if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
+  delete ctx;
+  return GPBO_OK;
+}
+
+const char *gpbo_last_error(const gpbo_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int64_t gpbo_launch_count(const gpbo_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl) {
+  if (!ctx || impl < 0 || impl > 2) return GPBO_EINVAL;
+  ctx->score_impl = impl;
+  return GPBO_OK;
+}
+
+void gp_model_free(gpbo_model *model) {
+  if (!model) return;
+  cudaSetDevice(model->device);
+  if (model->block) cudaFreeAsync(model->block, model->stream);  // stream-ordered pool
+  delete model;
+}
+
+gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int32_t *status,
+                   int32_t *jitter_k) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!a || !out) return fail(ctx, GPBO_EINVAL, "null args/out");
+  *out = nullptr;
+  if (a->S < 1 || !a->n || !a->d || !a->X || !a->y || !a->lengthscale || !a->signal_var ||
+      !a->noise_var)
+    return fail(ctx, GPBO_EINVAL, "S < 1 or null input array");
+  if (a->kernel != GPBO_RBF && a->kernel != GPBO_MATERN52)
+    return fail(ctx, GPBO_EINVAL, "unknown kernel");
+  if (a->mem != GPBO_HOST && a->mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
+  CK(cudaSetDevice(ctx->device));
+  const int S = a->S;
+  gpbo_model *m = new gpbo_model();
+  m->S = S;
+  m->kernel = a->kernel;
+  m->device = ctx->device;
+  m->stream = ctx->stream;
+  m->meta.resize(S);
+  int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0;
+  int smem_max = 0;
+  for (int s = 0; s < S; ++s) {
+    const int n = a->n[s], d = a->d[s];
+    if (n < 1 || n > GPBO_MAX_N || d < 1 || d > GPBO_MAX_D) {
+      delete m;
+      return fail(ctx, GPBO_EINVAL, "n_s must be in [1, 512] and d_s in [1, 64]");
+    }
+    SearchMeta &q = m->meta[s];
+    std::memset(&q, 0, sizeof(q));
+    q.n = n;
+    q.d = d;
+    q.n_pad = (int)round_up(n, 64);
+    q.d_pad = (int)round_up(d, 8);
+    q.kernel = a->kernel;
+    q.x_off = nx; nx += (int64_t)n * d;
+    q.ls_off = nls; nls += d;
+    q.y_off = ny; ny += n;
+    q.mat_off = nmat; nmat += (int64_t)n * n;
+    q.xs_off = nxs; nxs += (int64_t)q.n_pad * q.d_pad;
+    q.lt_off = nlt; nlt += (int64_t)q.n_pad * q.n_pad;
+    q.a_off = na; na += q.n_pad;
+    q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
+    const int nr = (n + 1) & ~1;
+    q.use_smem = n <= gpbo::kFitSmemMaxN;
+    const int smem = (3 * nr + (q.use_smem ? n * n : 0)) * 8;
+    smem_max = std::max(smem_max, smem);
+    m->nmax = std::max(m->nmax, n);
+    m->dmax = std::max(m->dmax, q.d_pad);
+  }
+  // hyper-parameters into the meta records (read from host, or from device if mem == DEVICE)
+  std::vector<float> sf2(S), sn2(S);
+  if (a->mem == GPBO_HOST) {
+    std::memcpy(sf2.data(), a->signal_var, S * 4);
+    std::memcpy(sn2.data(), a->noise_var, S * 4);
+  } else {
+    cudaError_t e1 = cudaMemcpy(sf2.data(), a->signal_var, S * 4, cudaMemcpyDeviceToHost);
+    cudaError_t e2 = cudaMemcpy(sn2.data(), a->noise_var, S * 4, cudaMemcpyDeviceToHost);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      delete m;
+      return fail(ctx, GPBO_EINVAL, "signal_var/noise_var are not device pointers");
+    }
+  }
+  for (int s = 0; s < S; ++s) { m->meta[s].sf2 = sf2[s]; m->meta[s].sn2 = sn2[s]; }
+  // one device block: meta | X | ls | Xs | LT | y | L | Linv | alpha | img
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += round_up((int64_t)bytes, 256); return o; };
+  const size_t o_meta = take(sizeof(SearchMeta) * S * 2);
+  const size_t o_x = take(nx * 4), o_ls = take(nls * 4), o_xs = take(nxs * 4);
+  const size_t o_lt = take(nlt * 4), o_y = take(ny * 8), o_L = take(nmat * 8);
+  const size_t o_Li = take(nmat * 8), o_a = take(na * 8), o_img = take(nimg);
+  cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
+  if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
+  m->meta_d = (SearchMeta *)(m->block + o_meta);
+  SearchMeta *meta_in = m->meta_d + S;
+  m->X32 = (float *)(m->block + o_x);
+  m->ls32 = (float *)(m->block + o_ls);
+  m->Xs32 = (float *)(m->block + o_xs);
+  m->LT32 = (float *)(m->block + o_lt);
+  m->y64 = (double *)(m->block + o_y);
+  m->L64 = (double *)(m->block + o_L);
+  m->Linv64 = (double *)(m->block + o_Li);
+  m->alpha64 = (double *)(m->block + o_a);
+  m->img = (unsigned char *)(m->block + o_img);
+  m->img_bytes = nimg;
+  const cudaMemcpyKind kind = a->mem == GPBO_HOST ? cudaMemcpyHostToDevice
+                                                  : cudaMemcpyDeviceToDevice;
+  auto cleanup_fail = [&](gpbo_status st, const std::string &msg) {
+    cudaStreamSynchronize(ctx->stream);
+    gp_model_free(m);
+    return fail(ctx, st, msg);
+  };
+#define CKM(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return cleanup_fail(GPBO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+  CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
+  CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));
+  CKM(cudaMemcpyAsync(m->y64, a->y, ny * 8, kind, ctx->stream));
+  CKM(cudaMemcpyAsync(meta_in, m->meta.data(), sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
+                      ctx->stream));
+  CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
+                       m->Xs32, m->LT32, m->alpha64, m->meta_d, ctx->stream));
+  ctx->launches += 1;
+  if (nimg > 0) {
+    CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs32, m->alpha64, m->img,
+                             ctx->stream));
+    ctx->launches += 1;
+  }
+  CKM(cudaMemcpyAsync(m->meta.data(), m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
+                      ctx->stream));
+  CKM(cudaStreamSynchronize(ctx->stream));
+#undef CKM
+  gpbo_status worst = GPBO_OK;
+  bool einval = false;
+  for (int s = 0; s < S; ++s) {
+    const SearchMeta &q = m->meta[s];
+    if (status) status[s] = q.status;
+    if (jitter_k) jitter_k[s] = q.jitter_k;
+    if (q.status == GPBO_EINVAL) einval = true;
+    if (q.status == GPBO_ENOTPD) worst = GPBO_ENOTPD;
+    else if (q.status == GPBO_WDEGENERATE && worst == GPBO_OK) worst = GPBO_WDEGENERATE;
+  }
+  if (einval) {
+    gp_model_free(m);
+    return fail(ctx, GPBO_EINVAL, "non-finite or out-of-domain fit input");
+  }
+  *out = m;
+  if (worst == GPBO_ENOTPD) ctx->err = "Cholesky failed at the largest jitter for some search";
+  return worst;
+}
+
+gpbo_status gp_model_stats(const gpbo_model *model, int32_t s, double *mean, double *std,
+                           double *best, double *alpha_l1) {
+  if (!model || s < 0 || s >= model->S) return GPBO_EINVAL;
+  const SearchMeta &q = model->meta[s];
+  if (mean) *mean = q.mean;
+  if (std) *std = q.std;
+  if (best) *best = q.best;
+  if (alpha_l1) *alpha_l1 = q.alpha_l1;
+  return GPBO_OK;
+}
+
+gpbo_status gp_model_export(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, double *L,
+                            double *Linv, double *alpha) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model || s < 0 || s >= model->S) return fail(ctx, GPBO_EINVAL, "bad model/search");
+  CK(cudaSetDevice(ctx->device));
+  const SearchMeta &q = model->meta[s];
+  const int n = q.n;
+  std::vector<double> buf((size_t)n * n);
+  double *outs[2] = {L, Linv};
+  double *srcs[2] = {model->L64, model->Linv64};
+  for (int w = 0; w < 2; ++w) {
+    if (!outs[w]) continue;
+    CK(cudaMemcpyAsync(buf.data(), srcs[w] + q.mat_off, buf.size() * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < n; ++j)      // col-major device -> row-major caller
+      for (int i = 0; i < n; ++i) outs[w][(size_t)i * n + j] = buf[(size_t)j * n + i];
+  }
+  if (alpha) {
+    CK(cudaMemcpyAsync(alpha, model->alpha64 + q.a_off, n * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GPBO_OK;
+}
+
+gpbo_status gp_posterior(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, const float *Xstar,
+                         int64_t M, gpbo_mem mem, float *mu, float *var, float *ei) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model || s < 0 || s >= model->S || M < 0 || (M > 0 && !Xstar))
+    return fail(ctx, GPBO_EINVAL, "bad model/search/candidates");
+  if (mem != GPBO_HOST && mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
+  CK(cudaSetDevice(ctx->device));
+  const SearchMeta &q = model->meta[s];
+  if (q.status != GPBO_OK && q.status != GPBO_WDEGENERATE)
+    return fail(ctx, GPBO_ENOTPD, "search has no valid fit");
+  if (M == 0) return GPBO_OK;
+  const float *xd = Xstar;
+  float *omu = mu, *ovar = var, *oei = ei;
+  if (mem == GPBO_HOST) {
+    const size_t xb = (size_t)M * q.d * 4, ob = (size_t)M * 4;
+    gpbo_status st = ensure_stage(ctx, xb + 3 * ob + 1024);
+    if (st) return st;
+    char *b = (char *)ctx->stage_d;
+    CK(cudaMemcpyAsync(b, Xstar, xb, cudaMemcpyHostToDevice, ctx->stream));
+    xd = (const float *)b;
+    char *ob0 = b + round_up(xb, 256);
+    omu = mu ? (float *)ob0 : nullptr;
+    ovar = var ? (float *)(ob0 + round_up(ob, 256)) : nullptr;
+    oei = ei ? (float *)(ob0 + 2 * round_up(ob, 256)) : nullptr;
+  }
+  const int64_t off[2] = {0, M};
+  const double best = q.best;
+  gpbo_status st = run_score(ctx, model, s, 1, xd, off, nullptr, &best, omu, ovar, oei);
+  if (st) return st;
+  if (mem == GPBO_HOST) {
+    if (mu) CK(cudaMemcpyAsync(mu, omu, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (var) CK(cudaMemcpyAsync(var, ovar, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ei) CK(cudaMemcpyAsync(ei, oei, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return GPBO_OK;
+}
+
+gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float *Xstar,
+                            const int64_t *m_off, const int64_t *m_global_base,
+                            const double *best, gpbo_mem mem, int64_t *idx, float *ei) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model || !m_off) return fail(ctx, GPBO_EINVAL, "null model/m_off");
+  if (mem != GPBO_HOST && mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
+  CK(cudaSetDevice(ctx->device));
+  const int S = model->S;
+  std::vector<double> best_std(S);
+  int64_t rows = 0, floats = 0;
+  for (int s = 0; s < S; ++s) {
+    const SearchMeta &q = model->meta[s];
+    best_std[s] = best ? (best[s] - q.mean) / q.std : q.best;
+    const int64_t Ms = m_off[s + 1] - m_off[s];
+    if (Ms < 0) return fail(ctx, GPBO_EINVAL, "m_off must be non-decreasing");
+    rows += Ms;
+    floats += Ms * q.d;
+  }
+  if (rows > 0 && !Xstar) return fail(ctx, GPBO_EINVAL, "null Xstar");
+  // rows of search s start at element sum_{t<s} (m_off[t+1] - m_off[t]) d_t of Xstar
+  const float *xd = Xstar;
+  if (mem == GPBO_HOST && floats > 0) {
+    gpbo_status st = ensure_stage(ctx, (size_t)floats * 4);
+    if (st) return st;
+    CK(cudaMemcpyAsync(ctx->stage_d, xd, (size_t)floats * 4, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    xd = (const float *)ctx->stage_d;
+  }
+  gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_global_base, best_std.data(),
+                             nullptr, nullptr, nullptr);
+  if (st) return st;
+  if (ctx->nranks > 1)
+    NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->keys_h, ctx->keys_d, S * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  for (int s = 0; s < S; ++s) {
+    const unsigned long long k = ctx->keys_h[s];
+    const SearchMeta &q = model->meta[s];
+    if (k == 0ull) {
+      if (idx) idx[s] = -1;
+      if (ei) ei[s] = 0.f;
+      continue;
+    }
+    const uint32_t lo = (uint32_t)(k & 0xFFFFFFFFull);
+    const uint32_t bits = (uint32_t)(k >> 32);
+    float e;
+    std::memcpy(&e, &bits, 4);
+    if (idx) idx[s] = (int64_t)(0xFFFFFFFFu - lo);
+    if (ei) ei[s] = (float)(q.std * (double)e);
+  }
+  return GPBO_OK;
+}
+
+}  // extern "C"

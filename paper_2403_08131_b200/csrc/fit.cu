@@ -1,0 +1,234 @@
+// H1-H4 of the hot path: standardise y, Gram matrix, jittered Cholesky,
+// triangular inverse, alpha -- one CTA per sub-search, float64 throughout.
+//
+// PAPER.md L249/L256 (§IV.D): the GP's "O(N^3) training complexity" is this factorisation.
+// The kernel/jitter/standardisation readings are R1, R2, R7, R9 of DESIGN.md.
+//
+// Layout: the working matrix A is n x n float64, column-major (column j contiguous), lower
+// triangle used.  For n <= kFitSmemMaxN it lives in shared memory; otherwise the CTA works in
+// place in the model's global Linv64 buffer (L2 resident).  All accesses go through generic
+// pointers, so the same code serves both cases.
+#include <cmath>
+
+#include "gpbo_internal.cuh"
+
+namespace gpbo {
+namespace {
+
+constexpr int kWarps = kFitThreads / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reductions (fixed tree order).
+template <class Op>
+__device__ double block_reduce(double v, double *red, Op op) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = red[lane < kWarps ? lane : 0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = op(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+struct AddOp { __device__ double operator()(double a, double b) const { return a + b; } };
+struct MaxOp { __device__ double operator()(double a, double b) const { return fmax(a, b); } };
+struct MinOp { __device__ double operator()(double a, double b) const { return fmin(a, b); } };
+
+__device__ __forceinline__ double kernel_value(double r2, double sf2, int kind) {
+  if (kind == GPBO_RBF) return sf2 * exp(-0.5 * r2);
+  const double r = sqrt(r2);
+  const double s5 = 2.23606797749978969640917366873;  // sqrt(5)
+  return sf2 * (1.0 + s5 * r + (5.0 / 3.0) * r2) * exp(-s5 * r);
+}
+
+__global__ void __launch_bounds__(kFitThreads, 1)
+fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
+           const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
+           double *Linv64, float *Xs32, float *LT32, double *alpha64,
+           SearchMeta *__restrict__ meta_out) {
+  extern __shared__ double sm[];
+  __shared__ double red[33];
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  SearchMeta m = meta_in[s];
+  const int n = m.n, d = m.d;
+  const int nr = (n + 1) & ~1;
+  double *yt = sm;
+  double *tmp = sm + nr;
+  double *w = sm + 2 * nr;
+  double *A = m.use_smem ? sm + 3 * nr : Linv64 + m.mat_off;
+  const float *X = X32 + m.x_off;
+  const float *ls = ls32 + m.ls_off;
+  const double *y = y64 + m.y_off;
+
+  // ---- input validation (GPBO_EINVAL on any non-finite / out-of-domain value)
+  int bad = 0;
+  for (int i = tid; i < n * d; i += kFitThreads) bad |= !isfinite(X[i]);
+  for (int i = tid; i < n; i += kFitThreads) bad |= !isfinite(y[i]);
+  for (int i = tid; i < d; i += kFitThreads) bad |= !(ls[i] > 0.f) || !isfinite(ls[i]);
+  bad |= !(m.sf2 > 0.f) || !isfinite(m.sf2) || !(m.sn2 >= 0.f) || !isfinite(m.sn2);
+  bad = __syncthreads_or(bad);
+  if (bad) {
+    if (tid == 0) { m.status = GPBO_EINVAL; m.jitter_k = -1; meta_out[s] = m; }
+    return;
+  }
+
+  // ---- H1: y~ = (y - mean) / std, ddof = 0 (reading R7); degenerate -> y~ = 0, std = 1
+  double acc = 0.0, amax = 0.0;
+  for (int i = tid; i < n; i += kFitThreads) { acc += y[i]; amax = fmax(amax, fabs(y[i])); }
+  const double mean = block_reduce(acc, red, AddOp()) / n;
+  amax = block_reduce(amax, red, MaxOp());
+  acc = 0.0;
+  for (int i = tid; i < n; i += kFitThreads) { const double t = y[i] - mean; acc += t * t; }
+  double stdv = sqrt(block_reduce(acc, red, AddOp()) / n);
+  const bool degenerate = !(stdv > 1e-12 * amax);
+  if (degenerate) stdv = 1.0;
+  double bmin = INFINITY;
+  for (int i = tid; i < n; i += kFitThreads) {
+    const double t = degenerate ? 0.0 : (y[i] - mean) / stdv;
+    yt[i] = t;
+    bmin = fmin(bmin, t);
+  }
+  const double best = block_reduce(bmin, red, MinOp());
+
+  // ---- scoring operand: X / l in float32 (IEEE division), zero padded to n_pad x d_pad
+  for (int e = tid; e < m.n_pad * m.d_pad; e += kFitThreads) {
+    const int i = e / m.d_pad, c = e - i * m.d_pad;
+    Xs32[m.xs_off + e] = (i < n && c < d) ? __fdiv_rn(X[i * d + c], ls[c]) : 0.f;
+  }
+
+  // ---- H2 + H3: Gram matrix and Cholesky with the jitter ladder j_k = 1e-8 10^k sf2
+  const double sf2 = m.sf2, sn2 = m.sn2;
+  int jk = -1;
+  double jit = 0.0;
+  double p10 = 1.0;
+  for (int k = 0; k < 7; ++k, p10 *= 10.0) {
+    jit = 1e-8 * p10 * sf2;
+    __syncthreads();
+    for (int j = warp; j < n; j += kWarps) {
+      for (int i = j + lane; i < n; i += 32) {
+        double r2 = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double li = (double)ls[c];
+          const double diff = (double)X[i * d + c] / li - (double)X[j * d + c] / li;
+          r2 += diff * diff;
+        }
+        double v = kernel_value(r2, sf2, m.kernel);
+        if (i == j) v += sn2 + jit;
+        A[(size_t)j * n + i] = v;
+      }
+    }
+    // right-looking column Cholesky, in place, lower triangle
+    bool ok = true;
+    for (int c = 0; c < n; ++c) {
+      __syncthreads();
+      const double p = A[(size_t)c * n + c];
+      if (!(p > 0.0) || !isfinite(p)) { ok = false; break; }  // uniform across the CTA
+      const double lcc = sqrt(p);
+      for (int i = c + 1 + tid; i < n; i += kFitThreads) A[(size_t)c * n + i] /= lcc;
+      __syncthreads();
+      if (tid == 0) A[(size_t)c * n + c] = lcc;
+      for (int j = c + 1 + warp; j < n; j += kWarps) {
+        const double ljc = A[(size_t)c * n + j];
+        for (int i = j + lane; i < n; i += 32) A[(size_t)j * n + i] -= A[(size_t)c * n + i] * ljc;
+      }
+    }
+    if (ok) { jk = k; break; }
+  }
+  __syncthreads();
+  if (jk < 0) {
+    if (tid == 0) {
+      m.status = GPBO_ENOTPD; m.jitter_k = -1; m.jitter = NAN;
+      m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = 0.0;
+      meta_out[s] = m;
+    }
+    return;
+  }
+  // keep L (col-major) for diagnostics
+  for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
+    const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
+    L64[m.mat_off + e] = (i >= j) ? A[e] : 0.0;
+  }
+
+  // ---- H4: in-place inverse of the lower-triangular factor (column sweep, right to left)
+  for (int j = n - 1; j >= 0; --j) {
+    __syncthreads();
+    const double dinv = 1.0 / A[(size_t)j * n + j];
+    for (int i = j + 1 + tid; i < n; i += kFitThreads) tmp[i] = A[(size_t)j * n + i];
+    __syncthreads();
+    if (tid == 0) A[(size_t)j * n + j] = dinv;
+    for (int i = j + 1 + tid; i < n; i += kFitThreads) {
+      double acc2 = 0.0;
+      for (int k = j + 1; k <= i; ++k) acc2 += A[(size_t)k * n + i] * tmp[k];
+      A[(size_t)j * n + i] = -dinv * acc2;
+    }
+  }
+  __syncthreads();
+  // w = L^-1 y~
+  for (int i = tid; i < n; i += kFitThreads) {
+    double a2 = 0.0;
+    for (int k = 0; k <= i; ++k) a2 += A[(size_t)k * n + i] * yt[k];
+    w[i] = a2;
+  }
+  __syncthreads();
+  // alpha = L^-T w  (warp per k, lanes over i >= k)
+  double l1 = 0.0;
+  for (int k = warp; k < m.n_pad; k += kWarps) {
+    double a2 = 0.0;
+    if (k < n)
+      for (int i = k + lane; i < n; i += 32) a2 += A[(size_t)k * n + i] * w[i];
+    a2 = warp_sum(a2);
+    if (lane == 0) { alpha64[m.a_off + k] = a2; l1 += fabs(a2); }
+  }
+  l1 = block_reduce(l1, red, AddOp());
+  // write L^-1 (col-major) and the float32 (L^-1)^T scoring operand: LT[k][j] = Linv[j][k]
+  if (m.use_smem)
+    for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
+      const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
+      Linv64[m.mat_off + e] = (i >= j) ? A[e] : 0.0;
+    }
+  else
+    for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
+      const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
+      if (i < j) A[e] = 0.0;
+    }
+  for (size_t e = tid; e < (size_t)m.n_pad * m.n_pad; e += kFitThreads) {
+    const int k = (int)(e / m.n_pad), j = (int)(e - (size_t)k * m.n_pad);
+    LT32[m.lt_off + e] = (k < n && j < n && j >= k) ? (float)A[(size_t)k * n + j] : 0.f;
+  }
+  if (tid == 0) {
+    m.status = degenerate ? GPBO_WDEGENERATE : GPBO_OK;
+    m.jitter_k = jk; m.jitter = jit;
+    m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = l1;
+    meta_out[s] = m;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
+                       const float *ls32, const double *y64, double *L64, double *Linv64,
+                       float *Xs32, float *LT32, double *alpha64, SearchMeta *meta_out,
+                       cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes);
+  if (e != cudaSuccess) return e;
+  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, X32, ls32, y64, L64, Linv64, Xs32,
+                                                     LT32, alpha64, meta_out);
+  return cudaGetLastError();
+}
+
+}  // namespace gpbo

@@ -1,0 +1,69 @@
+// Internal device/host definitions shared by the libgpbo CUDA translation units.
+// Nothing here is shared with oracle/ (the oracle is independent Python).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gpbo.h"
+
+namespace gpbo {
+
+constexpr int kFitThreads = 512;
+constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
+// Largest n whose full n x n float64 matrix (+3 n-vectors) the fit keeps in shared memory.
+constexpr int kFitSmemMaxN = 160;
+
+// Per-search state of a fitted model (device copy in gpbo_model::meta_d, host copy in meta_h).
+struct SearchMeta {
+  int32_t n, d;         // observations, encoded dims
+  int32_t n_pad, d_pad; // n rounded up to 64 (scoring operand), d rounded up to 8
+  int32_t kernel;       // gpbo_kernel
+  float sf2, sn2;       // signal / noise variance (standardised units)
+  int64_t x_off;        // raw X  (float32, n x d)            into model.X32
+  int64_t ls_off;       // lengthscales (float32, d)          into model.ls32
+  int64_t y_off;        // y (float64, n)                     into model.y64
+  int64_t mat_off;      // n x n float64 col-major            into model.L64 / model.Linv64
+  int64_t xs_off;       // X/l (float32, n_pad x d_pad)       into model.Xs32
+  int64_t lt_off;       // (L^-1)^T float32 n_pad x n_pad      into model.LT32
+  int64_t a_off;        // alpha (n_pad)                      into model.alpha64
+  int64_t img_off;      // tcgen05 operand image (bytes)      into model.img
+  // fit results
+  double mean, std, best, alpha_l1;
+  double jitter;
+  int32_t jitter_k;
+  int32_t status;       // gpbo_status of this search
+  int32_t use_smem;     // fit keeps its matrix in shared memory
+  int32_t pad_;
+};
+
+// One scoring launch covers several searches; tile t of the launch belongs to search
+// tile_search[t], local tile index t - tile_first[search].
+struct ScoreLaunch {
+  const SearchMeta *meta;
+  const float *Xstar;          // concatenated candidate rows
+  const int64_t *m_off;        // [S+1] candidate row offsets (device copy)
+  const int64_t *m_base;       // [S] global index of the first local row
+  const int64_t *x_off;        // [S] element offset of search s's first row in Xstar
+  const double *best;          // [S] standardised incumbent
+  const int32_t *tile_first;   // [S+1] prefix sums of tiles per search
+  int32_t S;
+  const float *Xs32;
+  const float *LT32;
+  const double *alpha64;
+  const float *ls32;
+  const unsigned char *img;    // tcgen05 operand images
+  unsigned long long *keys;    // [S] per-search argmax keys (atomicMax)
+  float *out_mu, *out_var, *out_ei;  // optional per-candidate outputs (raw units)
+};
+
+}  // namespace gpbo
+
+// Kernel launchers (defined in the .cu files).
+namespace gpbo {
+cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
+                       const float *ls32, const double *y64, double *L64, double *Linv64,
+                       float *Xs32, float *LT32, double *alpha64, SearchMeta *meta_out,
+                       cudaStream_t stream);
+cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, int nmax,
+                              cudaStream_t stream);
+}  // namespace gpbo

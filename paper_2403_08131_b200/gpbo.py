@@ -1,0 +1,246 @@
+"""Thin ctypes binding of libgpbo.so (include/gpbo.h).  Argument marshalling only.
+
+Every numerical step runs in the library's CUDA kernels; there is no Python or CPU fallback.
+Arrays may be numpy arrays (host memory -> GPBO_HOST) or CUDA torch tensors (-> GPBO_DEVICE);
+all arrays of one call must live in the same space.  Names follow include/gpbo.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpbo.so")
+
+OK, EINVAL, ENOTPD, WDEGENERATE, ESAMPLING, ECUDA, ENCCL, ENOMEM, ENOTSUP = range(9)
+RBF, MATERN52 = 0, 1
+HOST, DEVICE = 0, 1
+STATUS_NAMES = ["OK", "EINVAL", "ENOTPD", "WDEGENERATE", "ESAMPLING", "ECUDA", "ENCCL",
+                "ENOMEM", "ENOTSUP"]
+NCCL_ID_BYTES = 128
+
+
+class GpboError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 9 else status}: {msg}")
+        self.status = status
+
+
+class FitArgs(C.Structure):
+    _fields_ = [("S", C.c_int32), ("n", C.c_void_p), ("d", C.c_void_p), ("X", C.c_void_p),
+                ("y", C.c_void_p), ("lengthscale", C.c_void_p), ("signal_var", C.c_void_p),
+                ("noise_var", C.c_void_p), ("kernel", C.c_int), ("mem", C.c_int)]
+
+
+_lib = None
+
+
+def load():
+    """Load the in-tree libgpbo.so; fails loudly when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "gpbo_nccl_unique_id": (C.c_int, [vp]),
+        "gpbo_ctx_create": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+        "gpbo_ctx_destroy": (C.c_int, [vp]),
+        "gpbo_last_error": (C.c_char_p, [vp]),
+        "gpbo_version": (C.c_char_p, []),
+        "gp_fit": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(vp), vp, vp]),
+        "gp_model_free": (None, [vp]),
+        "gp_model_stats": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "gp_model_export": (C.c_int, [vp, vp, i32, vp, vp, vp]),
+        "gp_posterior": (C.c_int, [vp, vp, i32, vp, i64, C.c_int, vp, vp, vp]),
+        "ei_score_argmax": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
+        "gpbo_launch_count": (i64, [vp]),
+        "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Names of the entry points include/gpbo.h declares (for the load/export test)."""
+    return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
+            "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
+            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl"]
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a, dtype):
+    """(address, mem) of a contiguous array of the given numpy dtype; None -> (None, None)."""
+    if a is None:
+        return None, None
+    if _is_torch(a):
+        import torch
+        want = {np.float32: torch.float32, np.float64: torch.float64,
+                np.int64: torch.int64, np.int32: torch.int32}[dtype]
+        if a.dtype != want or not a.is_contiguous():
+            raise TypeError(f"tensor must be contiguous {want}")
+        return a.data_ptr(), (DEVICE if a.is_cuda else HOST)
+    if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+        raise TypeError(f"array must be a C-contiguous numpy {np.dtype(dtype)}")
+    return a.ctypes.data, HOST
+
+
+def _mem_of(*pairs):
+    mems = {m for _, m in pairs if m is not None}
+    if len(mems) > 1:
+        raise TypeError("all arrays of one call must be host or all device")
+    return mems.pop() if mems else HOST
+
+
+class Model:
+    def __init__(self, ctx, handle, S, n, d, status, jitter_k):
+        self.ctx, self.handle, self.S = ctx, handle, S
+        self.n, self.d = list(n), list(d)
+        self.status, self.jitter_k = status, jitter_k
+
+    def stats(self, s):
+        lib = load()
+        vals = [C.c_double() for _ in range(4)]
+        _check(self.ctx, lib.gp_model_stats(self.handle, s, *[C.byref(v) for v in vals]))
+        return dict(zip(("mean", "std", "best", "alpha_l1"), (v.value for v in vals)))
+
+    def export(self, s):
+        """float64 (L, L^-1, alpha) of search s (row-major lower triangles)."""
+        n = self.n[s]
+        L = np.zeros((n, n))
+        Li = np.zeros((n, n))
+        a = np.zeros(n)
+        _check(self.ctx, load().gp_model_export(self.ctx.handle, self.handle, s, L.ctypes.data,
+                                                Li.ctypes.data, a.ctypes.data))
+        return L, Li, a
+
+    def free(self):
+        if self.handle:
+            load().gp_model_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _check(ctx, st, ok=(OK,)):
+    if st not in ok:
+        msg = load().gpbo_last_error(ctx.handle if ctx is not None else None)
+        raise GpboError(st, msg.decode() if msg else "")
+    return st
+
+
+def nccl_unique_id():
+    buf = (C.c_char * NCCL_ID_BYTES)()
+    st = load().gpbo_nccl_unique_id(C.addressof(buf))
+    if st != OK:
+        raise GpboError(st, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+class Context:
+    """gpbo_ctx: one per (rank, device, stream)."""
+
+    def __init__(self, device=0, stream=None, nranks=1, rank=0, nccl_id=None):
+        lib = load()
+        h = C.c_void_p()
+        sp = None
+        if stream is not None:
+            sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_char * NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+        st = lib.gpbo_ctx_create(device, sp, nranks, rank,
+                                 C.addressof(idbuf) if idbuf is not None else None, C.byref(h))
+        if st != OK:
+            raise GpboError(st, "gpbo_ctx_create failed")
+        self.handle = h
+        self.device, self.nranks, self.rank = device, nranks, rank
+
+    def close(self):
+        if self.handle:
+            load().gpbo_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self):
+        return int(load().gpbo_launch_count(self.handle))
+
+    def set_score_impl(self, impl):
+        """0 auto, 1 CUDA-core, 2 tcgen05 (see include/gpbo.h)."""
+        _check(self, load().gpbo_set_score_impl(self.handle, int(impl)))
+
+    def fit(self, n, d, X, y, lengthscale, signal_var, noise_var, kernel=MATERN52):
+        """gp_fit over a ragged batch; returns a Model (status per search in model.status)."""
+        lib = load()
+        S = len(n)
+        n_a = np.ascontiguousarray(n, dtype=np.int32)
+        d_a = np.ascontiguousarray(d, dtype=np.int32)
+        ptrs = [_ptr(X, np.float32), _ptr(y, np.float64), _ptr(lengthscale, np.float32),
+                _ptr(signal_var, np.float32), _ptr(noise_var, np.float32)]
+        mem = _mem_of(*ptrs)
+        args = FitArgs(S, n_a.ctypes.data, d_a.ctypes.data, ptrs[0][0], ptrs[1][0], ptrs[2][0],
+                       ptrs[3][0], ptrs[4][0], int(kernel), mem)
+        h = C.c_void_p()
+        status = np.zeros(S, np.int32)
+        jk = np.zeros(S, np.int32)
+        st = lib.gp_fit(self.handle, C.byref(args), C.byref(h), status.ctypes.data,
+                        jk.ctypes.data)
+        _check(self, st, ok=(OK, ENOTPD, WDEGENERATE))
+        return Model(self, h, S, n_a, d_a, status, jk)
+
+    def posterior(self, model, s, Xstar, want=("mu", "var", "ei")):
+        """gp_posterior: raw-unit (mu, var, ei) for every row of X* (same space as X*)."""
+        px, mem = _ptr(Xstar, np.float32)
+        M = int(Xstar.shape[0])
+        outs = []
+        for name in ("mu", "var", "ei"):
+            if name not in want:
+                outs.append(None)
+            elif _is_torch(Xstar):
+                import torch
+                outs.append(torch.empty(M, dtype=torch.float32, device=Xstar.device))
+            else:
+                outs.append(np.empty(M, np.float32))
+        op = [(_ptr(o, np.float32)[0] if o is not None else None) for o in outs]
+        _check(self, load().gp_posterior(self.handle, model.handle, s, px, M, mem, *op))
+        return tuple(outs)
+
+    def score_argmax(self, model, Xstar, m_off, m_global_base=None, best=None):
+        """ei_score_argmax -> (idx int64[S], ei float32[S] raw units)."""
+        px, mem = _ptr(Xstar, np.float32)
+        off = np.ascontiguousarray(m_off, dtype=np.int64)
+        base = None if m_global_base is None else np.ascontiguousarray(m_global_base, np.int64)
+        b = None if best is None else np.ascontiguousarray(best, np.float64)
+        idx = np.zeros(model.S, np.int64)
+        ei = np.zeros(model.S, np.float32)
+        _check(self, load().ei_score_argmax(
+            self.handle, model.handle, px, off.ctypes.data,
+            base.ctypes.data if base is not None else None,
+            b.ctypes.data if b is not None else None, mem, idx.ctypes.data, ei.ctypes.data))
+        return idx, ei
+
+
+def version():
+    return load().gpbo_version().decode()

@@ -1,0 +1,211 @@
+"""GPU parity: libgpbo (through the C ABI) against the float64 oracle on seeded inputs.
+
+Tolerances and the argmax rule are the readings T1 / R11 in tests/helpers.py.
+"""
+import numpy as np
+import pytest
+
+from oracle import gp
+from tests import helpers as H
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_08131_b200 import gpbo
+    ctx = gpbo.Context(device=0)
+    yield gpbo, ctx
+    ctx.close()
+
+
+def _fit(G, w):
+    gpbo, ctx = G
+    return ctx.fit(*H.pack(w), kernel=w.kernel)
+
+
+IMPLS = [0, 1]  # auto (tcgen05 where supported), CUDA-core
+
+
+# ------------------------------------------------------------------ fit (H1-H4)
+@pytest.mark.parametrize("n,d", [(1, 1), (2, 3), (16, 2), (17, 5), (33, 8), (100, 5), (160, 20),
+                                 (161, 9), (200, 20), (255, 35), (500, 60)])
+@pytest.mark.parametrize("kernel", [gp.MATERN52, gp.RBF])
+def test_fit_matches_oracle(G, n, d, kernel):
+    w = gen.random_case(n * 7 + d, n, d, 4, kernel=kernel)
+    m = _fit(G, w)
+    om = H.oracle_fits(w)[0]
+    assert m.status[0] in (0, 3) and m.jitter_k[0] == om.jitter_k
+    L, Li, a = m.export(0)
+    st = m.stats(0)
+    assert abs(st["mean"] - om.mean) <= 1e-12 * max(1, abs(om.mean))
+    assert abs(st["std"] - om.std) <= 1e-12 * om.std
+    assert abs(st["best"] - om.best) <= 1e-12 * max(1, abs(om.best))
+    np.testing.assert_allclose(L, om.L, rtol=0, atol=1e-12 * np.abs(om.L).max())
+    Li_ref = np.linalg.inv(om.L)  # LAPACK inverse of the oracle's factor
+    np.testing.assert_allclose(Li, Li_ref, rtol=0, atol=1e-9 * np.abs(Li_ref).max())
+    np.testing.assert_allclose(a, om.alpha, rtol=0, atol=1e-7 * np.abs(om.alpha).max())
+
+
+def test_fit_jitter_escalation_and_failures(G):
+    gpbo, ctx = G
+    rng = np.random.default_rng(0)
+    X = np.repeat(rng.random((6, 2)).astype(np.float32), 3, axis=0)
+    y = rng.standard_normal(18)
+    ls = np.array([0.3, 0.4], np.float32)
+    m = ctx.fit([18], [2], X.ravel().copy(), y, ls, np.ones(1, np.float32),
+                np.zeros(1, np.float32), kernel=gp.RBF)
+    om = gp.fit(X, y, ls, 1.0, 0.0, gp.RBF)
+    assert m.jitter_k[0] == om.jitter_k > 0
+    # no jitter can repair a negative noise variance -> rejected up front (EINVAL)
+    with pytest.raises(gpbo.GpboError) as e:
+        ctx.fit([3], [1], np.zeros(3, np.float32), np.arange(3.0), np.ones(1, np.float32),
+                np.ones(1, np.float32), -np.ones(1, np.float32))
+    assert e.value.status == gpbo.EINVAL
+    y2 = y.copy()
+    y2[3] = np.nan
+    with pytest.raises(gpbo.GpboError) as e:
+        ctx.fit([18], [2], X.ravel().copy(), y2, ls, np.ones(1, np.float32),
+                np.full(1, 1e-4, np.float32))
+    assert e.value.status == gpbo.EINVAL
+
+
+def test_fit_degenerate(G):
+    gpbo, ctx = G
+    w = gen.random_case(3, 12, 2, 300)
+    w.searches[0].y[:] = 4.2
+    m = _fit(G, w)
+    assert m.status[0] == gpbo.WDEGENERATE
+    om = H.oracle_fits(w)[0]
+    res = gp.score(om, w.Xstar[0])
+    mu, var, ei = ctx_post(G, m, 0, w.Xstar[0])
+    H.check_T1(om, res, mu, var, ei, "degenerate")
+
+
+def ctx_post(G, m, s, Xs):
+    gpbo, ctx = G
+    return ctx.posterior(m, s, np.ascontiguousarray(Xs))
+
+
+# ------------------------------------------------------------------ posterior (H6-H8)
+CASES = [
+    ("cfg1", lambda: gen.make(1)),
+    ("cfg1_rbf", lambda: gen.make(1, kernel=gp.RBF)),
+    ("cfg2", lambda: gen.make(2, M=8192)),
+    ("cfg3", lambda: gen.make(3, S=8, M=2048)),
+    ("cfg4", lambda: gen.make(4, M=2048)),
+    ("n2", lambda: gen.random_case(1, 2, 3, 777)),
+    ("n17_d9", lambda: gen.random_case(2, 17, 9, 1000)),
+    ("n129_d33", lambda: gen.random_case(4, 129, 33, 1000)),
+    ("n255_d64", lambda: gen.random_case(5, 255, 64, 600)),
+    ("n511_d20", lambda: gen.random_case(6, 511, 20, 400)),
+]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+def test_posterior_matches_oracle(G, name, make, impl):
+    gpbo, ctx = G
+    ctx.set_score_impl(impl)
+    try:
+        w = make()
+        m = _fit(G, w)
+        oms = H.oracle_fits(w)
+        for s in range(w.S):
+            res = gp.score(oms[s], w.Xstar[s])
+            mu, var, ei = ctx.posterior(m, s, w.Xstar[s])
+            H.check_T1(oms[s], res, mu, var, ei, f"{name}[{s}]")
+    finally:
+        ctx.set_score_impl(0)
+
+
+# ------------------------------------------------------------------ argmax (H9)
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("name,make", [
+    ("cfg1", lambda: gen.make(1)),
+    ("cfg2", lambda: gen.make(2, M=65536)),
+    ("cfg3", lambda: gen.make(3, M=4096)),
+    ("ragged", lambda: gen.random_case(9, [5, 64, 130], [3, 3, 3], [1, 129, 1000])),
+    ("ragged_d", lambda: gen.random_case(10, [40, 7, 90], [2, 11, 5], [300, 64, 65])),
+], ids=["cfg1", "cfg2", "cfg3", "ragged", "ragged_d"])
+def test_argmax_matches_oracle(G, name, make, impl):
+    gpbo, ctx = G
+    ctx.set_score_impl(impl)
+    try:
+        w = make()
+        m = _fit(G, w)
+        Xs, off = H.pack_candidates(w)
+        idx, ei = ctx.score_argmax(m, Xs, off)
+        oms = H.oracle_fits(w)
+        for s in range(w.S):
+            res = gp.score(oms[s], w.Xstar[s])
+            H.check_argmax(res, int(idx[s]), f"{name}[{s}]")
+            assert abs(ei[s] / oms[s].std - res.ei) <= H.TOL * res.ei + 1e-30
+    finally:
+        ctx.set_score_impl(0)
+
+
+def test_exact_tie_resolves_to_lowest_global_index(G):
+    """R10 / S:L407: identical candidates tie bit-exactly; the lowest global index wins."""
+    gpbo, ctx = G
+    w = gen.random_case(11, 30, 4, 500)
+    m = _fit(G, w)
+    Xs = w.Xstar[0].copy()
+    om = H.oracle_fits(w)[0]
+    best = gp.score(om, Xs).idx
+    Xs[400] = Xs[best]   # a later duplicate of the maximiser
+    Xs[best // 2] = Xs[best]  # an earlier duplicate
+    idx, _ = ctx.score_argmax(m, np.ascontiguousarray(Xs), [0, 500])
+    assert idx[0] == best // 2
+
+
+def test_sharded_scoring_is_bit_identical(G):
+    """P13 (G-shard simulator): scoring contiguous shards separately with their global bases and
+    taking the host-side max of (EI, -idx) reproduces the unsharded result bit-exactly."""
+    gpbo, ctx = G
+    w = gen.make(2, M=20000)
+    m = _fit(G, w)
+    Xs = w.Xstar[0]
+    idx0, ei0 = ctx.score_argmax(m, Xs, [0, 20000])
+    for shards in (2, 3, 8):
+        per = -(-20000 // shards)
+        picks = []
+        for r in range(shards):
+            a, b = r * per, min(20000, (r + 1) * per)
+            i, e = ctx.score_argmax(m, np.ascontiguousarray(Xs[a:b]), [0, b - a], [a])
+            picks.append((e[0], -i[0]))
+        e, negi = max(picks)
+        assert -negi == idx0[0] and e == ei0[0]
+
+
+def test_device_and_host_memory_agree(G):
+    import torch
+    gpbo, ctx = G
+    w = gen.make(3, S=4, M=1000)
+    n, d, X, y, ls, sf2, sn2 = H.pack(w)
+    mh = ctx.fit(n, d, X, y, ls, sf2, sn2)
+    t = lambda a: torch.from_numpy(a).cuda()
+    md = ctx.fit(n, d, t(X), t(y), t(ls), t(sf2), t(sn2))
+    Xs, off = H.pack_candidates(w)
+    ih, eh = ctx.score_argmax(mh, Xs, off)
+    idv, edv = ctx.score_argmax(md, t(Xs), off)
+    assert np.array_equal(ih, idv) and np.array_equal(eh, edv)
+    mu_h, var_h, ei_h = ctx.posterior(mh, 1, w.Xstar[1])
+    mu_d, var_d, ei_d = ctx.posterior(md, 1, t(w.Xstar[1]))
+    assert np.array_equal(mu_h, mu_d.cpu().numpy()) and np.array_equal(ei_h, ei_d.cpu().numpy())
+
+
+def test_nan_candidate_is_never_chosen(G):
+    gpbo, ctx = G
+    w = gen.random_case(12, 20, 3, 256)
+    m = _fit(G, w)
+    Xs = w.Xstar[0].copy()
+    om = H.oracle_fits(w)[0]
+    best = gp.score(om, Xs).idx
+    Xs[best, 1] = np.nan
+    idx, _ = ctx.score_argmax(m, np.ascontiguousarray(Xs), [0, 256])
+    assert idx[0] != best and idx[0] >= 0
