@@ -153,10 +153,22 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
 /* Number of CUDA kernels the library launched on ctx since creation (for bench accounting). */
 int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 
+/* Candidates the last ei_score_argmax call on ctx re-scored in the float64 refine phase
+ * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */
+int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
+
 /* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,
  * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP).  Diagnostic/testing. */
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl);
+
+/* Test hook: run only the fast phase of the scoring path on M device-resident candidates of
+ * search s and write, per candidate (device float32 arrays of M, standardised units): the fast
+ * mean mu~, its error bound dmu, the latent variance s2~, its error bound dvar, and the EI
+ * bracket [ei_lo, ei_hi] the argmax filter uses.  Tests check the bracket contains the oracle. */
+gpbo_status gpbo_debug_fast_phase(gpbo_ctx *ctx, const gpbo_model *model, int32_t s,
+                                  const float *Xstar_dev, int64_t M, float *mu, float *dmu,
+                                  float *var, float *dvar, float *ei_lo, float *ei_hi);
 
 #ifdef __cplusplus
 }

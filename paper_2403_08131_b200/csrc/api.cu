@@ -22,15 +22,18 @@ struct gpbo_ctx {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
   std::string err;
-  unsigned long long *keys_d = nullptr;
+  unsigned long long *keys_d = nullptr;  // [cap] keys | [cap] u32 thresholds | u32 list count
   unsigned long long *keys_h = nullptr;
   int keys_cap = 0;
+  gpbo::RefineEntry *list_d = nullptr;   // refine list of the argmax path
+  size_t list_cap = 0;
   void *stage_d = nullptr;  // device staging of host-resident candidates / outputs
   size_t stage_cap = 0;
   void *aux_d = nullptr;    // per-call small arrays (offsets, bases, best, tile prefix)
   void *aux_h = nullptr;    // pinned mirror
   size_t aux_cap = 0;
   int64_t launches = 0;
+  int64_t last_refine = 0;  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05
 };
@@ -46,6 +49,7 @@ struct gpbo_model {
   char *block = nullptr;         // one cudaMallocAsync block, sub-allocated below
   float *X32 = nullptr, *ls32 = nullptr, *Xs32 = nullptr, *LT32 = nullptr;
   double *y64 = nullptr, *L64 = nullptr, *Linv64 = nullptr, *alpha64 = nullptr;
+  double *Xs64 = nullptr;
   unsigned char *img = nullptr;  // tcgen05 operand images
   int64_t img_bytes = 0;
 };
@@ -104,16 +108,34 @@ gpbo_status ensure_keys(gpbo_ctx *ctx, int S) {
   if (ctx->keys_d) CK(cudaFree(ctx->keys_d));
   if (ctx->keys_h) CK(cudaFreeHost(ctx->keys_h));
   int cap = std::max(S, 64);
-  CK(cudaMalloc(&ctx->keys_d, cap * sizeof(unsigned long long)));
-  CK(cudaMallocHost(&ctx->keys_h, cap * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->keys_d, cap * (sizeof(unsigned long long) + 4) + 16));
+  CK(cudaMallocHost(&ctx->keys_h, (cap + 1) * sizeof(unsigned long long)));
   ctx->keys_cap = cap;
   return GPBO_OK;
 }
 
-// Shared scoring launch used by gp_posterior and ei_score_argmax.
+gpbo_status ensure_list(gpbo_ctx *ctx, size_t entries) {
+  if (entries <= ctx->list_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->list_d) CK(cudaFree(ctx->list_d));
+  ctx->list_d = nullptr;
+  ctx->list_cap = 0;
+  size_t cap = std::max<size_t>(entries, 1 << 16);
+  CK(cudaMalloc(&ctx->list_d, cap * sizeof(gpbo::RefineEntry)));
+  ctx->list_cap = cap;
+  return GPBO_OK;
+}
+
+struct Outputs {
+  float *mu = nullptr, *var = nullptr, *ei = nullptr;   // posterior mode (device)
+  float *dbg[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // debug mode
+};
+
+// Shared scoring launch used by gp_posterior and ei_score_argmax: the fast phase (tcgen05 or
+// CUDA-core kernel) followed by the float64 refine phase.
 gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S,
                       const float *Xstar_dev, const int64_t *m_off, const int64_t *m_base,
-                      const double *best_std, float *out_mu, float *out_var, float *out_ei) {
+                      const double *best_std, int mode, const Outputs &out) {
   // aux layout: m_off[S+1] i64 | m_base[S] i64 | x_off[S] i64 | best[S] f64 | tile_first[S+1] i32
   const size_t bytes = (size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4;
   gpbo_status st = ensure_aux(ctx, bytes + 64);
@@ -156,8 +178,16 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     h_tiles[i + 1] = h_tiles[i] + (int32_t)t;
   }
   h_off[S] = m_off[S] - m_off[0];
+  const int64_t rows = h_off[S];
+  if (mode == gpbo::kModeArgmax) {
+    st = ensure_list(ctx, (size_t)rows);
+    if (st) return st;
+  }
   CK(cudaMemcpyAsync(ctx->aux_d, ctx->aux_h, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemsetAsync(ctx->keys_d, 0, S * sizeof(unsigned long long), ctx->stream));
+  unsigned int *thr_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap);
+  unsigned int *count_d = thr_d + ctx->keys_cap;
+  CK(cudaMemsetAsync(ctx->keys_d, 0, ctx->keys_cap * (sizeof(unsigned long long) + 4) + 4,
+                     ctx->stream));
   char *dptr = (char *)ctx->aux_d;
   gpbo::ScoreLaunch p{};
   p.meta = model->meta_d + s_first;
@@ -174,17 +204,44 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.ls32 = model->ls32;
   p.img = model->img;
   p.keys = ctx->keys_d;
-  p.out_mu = out_mu;
-  p.out_var = out_var;
-  p.out_ei = out_ei;
+  p.out_var = out.var;
+  p.mode = mode;
+  p.thr = thr_d;
+  p.list = ctx->list_d;
+  p.list_count = count_d;
+  p.list_cap = (uint32_t)std::min<size_t>(ctx->list_cap, 0xFFFFFFFFu);
+  p.dbg_mu = out.dbg[0]; p.dbg_dmu = out.dbg[1]; p.dbg_var = out.dbg[2];
+  p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
   const int tiles = h_tiles[S];
-  if (tiles > 0) {
-    if (use_tc)
-      CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
-    else
-      CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
-    ctx->launches += 1;
+  if (tiles == 0) return GPBO_OK;
+  if (use_tc)
+    CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
+  else
+    CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
+  ctx->launches += 1;
+  if (mode == gpbo::kModeDebug) return GPBO_OK;
+  gpbo::RefineLaunch r{};
+  r.meta = p.meta;
+  r.Xstar = p.Xstar;
+  r.m_off = p.m_off; r.m_base = p.m_base; r.x_off = p.x_off;
+  r.best = p.best;
+  r.Xs64 = model->Xs64;
+  r.ls32 = model->ls32;
+  r.alpha64 = model->alpha64;
+  r.Linv64 = model->Linv64;
+  r.keys = ctx->keys_d;
+  r.thr = thr_d;
+  if (mode == gpbo::kModeArgmax) {
+    r.list = ctx->list_d;
+    r.list_count = count_d;
+  } else {
+    r.dense_s = 0;
+    r.dense_rows = rows;
+    r.dense_var = out.var;
+    r.out_mu = out.mu; r.out_var = out.var; r.out_ei = out.ei;
   }
+  CK(gpbo::launch_refine(r, rows, ctx->num_sms, ctx->stream));
+  ctx->launches += 1;
   return GPBO_OK;
 }
 
@@ -250,6 +307,7 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
   if (ctx->keys_d) cudaFree(ctx->keys_d);
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
+  if (ctx->list_d) cudaFree(ctx->list_d);
   delete ctx;
   return GPBO_OK;
 }
@@ -257,6 +315,8 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
 const char *gpbo_last_error(const gpbo_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 int64_t gpbo_launch_count(const gpbo_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_refine : -1; }
 
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl) {
   if (!ctx || impl < 0 || impl > 2) return GPBO_EINVAL;
@@ -341,6 +401,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   const size_t o_x = take(nx * 4), o_ls = take(nls * 4), o_xs = take(nxs * 4);
   const size_t o_lt = take(nlt * 4), o_y = take(ny * 8), o_L = take(nmat * 8);
   const size_t o_Li = take(nmat * 8), o_a = take(na * 8), o_img = take(nimg);
+  const size_t o_x64 = take(nx * 8);
   cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
   if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
   m->meta_d = (SearchMeta *)(m->block + o_meta);
@@ -354,6 +415,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   m->Linv64 = (double *)(m->block + o_Li);
   m->alpha64 = (double *)(m->block + o_a);
   m->img = (unsigned char *)(m->block + o_img);
+  m->Xs64 = (double *)(m->block + o_x64);
   m->img_bytes = nimg;
   const cudaMemcpyKind kind = a->mem == GPBO_HOST ? cudaMemcpyHostToDevice
                                                   : cudaMemcpyDeviceToDevice;
@@ -374,7 +436,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   CKM(cudaMemcpyAsync(meta_in, m->meta.data(), sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
                       ctx->stream));
   CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
-                       m->Xs32, m->LT32, m->alpha64, m->meta_d, ctx->stream));
+                       m->Xs32, m->Xs64, m->LT32, m->alpha64, m->meta_d, ctx->stream));
   ctx->launches += 1;
   if (nimg > 0) {
     CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs32, m->alpha64, m->img,
@@ -452,29 +514,51 @@ gpbo_status gp_posterior(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, cons
   if (q.status != GPBO_OK && q.status != GPBO_WDEGENERATE)
     return fail(ctx, GPBO_ENOTPD, "search has no valid fit");
   if (M == 0) return GPBO_OK;
+  // device staging: [X* if host] | mu | var | ei  (var is always needed by the refine pass)
+  const size_t xb = mem == GPBO_HOST ? round_up((int64_t)M * q.d * 4, 256) : 0;
+  const size_t ob = round_up(M * 4, 256);
+  gpbo_status st = ensure_stage(ctx, xb + 3 * ob);
+  if (st) return st;
+  char *b = (char *)ctx->stage_d;
   const float *xd = Xstar;
-  float *omu = mu, *ovar = var, *oei = ei;
   if (mem == GPBO_HOST) {
-    const size_t xb = (size_t)M * q.d * 4, ob = (size_t)M * 4;
-    gpbo_status st = ensure_stage(ctx, xb + 3 * ob + 1024);
-    if (st) return st;
-    char *b = (char *)ctx->stage_d;
-    CK(cudaMemcpyAsync(b, Xstar, xb, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(b, Xstar, (size_t)M * q.d * 4, cudaMemcpyHostToDevice, ctx->stream));
     xd = (const float *)b;
-    char *ob0 = b + round_up(xb, 256);
-    omu = mu ? (float *)ob0 : nullptr;
-    ovar = var ? (float *)(ob0 + round_up(ob, 256)) : nullptr;
-    oei = ei ? (float *)(ob0 + 2 * round_up(ob, 256)) : nullptr;
   }
+  Outputs o;
+  o.mu = (mem == GPBO_DEVICE && mu) ? mu : (float *)(b + xb);
+  o.var = (mem == GPBO_DEVICE && var) ? var : (float *)(b + xb + ob);
+  o.ei = (mem == GPBO_DEVICE && ei) ? ei : (float *)(b + xb + 2 * ob);
   const int64_t off[2] = {0, M};
   const double best = q.best;
-  gpbo_status st = run_score(ctx, model, s, 1, xd, off, nullptr, &best, omu, ovar, oei);
+  st = run_score(ctx, model, s, 1, xd, off, nullptr, &best, gpbo::kModePosterior, o);
   if (st) return st;
   if (mem == GPBO_HOST) {
-    if (mu) CK(cudaMemcpyAsync(mu, omu, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    if (var) CK(cudaMemcpyAsync(var, ovar, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    if (ei) CK(cudaMemcpyAsync(ei, oei, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (mu) CK(cudaMemcpyAsync(mu, o.mu, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (var) CK(cudaMemcpyAsync(var, o.var, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ei) CK(cudaMemcpyAsync(ei, o.ei, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
   }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return GPBO_OK;
+}
+
+gpbo_status gpbo_debug_fast_phase(gpbo_ctx *ctx, const gpbo_model *model, int32_t s,
+                                  const float *Xstar_dev, int64_t M, float *mu, float *dmu,
+                                  float *var, float *dvar, float *ei_lo, float *ei_hi) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model || s < 0 || s >= model->S || M <= 0 || !Xstar_dev || !mu || !dmu || !var ||
+      !dvar || !ei_lo || !ei_hi)
+    return fail(ctx, GPBO_EINVAL, "bad debug arguments (device arrays required)");
+  CK(cudaSetDevice(ctx->device));
+  Outputs o;
+  float *d[6] = {mu, dmu, var, dvar, ei_lo, ei_hi};
+  for (int i = 0; i < 6; ++i) o.dbg[i] = d[i];
+  const int64_t off[2] = {0, M};
+  const double best = model->meta[s].best;
+  gpbo_status st = run_score(ctx, model, s, 1, Xstar_dev, off, nullptr, &best,
+                             gpbo::kModeDebug, o);
+  if (st) return st;
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
   return GPBO_OK;
@@ -509,14 +593,18 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
     xd = (const float *)ctx->stage_d;
   }
   gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_global_base, best_std.data(),
-                             nullptr, nullptr, nullptr);
+                             gpbo::kModeArgmax, Outputs());
   if (st) return st;
   if (ctx->nranks > 1)
     NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
   CK(cudaMemcpyAsync(ctx->keys_h, ctx->keys_d, S * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned int *count_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap) + ctx->keys_cap;
+  CK(cudaMemcpyAsync(ctx->keys_h + ctx->keys_cap, count_d, 4, cudaMemcpyDeviceToHost,
+                     ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
+  ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
   for (int s = 0; s < S; ++s) {
     const unsigned long long k = ctx->keys_h[s];
     const SearchMeta &q = model->meta[s];

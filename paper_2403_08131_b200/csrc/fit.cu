@@ -25,14 +25,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Deterministic block reductions (fixed tree order).
 template <class Op>
-__device__ double block_reduce(double v, double *red, Op op) {
+__device__ double block_reduce(double v, double *red, Op op, double identity) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
   if (lane == 0) red[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    double t = red[lane < kWarps ? lane : 0];
+    double t = lane < kWarps ? red[lane] : identity;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t = op(t, __shfl_xor_sync(0xffffffffu, t, o));
     if (lane == 0) red[32] = t;
@@ -57,7 +57,7 @@ __device__ __forceinline__ double kernel_value(double r2, double sf2, int kind) 
 __global__ void __launch_bounds__(kFitThreads, 1)
 fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
            const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
-           double *Linv64, float *Xs32, float *LT32, double *alpha64,
+           double *Linv64, float *Xs32, double *Xs64, float *LT32, double *alpha64,
            SearchMeta *__restrict__ meta_out) {
   extern __shared__ double sm[];
   __shared__ double red[33];
@@ -89,11 +89,11 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   // ---- H1: y~ = (y - mean) / std, ddof = 0 (reading R7); degenerate -> y~ = 0, std = 1
   double acc = 0.0, amax = 0.0;
   for (int i = tid; i < n; i += kFitThreads) { acc += y[i]; amax = fmax(amax, fabs(y[i])); }
-  const double mean = block_reduce(acc, red, AddOp()) / n;
-  amax = block_reduce(amax, red, MaxOp());
+  const double mean = block_reduce(acc, red, AddOp(), 0.0) / n;
+  amax = block_reduce(amax, red, MaxOp(), 0.0);
   acc = 0.0;
   for (int i = tid; i < n; i += kFitThreads) { const double t = y[i] - mean; acc += t * t; }
-  double stdv = sqrt(block_reduce(acc, red, AddOp()) / n);
+  double stdv = sqrt(block_reduce(acc, red, AddOp(), 0.0) / n);
   const bool degenerate = !(stdv > 1e-12 * amax);
   if (degenerate) stdv = 1.0;
   double bmin = INFINITY;
@@ -102,13 +102,25 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     yt[i] = t;
     bmin = fmin(bmin, t);
   }
-  const double best = block_reduce(bmin, red, MinOp());
+  const double best = block_reduce(bmin, red, MinOp(), INFINITY);
 
-  // ---- scoring operand: X / l in float32 (IEEE division), zero padded to n_pad x d_pad
+  // ---- scoring operands: X / l in float32 (IEEE division), zero padded to n_pad x d_pad,
+  // and in float64 (n x d) for the refine phase; pmax = max_j |x_j / l|^2
   for (int e = tid; e < m.n_pad * m.d_pad; e += kFitThreads) {
     const int i = e / m.d_pad, c = e - i * m.d_pad;
     Xs32[m.xs_off + e] = (i < n && c < d) ? __fdiv_rn(X[i * d + c], ls[c]) : 0.f;
   }
+  double pm = 0.0;
+  for (int i = tid; i < n; i += kFitThreads) {
+    double q = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double v = (double)X[i * d + c] / (double)ls[c];
+      Xs64[m.x_off + i * d + c] = v;
+      q += v * v;
+    }
+    pm = fmax(pm, q);
+  }
+  const double pmax = block_reduce(pm, red, MaxOp(), 0.0);
 
   // ---- H2 + H3: Gram matrix and Cholesky with the jitter ladder j_k = 1e-8 10^k sf2
   const double sf2 = m.sf2, sn2 = m.sn2;
@@ -185,15 +197,23 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   }
   __syncthreads();
   // alpha = L^-T w  (warp per k, lanes over i >= k)
-  double l1 = 0.0;
+  double l1 = 0.0, amx = 0.0;
   for (int k = warp; k < m.n_pad; k += kWarps) {
     double a2 = 0.0;
     if (k < n)
       for (int i = k + lane; i < n; i += 32) a2 += A[(size_t)k * n + i] * w[i];
     a2 = warp_sum(a2);
-    if (lane == 0) { alpha64[m.a_off + k] = a2; l1 += fabs(a2); }
+    if (lane == 0) { alpha64[m.a_off + k] = a2; l1 += fabs(a2); amx = fmax(amx, fabs(a2)); }
   }
-  l1 = block_reduce(l1, red, AddOp());
+  l1 = block_reduce(l1, red, AddOp(), 0.0);
+  amx = block_reduce(amx, red, MaxOp(), 0.0);
+  double rs = 0.0;
+  for (int j = tid; j < n; j += kFitThreads) {
+    double a3 = 0.0;
+    for (int k = 0; k <= j; ++k) a3 += fabs(A[(size_t)k * n + j]);
+    rs = fmax(rs, a3);
+  }
+  rs = block_reduce(rs, red, MaxOp(), 0.0);
   // write L^-1 (col-major) and the float32 (L^-1)^T scoring operand: LT[k][j] = Linv[j][k]
   if (m.use_smem)
     for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
@@ -213,6 +233,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     m.status = degenerate ? GPBO_WDEGENERATE : GPBO_OK;
     m.jitter_k = jk; m.jitter = jit;
     m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = l1;
+    m.pmax = (float)pmax; m.alpha_max = (float)amx; m.linv_rowsum = (float)rs;
     meta_out[s] = m;
   }
 }
@@ -221,13 +242,13 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
 
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
                        const float *ls32, const double *y64, double *L64, double *Linv64,
-                       float *Xs32, float *LT32, double *alpha64, SearchMeta *meta_out,
-                       cudaStream_t stream) {
+                       float *Xs32, double *Xs64, float *LT32, double *alpha64,
+                       SearchMeta *meta_out, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_bytes);
   if (e != cudaSuccess) return e;
   fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, X32, ls32, y64, L64, Linv64, Xs32,
-                                                     LT32, alpha64, meta_out);
+                                                     Xs64, LT32, alpha64, meta_out);
   return cudaGetLastError();
 }
 

@@ -29,11 +29,28 @@ struct SearchMeta {
   int64_t img_off;      // tcgen05 operand image (bytes)      into model.img
   // fit results
   double mean, std, best, alpha_l1;
+  float pmax;           // max_j |x_j / l|^2 (error-bound input of the fast phase)
+  float alpha_max;      // max_j |alpha_j|
+  float linv_rowsum;    // max_j sum_k |(L^-1)_jk| (variance error-bound input)
   double jitter;
   int32_t jitter_k;
   int32_t status;       // gpbo_status of this search
   int32_t use_smem;     // fit keeps its matrix in shared memory
   int32_t pad_;
+};
+
+// Candidate flagged by the fast phase for the float64 refine phase.
+struct RefineEntry {
+  int32_t s;      // search (launch-relative)
+  uint32_t row;   // local candidate row
+  float var;      // standardised latent variance from the fast phase (float32-accurate)
+  float ei_hi;    // upper bound of EI~ from the fast phase
+};
+
+enum ScoreMode : int32_t {
+  kModeArgmax = 0,     // fast phase flags candidates, refine computes the final keys
+  kModePosterior = 1,  // fast phase writes var~ of every candidate, refine writes mu/var/ei
+  kModeDebug = 2       // fast phase writes its own mu32 / dmu / EI bounds (tests)
 };
 
 // One scoring launch covers several searches; tile t of the launch belongs to search
@@ -54,6 +71,32 @@ struct ScoreLaunch {
   const unsigned char *img;    // tcgen05 operand images
   unsigned long long *keys;    // [S] per-search argmax keys (atomicMax)
   float *out_mu, *out_var, *out_ei;  // optional per-candidate outputs (raw units)
+  int32_t mode;                // ScoreMode
+  unsigned int *thr;           // [S] float bits of the running max EI_lo (argmax mode)
+  RefineEntry *list;           // refine list (argmax mode)
+  unsigned int *list_count;
+  uint32_t list_cap;
+  float *dbg_mu, *dbg_dmu, *dbg_var, *dbg_dvar, *dbg_eilo, *dbg_eihi;  // debug mode
+};
+
+// Float64 refine phase (refine.cu).
+struct RefineLaunch {
+  const SearchMeta *meta;
+  const float *Xstar;
+  const int64_t *m_off, *m_base, *x_off;
+  const double *best;
+  const double *Xs64;          // X / l in float64, n x d per search (indexed by x_off)
+  const float *ls32;
+  const double *alpha64;
+  const double *Linv64;        // L^-1, n x n column-major per search (mat_off)
+  unsigned long long *keys;
+  const unsigned int *thr;
+  const RefineEntry *list;     // argmax mode: entries; posterior mode: NULL (dense rows)
+  const unsigned int *list_count;
+  int32_t dense_s;             // posterior mode: search index
+  int64_t dense_rows;          // posterior mode: number of rows
+  const float *dense_var;      // posterior mode: var~ per row from the fast phase
+  float *out_mu, *out_var, *out_ei;
 };
 
 }  // namespace gpbo
@@ -62,8 +105,10 @@ struct ScoreLaunch {
 namespace gpbo {
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
                        const float *ls32, const double *y64, double *L64, double *Linv64,
-                       float *Xs32, float *LT32, double *alpha64, SearchMeta *meta_out,
-                       cudaStream_t stream);
+                       float *Xs32, double *Xs64, float *LT32, double *alpha64,
+                       SearchMeta *meta_out, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, int nmax,
                               cudaStream_t stream);
+cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
+                          cudaStream_t stream);
 }  // namespace gpbo

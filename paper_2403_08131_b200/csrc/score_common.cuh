@@ -35,6 +35,13 @@ __device__ __forceinline__ float ei_f32(double mu, float var, double best) {
   return sig * tau_f32(imp / sig);
 }
 
+// Error bound of the fast-phase variance sf2 - |v|^2 (v = L^-1 k* from float32 K*):
+// empirically ~ u sqrt(n) (sf2 + |v|^2) (2 + 0.01 |L^-1|_inf sqrt(sf2)) on the bracket-test
+// workloads; the factor 16 is the safety margin ("fast/refine split").
+__device__ __forceinline__ float var_bound(float u, float sf2, float s2, int n, float linv_rs) {
+  return 16.f * u * sqrtf((float)n) * (sf2 + s2) * (1.f + 0.01f * linv_rs * sqrtf(sf2));
+}
+
 // H9 key: EI >= +0 canonicalised (kills -0 and NaN), then (bits << 32) | (2^32-1 - idx).
 __device__ __forceinline__ unsigned long long make_key(float ei, uint64_t gidx) {
   if (isnan(ei)) return 0ull;
@@ -52,27 +59,81 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k)
   return k;
 }
 
-// Per-candidate epilogue: optional raw outputs (H11) and the CTA argmax -> atomicMax (H9).
-// Must be called by every thread of the block (uniform search per block).
-__device__ __forceinline__ void finish_candidate(const ScoreLaunch &p, int s,
-                                                 const SearchMeta &m, bool valid,
-                                                 int64_t row0, int64_t row, double mu, float var,
-                                                 float ei) {
-  __shared__ unsigned long long wk[32];
-  unsigned long long key = valid ? make_key(ei, (uint64_t)(p.m_base[s] + row)) : 0ull;
-  if (valid) {
-    if (p.out_mu) p.out_mu[row0 + row] = (float)(m.mean + m.std * mu);
-    if (p.out_var) p.out_var[row0 + row] = (float)(m.std * m.std * (double)var);
-    if (p.out_ei) p.out_ei[row0 + row] = (float)(m.std * (double)ei);
+// Epilogue of the fast phase for one candidate (every thread of the block calls it; the block
+// belongs to one search).  mu: standardised fast mean (float32 K*), dmu: its error bound,
+// var: standardised latent variance, dvar: its error bound.
+//   kModeArgmax:    EI is bracketed by monotonicity of EI in (mu, sigma):
+//                   EI_hi = EI(mu - dmu, var + dvar), EI_lo = EI(mu + dmu, var - dvar)
+//                   (+-2e-4 relative for the float32 tau()).  The block max of EI_lo raises the
+//                   search's running threshold; candidates with EI_hi >= threshold go to the
+//                   refine list; candidates with EI_hi == 0 have EI == 0 exactly and settle
+//                   their key here.
+//   kModePosterior: store var~ for the dense refine pass.
+//   kModeDebug:     store the phase's own values.
+__device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool valid,
+                                            int64_t row0, int64_t row, double mu, float dmu,
+                                            float var, float dvar) {
+  const bool ok = valid && isfinite(mu) && isfinite(var);
+  const double best = p.best[s];
+  float ei_lo = 0.f, ei_hi = 0.f;
+  if (ok && p.mode != kModePosterior) {
+    ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
+    ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
   }
-  key = warp_max_u64(key);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) wk[warp] = key;
+  if (p.mode == kModePosterior) {
+    if (valid) p.out_var[row0 + row] = var;
+    return;
+  }
+  if (p.mode == kModeDebug) {
+    if (valid) {
+      const int64_t i = row0 + row;
+      p.dbg_mu[i] = (float)mu; p.dbg_dmu[i] = dmu; p.dbg_var[i] = var; p.dbg_dvar[i] = dvar;
+      p.dbg_eilo[i] = ok ? ei_lo : NAN; p.dbg_eihi[i] = ok ? ei_hi : NAN;
+    }
+    return;
+  }
+  __shared__ unsigned int s_thr[32];
+  __shared__ unsigned long long s_zk[32];
+  const uint64_t gidx = (uint64_t)(p.m_base[s] + row);
+  unsigned int lo_bits = ok ? __float_as_uint(fmaxf(ei_lo, 0.f)) : 0u;
+  unsigned long long zkey = (ok && !(ei_hi > 0.f)) ? make_key(0.f, gidx) : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo_bits = max(lo_bits, __shfl_xor_sync(0xffffffffu, lo_bits, o));
+    const unsigned long long q = __shfl_xor_sync(0xffffffffu, zkey, o);
+    zkey = q > zkey ? q : zkey;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { s_thr[warp] = lo_bits; s_zk[warp] = zkey; }
   __syncthreads();
   if (warp == 0) {
-    unsigned long long k2 = lane < (int)(blockDim.x >> 5) ? wk[lane] : 0ull;
-    k2 = warp_max_u64(k2);
-    if (lane == 0 && k2) atomicMax(p.keys + s, k2);
+    unsigned int lb = lane < nw ? s_thr[lane] : 0u;
+    unsigned long long zk = lane < nw ? s_zk[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lb = max(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+      const unsigned long long q = __shfl_xor_sync(0xffffffffu, zk, o);
+      zk = q > zk ? q : zk;
+    }
+    if (lane == 0) {
+      const unsigned int old = atomicMax(p.thr + s, lb);
+      if (zk) atomicMax(p.keys + s, zk);
+      s_thr[0] = max(old, lb);
+    }
+  }
+  __syncthreads();
+  const float thr = __uint_as_float(s_thr[0]);
+  const bool flag = ok && ei_hi > 0.f && ei_hi >= thr;
+  const unsigned int mask = __ballot_sync(0xffffffffu, flag);
+  if (mask) {
+    const int leader = __ffs(mask) - 1;
+    unsigned int base = 0;
+    if (lane == leader) base = atomicAdd(p.list_count, (unsigned int)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (flag) {
+      const unsigned int pos = base + __popc(mask & ((1u << lane) - 1u));
+      if (pos < p.list_cap) p.list[pos] = RefineEntry{s, (uint32_t)row, var, ei_hi};
+    }
   }
 }
 

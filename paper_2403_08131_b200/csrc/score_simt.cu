@@ -46,6 +46,7 @@ score_simt_kernel(const ScoreLaunch p) {
   const float *Xs = p.Xs32 + mref.xs_off;
   const double *alpha = p.alpha64 + mref.a_off;
   double mu = 0.0;
+  float a1 = 0.f;  // sum_j |K*_j alpha_j|: scale of the mean's rounding error
   for (int j = 0; j < n; ++j) {
     float r2 = 0.f;
 #pragma unroll
@@ -57,7 +58,9 @@ score_simt_kernel(const ScoreLaunch p) {
     }
     const float k = kernel_f32(r2, sf2, kind);
     ks[j * TM + threadIdx.x] = k;
-    mu = fma((double)k, __ldg(alpha + j), mu);
+    const double aj = __ldg(alpha + j);
+    mu = fma((double)k, aj, mu);
+    a1 = fmaf(k, fabsf((float)aj), a1);
   }
 
   // ---- H7: s2 = |L^-1 k*|^2 in blocks of 8 columns of (L^-1)^T
@@ -81,11 +84,17 @@ score_simt_kernel(const ScoreLaunch p) {
     for (int q = 0; q < 8; ++q) s2 = fmaf(acc[q], acc[q], s2);
   }
 
-  // ---- H8 + H9
-  const double best = p.best[s];
+  // ---- H8 + H9 (fast phase): error bounds, then EI bracket / refine flagging.
+  // K* relative error <= (5/6) dr2 + ~(s + 10) u with dr2 <= 2 (d + 3) u (|x*|^2 + |x_j|^2) for
+  // the float32 direct differences; kappa factors are margins.
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < DMAX; ++c) q = fmaf(xs[c], xs[c], q);
+  const float u = 5.9604645e-8f;
+  const float dmu = 0.2f * u * a1 * (2.f * (float)(d + 3) * (q + mref.pmax) + 64.f);
   const float var = fmaxf(sf2 - s2, 0.f);
-  const float ei = ei_f32(mu, var, best);
-  finish_candidate(p, s, mref, valid, row0, row, mu, var, ei);
+  const float dvar = var_bound(u, sf2, s2, n, mref.linv_rowsum);
+  finish_fast(p, s, valid, row0, row, mu, dmu, var, dvar);
 }
 
 template <int DMAX, int TM>

@@ -60,7 +60,9 @@ def load():
         "gp_posterior": (C.c_int, [vp, vp, i32, vp, i64, C.c_int, vp, vp, vp]),
         "ei_score_argmax": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "gpbo_launch_count": (i64, [vp]),
+        "gpbo_last_refine_count": (i64, [vp]),
         "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
+        "gpbo_debug_fast_phase": (C.c_int, [vp, vp, i32, vp, i64] + [vp] * 6),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -74,7 +76,8 @@ def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
             "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
-            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl"]
+            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count",
+            "gpbo_debug_fast_phase"]
 
 
 def _is_torch(a):
@@ -187,6 +190,10 @@ class Context:
     def launches(self):
         return int(load().gpbo_launch_count(self.handle))
 
+    @property
+    def last_refine_count(self):
+        return int(load().gpbo_last_refine_count(self.handle))
+
     def set_score_impl(self, impl):
         """0 auto, 1 CUDA-core, 2 tcgen05 (see include/gpbo.h)."""
         _check(self, load().gpbo_set_score_impl(self.handle, int(impl)))
@@ -226,6 +233,20 @@ class Context:
         op = [(_ptr(o, np.float32)[0] if o is not None else None) for o in outs]
         _check(self, load().gp_posterior(self.handle, model.handle, s, px, M, mem, *op))
         return tuple(outs)
+
+    def debug_fast_phase(self, model, s, Xstar):
+        """Fast-phase values of every candidate (CUDA tensor X*): dict of CUDA tensors
+        mu, dmu, var, dvar, ei_lo, ei_hi (standardised units)."""
+        import torch
+        px, mem = _ptr(Xstar, np.float32)
+        if mem != DEVICE:
+            raise TypeError("debug_fast_phase needs a CUDA tensor")
+        M = int(Xstar.shape[0])
+        names = ("mu", "dmu", "var", "dvar", "ei_lo", "ei_hi")
+        outs = {k: torch.empty(M, dtype=torch.float32, device=Xstar.device) for k in names}
+        _check(self, load().gpbo_debug_fast_phase(self.handle, model.handle, s, px, M,
+                                                  *[outs[k].data_ptr() for k in names]))
+        return outs
 
     def score_argmax(self, model, Xstar, m_off, m_global_base=None, best=None):
         """ei_score_argmax -> (idx int64[S], ei float32[S] raw units)."""
