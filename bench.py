@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the GP-surrogate + EI hot path (BASELINE.json metric) on 1..8 B200s.
+
+One step = one pass of the whole hot path over one batch: gp_fit (H1-H4) on the observed
+configurations + ei_score_argmax (H6-H10: fast tensor/CUDA-core phase, float64 refine of the
+candidates that can still win, per-search argmax, NCCL max-all-reduce across ranks).
+
+Workload (N=1 line): BASELINE.json configs[1] -- one 20-parameter search, n = 200 observations,
+M = 2^20 random candidates per GPU (weak scaling: each rank scores its own 2^20-candidate shard
+of a pool of N * 2^20; the fit is replicated).  Inputs are seeded synthetic data shaped like the
+paper's (workloads/gen.py), resident in HBM when timing starts; L2 is
+flushed (256 MiB write) between timed steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the float64 CPU oracle (oracle/) on a
+bounded sample of the same workload (rank 0 only; other ranks exit 0).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GP-posterior+EI candidates scored/sec at 1/2/4/8 B200; % of roofline"
+UNIT = "candidates/s"
+
+
+def flops_per_candidate(n, d):
+    """F_c = 2nd (distances) + n(n+1) (triangular V) + 4n (mu, sum v^2)."""
+    return 2 * n * d + n * (n + 1) + 4 * n
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm=j.get("hbm_gbs", 6650.0), bf16=j.get("bf16_tflops", 1590.0),
+                    bf16_sus=j.get("bf16_tflops_sustained", 1400.0),
+                    sm_mhz=j.get("sm_max_mhz", 1965.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_mhz=1965.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", ",".join(str(g) for g in range(self.gpus)), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                util = float(r[4])
+                if util > 0:
+                    sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_rate(cfg, M_sample, seed_rank=0):
+    """Time the float64 oracle on a bounded sample of the workload (host cores)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gp
+    from workloads import gen
+    cores = os.cpu_count()
+    w = gen.make(cfg, M=M_sample)
+    with threadpool_limits(limits=cores):
+        t0 = time.perf_counter()
+        for s, Xs in zip(w.searches, w.Xstar):
+            m = gp.fit(s.X, s.y, s.lengthscale, s.sf2, s.sn2, w.kernel)
+            gp.score(m, Xs)
+        dt = time.perf_counter() - t0
+    total = sum(x.shape[0] for x in w.Xstar)
+    return total / dt, cores, total, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--layout", default="uniform", choices=["uniform", "bo"])
+    ap.add_argument("--score-impl", type=int, default=0, help="0 auto, 1 CUDA-core, 2 tcgen05")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from workloads import gen
+    S0, n0, d0, M0 = gen.CONFIG_SHAPES[args.config]
+    per_gpu = M0 if args.config != 4 else M0 // 8
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # the oracle as it stands, each step a bounded sample of the same workload
+        M_ref = max(4096, min(per_gpu, 1 << 14))
+        times = []
+        for i in range(args.warmup + args.steps):
+            rate, cores, total, dt = cpu_oracle_rate(args.config, M_ref)
+            if i >= args.warmup:
+                times.append(dt)
+        T = float(np.sum(times))
+        value = total * args.steps / T
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S0, "n": n0,
+                           "d": d0, "M_per_step_sample": M_ref},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                                 "kind": "oracle",
+                                 "sample": f"{M_ref} candidates of {gen.CONFIG_NAMES[args.config]}"
+                                           " per step (fit + score + argmax, float64 numpy)"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2403_08131_b200 import gpbo
+
+    nccl_id = None
+    if world > 1:
+        obj = [gpbo.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = gpbo.Context(device=local, stream=stream, nranks=world, rank=rank, nccl_id=nccl_id)
+    ctx.set_score_impl(args.score_impl)
+
+    # ---- inputs (seeded, host -> HBM once, untimed)
+    M_total = per_gpu * world
+    w = gen.make(args.config, M=M_total, rank=rank, world=world, layout=args.layout)
+    S = w.S
+    n = [s.X.shape[0] for s in w.searches]
+    d = [s.X.shape[1] for s in w.searches]
+    Xh = np.ascontiguousarray(np.concatenate([s.X.ravel() for s in w.searches]), np.float32)
+    yh = np.ascontiguousarray(np.concatenate([s.y for s in w.searches]), np.float64)
+    lsh = np.ascontiguousarray(np.concatenate([s.lengthscale for s in w.searches]), np.float32)
+    sf2h = np.array([s.sf2 for s in w.searches], np.float32)
+    sn2h = np.array([s.sn2 for s in w.searches], np.float32)
+    Xsh = np.ascontiguousarray(np.concatenate([x.ravel() for x in w.Xstar]), np.float32)
+    m_off = np.zeros(S + 1, np.int64)
+    m_off[1:] = np.cumsum([x.shape[0] for x in w.Xstar])
+    base = np.array(w.m_global_base, np.int64)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    Xd, yd, lsd, sf2d, sn2d, Xsd = t(Xh), t(yh), t(lsh), t(sf2h), t(sn2h), t(Xsh)
+    Xs_pin = torch.from_numpy(Xsh).pin_memory()
+    local_cands = int(m_off[-1])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step_device():
+        m = ctx.fit(n, d, Xd, yd, lsd, sf2d, sn2d, kernel=w.kernel)
+        idx, ei = ctx.score_argmax(m, Xsd, m_off, base)
+        m.free()
+        return idx, ei
+
+    def step_host():
+        m = ctx.fit(n, d, Xh, yh, lsh, sf2h, sn2h, kernel=w.kernel)
+        idx, ei = ctx.score_argmax(m, Xs_pin, m_off, base)
+        m.free()
+        return idx, ei
+
+    def timed(step, K, W):
+        for _ in range(W):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.launches
+        ctx.set_profiling(True)
+        tot = 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        refined = 0
+        for _ in range(K):
+            flush.zero_()
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+            refined += ctx.last_refine_count
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        kt = {k: ctx.kernel_time(k) for k in ctx.KERNELS}
+        ctx.set_profiling(False)
+        return tot, ctx.launches - l0, kt, refined
+
+    # ---- device-resident timing (the value) with clocks sampled during it
+    with ClockSampler(world if rank == 0 else 0) as clk:
+        T_dev, launches, kt, refined = timed(step_device, args.steps, args.warmup)
+    # ---- end-to-end through the C ABI with host buffers
+    T_e2e, _, _, _ = timed(step_host, args.steps, args.warmup)
+
+    def vmax(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    T_dev, T_e2e = vmax(T_dev), vmax(T_e2e)
+    fast_n, fast_ms = kt["fast"]
+    fast_ms = vmax(fast_ms)
+    total_cands = M_total * args.steps
+    value = total_cands / (T_dev / 1e3)
+    e2e_value = total_cands / (T_e2e / 1e3)
+    idx, ei = step_device()
+    if rank == 0:
+        peaks = load_peaks()
+        impl_used = "tcgen05" if ctx.last_impl == 2 else "cuda-core"
+        Fc = sum(flops_per_candidate(nn, dd) * x.shape[0] for nn, dd, x in zip(n, d, w.Xstar))
+        achieved = Fc / (fast_ms / fast_n / 1e3) / 1e12  # TFLOP/s of the fast-phase kernel
+        if impl_used == "tcgen05":
+            peak = peaks["bf16_sus"]
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_src": f"{peaks['src']} bf16 dense sustained (fp16 same rate)"}
+        else:
+            peak = 148 * 128 * 2 * peaks["sm_mhz"] * 1e6 / 1e12
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_src": "FP32 FFMA: 148 SM x 128 lanes x 2 flop x max SM clock"}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, cores, tot_c, dt = cpu_oracle_rate(args.config, args.cpu_sample)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{tot_c} candidates of {gen.CONFIG_NAMES[args.config]} "
+                             f"(fit + score + argmax, float64 numpy, {dt:.1f} s)"}
+        h2d = Xh.nbytes + yh.nbytes + lsh.nbytes + sf2h.nbytes + sn2h.nbytes + Xsh.nbytes
+        d2h = 8 * S + 4 + 192 * S
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": T_dev / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16x3+f32+f64" if impl_used == "tcgen05" else "f32+f64",
+            "data": "synthetic",
+            "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
+                       "M_per_gpu": per_gpu, "M_global": M_total,
+                       "kernel": "matern52" if w.kernel == 1 else "rbf",
+                       "layout": args.layout, "l2": "flushed between steps (256 MiB write)",
+                       "scoring": impl_used},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "breakdown_ms_per_step": {k: kt[k][1] / args.steps for k in kt},
+            "refined_per_step": refined / args.steps,
+            "result": {"idx": int(idx[0]), "ei": float(ei[0])},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

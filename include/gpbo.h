@@ -156,6 +156,15 @@ int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 /* Candidates the last ei_score_argmax call on ctx re-scored in the float64 refine phase
  * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
+/* Fast-phase implementation of the last scoring call: 1 = CUDA-core, 2 = tcgen05. */
+int gpbo_last_score_impl(const gpbo_ctx *ctx);
+
+/* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel
+ * launch (for bench.py's roofline).  gpbo_set_profiling(ctx, 1) enables it and clears the
+ * totals; gpbo_kernel_time returns the launch count and summed milliseconds of one kind:
+ * 0 = fit (H1-H4), 1 = scoring fast phase (H6-H9), 2 = float64 refine phase, 3 = operand pack. */
+gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on);
+gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms);
 
 /* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,

@@ -33,7 +33,14 @@ struct gpbo_ctx {
   void *aux_h = nullptr;    // pinned mirror
   size_t aux_cap = 0;
   int64_t launches = 0;
-  int64_t last_refine = 0;  // candidates the last argmax call flagged for the refine phase
+  // optional per-kernel CUDA-event timing (gpbo_set_profiling): kinds fit / fast / refine / pack
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;
+  double kern_ms[4] = {0, 0, 0, 0};
+  int64_t kern_count[4] = {0, 0, 0, 0};
+  int64_t last_refine = 0;
+  int last_impl = 0;        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05
 };
@@ -77,6 +84,51 @@ gpbo_status fail(gpbo_ctx *ctx, gpbo_status st, const std::string &msg) {
   } while (0)
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+enum { kKernFit = 0, kKernFast = 1, kKernRefine = 2, kKernPack = 3 };
+
+cudaEvent_t take_event(gpbo_ctx *ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one library kernel launch with events on ctx's stream when profiling is on.
+struct KernTimer {
+  gpbo_ctx *ctx;
+  int kind;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KernTimer(gpbo_ctx *c, int k) : ctx(c), kind(k) {
+    if (!ctx->profiling) return;
+    a = take_event(ctx);
+    b = take_event(ctx);
+    cudaEventRecord(a, ctx->stream);
+  }
+  ~KernTimer() {
+    if (!a) return;
+    cudaEventRecord(b, ctx->stream);
+    ctx->ev_open.push_back({kind, {a, b}});
+  }
+};
+
+// Called after a stream synchronisation: fold the closed event pairs into the totals.
+void harvest_events(gpbo_ctx *ctx) {
+  for (auto &o : ctx->ev_open) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, o.second.first, o.second.second) == cudaSuccess) {
+      ctx->kern_ms[o.first] += ms;
+      ctx->kern_count[o.first] += 1;
+    }
+    ctx->ev_pool.push_back(o.second.first);
+    ctx->ev_pool.push_back(o.second.second);
+  }
+  ctx->ev_open.clear();
+}
 
 gpbo_status ensure_stage(gpbo_ctx *ctx, size_t bytes) {
   if (bytes <= ctx->stage_cap) return GPBO_OK;
@@ -213,11 +265,15 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.dbg_mu = out.dbg[0]; p.dbg_dmu = out.dbg[1]; p.dbg_var = out.dbg[2];
   p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
   const int tiles = h_tiles[S];
+  ctx->last_impl = use_tc ? 2 : 1;
   if (tiles == 0) return GPBO_OK;
-  if (use_tc)
-    CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
-  else
-    CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
+  {
+    KernTimer t(ctx, kKernFast);
+    if (use_tc)
+      CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
+    else
+      CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
+  }
   ctx->launches += 1;
   if (mode == gpbo::kModeDebug) return GPBO_OK;
   gpbo::RefineLaunch r{};
@@ -240,7 +296,10 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     r.dense_var = out.var;
     r.out_mu = out.mu; r.out_var = out.var; r.out_ei = out.ei;
   }
-  CK(gpbo::launch_refine(r, rows, ctx->num_sms, ctx->stream));
+  {
+    KernTimer t(ctx, kKernRefine);
+    CK(gpbo::launch_refine(r, rows, ctx->num_sms, ctx->stream));
+  }
   ctx->launches += 1;
   return GPBO_OK;
 }
@@ -308,6 +367,8 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->keys_d) cudaFree(ctx->keys_d);
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
   if (ctx->list_d) cudaFree(ctx->list_d);
+  harvest_events(ctx);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
   return GPBO_OK;
 }
@@ -317,6 +378,26 @@ const char *gpbo_last_error(const gpbo_ctx *ctx) { return ctx ? ctx->err.c_str()
 int64_t gpbo_launch_count(const gpbo_ctx *ctx) { return ctx ? ctx->launches : -1; }
 
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_refine : -1; }
+
+int gpbo_last_score_impl(const gpbo_ctx *ctx) { return ctx ? ctx->last_impl : -1; }
+
+gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on) {
+  if (!ctx) return GPBO_EINVAL;
+  cudaStreamSynchronize(ctx->stream);
+  harvest_events(ctx);
+  ctx->profiling = on != 0;
+  for (int i = 0; i < 4; ++i) { ctx->kern_ms[i] = 0.0; ctx->kern_count[i] = 0; }
+  return GPBO_OK;
+}
+
+gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms) {
+  if (!ctx || kind < 0 || kind > 3) return GPBO_EINVAL;
+  cudaStreamSynchronize(ctx->stream);
+  harvest_events(ctx);
+  if (count) *count = ctx->kern_count[kind];
+  if (ms) *ms = ctx->kern_ms[kind];
+  return GPBO_OK;
+}
 
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl) {
   if (!ctx || impl < 0 || impl > 2) return GPBO_EINVAL;
@@ -435,10 +516,14 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   CKM(cudaMemcpyAsync(m->y64, a->y, ny * 8, kind, ctx->stream));
   CKM(cudaMemcpyAsync(meta_in, m->meta.data(), sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
                       ctx->stream));
-  CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
-                       m->Xs32, m->Xs64, m->LT32, m->alpha64, m->meta_d, ctx->stream));
+  {
+    KernTimer t(ctx, kKernFit);
+    CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
+                         m->Xs32, m->Xs64, m->LT32, m->alpha64, m->meta_d, ctx->stream));
+  }
   ctx->launches += 1;
   if (nimg > 0) {
+    KernTimer t(ctx, kKernPack);
     CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs32, m->alpha64, m->img,
                              ctx->stream));
     ctx->launches += 1;
@@ -446,6 +531,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   CKM(cudaMemcpyAsync(m->meta.data(), m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
                       ctx->stream));
   CKM(cudaStreamSynchronize(ctx->stream));
+  harvest_events(ctx);
 #undef CKM
   gpbo_status worst = GPBO_OK;
   bool einval = false;
@@ -604,6 +690,7 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
+  harvest_events(ctx);
   ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
   for (int s = 0; s < S; ++s) {
     const unsigned long long k = ctx->keys_h[s];

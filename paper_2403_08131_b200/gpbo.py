@@ -61,6 +61,9 @@ def load():
         "ei_score_argmax": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "gpbo_launch_count": (i64, [vp]),
         "gpbo_last_refine_count": (i64, [vp]),
+        "gpbo_last_score_impl": (C.c_int, [vp]),
+        "gpbo_set_profiling": (C.c_int, [vp, C.c_int]),
+        "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
         "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
         "gpbo_debug_fast_phase": (C.c_int, [vp, vp, i32, vp, i64] + [vp] * 6),
     }
@@ -76,7 +79,8 @@ def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
             "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
-            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count",
+            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
+            "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase"]
 
 
@@ -193,6 +197,22 @@ class Context:
     @property
     def last_refine_count(self):
         return int(load().gpbo_last_refine_count(self.handle))
+
+    @property
+    def last_impl(self):
+        return int(load().gpbo_last_score_impl(self.handle))
+
+    def set_profiling(self, on=True):
+        _check(self, load().gpbo_set_profiling(self.handle, int(bool(on))))
+
+    KERNELS = ("fit", "fast", "refine", "pack")
+
+    def kernel_time(self, kind):
+        """(launches, total ms) of one library kernel kind since set_profiling(True)."""
+        k = self.KERNELS.index(kind) if isinstance(kind, str) else int(kind)
+        cnt, ms = C.c_int64(), C.c_double()
+        _check(self, load().gpbo_kernel_time(self.handle, k, C.byref(cnt), C.byref(ms)))
+        return cnt.value, ms.value
 
     def set_score_impl(self, impl):
         """0 auto, 1 CUDA-core, 2 tcgen05 (see include/gpbo.h)."""
