@@ -166,6 +166,13 @@ int gpbo_last_score_impl(const gpbo_ctx *ctx);
 gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on);
 gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms);
 
+/* Test hook: one CTA computes D[128 x N] = A[128 x K] B[N x K]^T (fp16 row-major device inputs,
+ * fp32 output) through the same tcgen05 path the scoring kernel uses: K-major operands in the
+ * `row_bytes` (32/64/128) swizzle layout, one MMA per 16-wide k step, B read from a row offset
+ * `b_row_off` (multiple of 8) of its shared-memory tile, accumulator in TMEM.  Synchronous. */
+gpbo_status gpbo_tc_selftest(const void *A, const void *B, float *D, int N, int K, int row_bytes,
+                             int b_row_off);
+
 /* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,
  * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP).  Diagnostic/testing. */

@@ -224,7 +224,9 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     const int64_t Ms = m_off[i + 1] - m_off[i];
     if (Ms < 0 || h_base[i] < 0 || h_base[i] + Ms >= 0xFFFFFFFFll)
       return fail(ctx, GPBO_EINVAL, "candidate offsets out of range (M_s must be < 2^32-1)");
-    const int64_t t = (Ms + tile - 1) / tile;
+    const int st_i = model->meta[s_first + i].status;
+    const bool fitted = st_i == GPBO_OK || st_i == GPBO_WDEGENERATE;
+    const int64_t t = fitted ? (Ms + tile - 1) / tile : 0;  // failed fits score nothing
     if ((int64_t)h_tiles[i] + t > (1ll << 30))
       return fail(ctx, GPBO_EINVAL, "too many candidates in one call");
     h_tiles[i + 1] = h_tiles[i] + (int32_t)t;
@@ -270,7 +272,8 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   {
     KernTimer t(ctx, kKernFast);
     if (use_tc)
-      CK(gpbo::launch_score_tc(p, tiles, dmax, nmax, ctx->num_sms, ctx->stream));
+      CK(gpbo::launch_score_tc(p, model->meta.data() + s_first, S, tiles, ctx->num_sms,
+                               ctx->stream));
     else
       CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
   }
@@ -454,6 +457,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     q.lt_off = nlt; nlt += (int64_t)q.n_pad * q.n_pad;
     q.a_off = na; na += q.n_pad;
     q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
+    gpbo::tc_fill_geometry(q);
     const int nr = (n + 1) & ~1;
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     const int smem = (3 * nr + (q.use_smem ? n * n : 0)) * 8;
@@ -524,7 +528,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   ctx->launches += 1;
   if (nimg > 0) {
     KernTimer t(ctx, kKernPack);
-    CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs32, m->alpha64, m->img,
+    CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs64, m->alpha64, m->ls32, m->img,
                              ctx->stream));
     ctx->launches += 1;
   }

@@ -32,6 +32,17 @@ struct SearchMeta {
   float pmax;           // max_j |x_j / l|^2 (error-bound input of the fast phase)
   float alpha_max;      // max_j |alpha_j|
   float linv_rowsum;    // max_j sum_k |(L^-1)_jk| (variance error-bound input)
+  // ---- tcgen05 fast phase (score_tc.cu); valid when tc_ok
+  int32_t tc_ok;
+  int32_t n16;          // n rounded up to 16 (V accumulator columns)
+  int32_t kb;           // 16-wide K blocks of the augmented distance operand [x, |x|^2, 1]
+  int32_t npan;         // 32-wide training-point panels
+  int32_t img_bytes;    // operand image bytes (shared-memory resident per search)
+  int32_t off_l, off_a, off_w;  // byte offsets of L^-1 panels, alpha pairs, candidate scales
+  float c0, c1, c2, c3; // kernel-value constants in the scaled MMA units (see pack_tc)
+  float hscale;         // true h = MMA h * hscale
+  float vunscale2;      // |v|^2 = sum of squared V accumulator * vunscale2
+  float pmax_h;         // max_j p^_j in true h units (error-bound input)
   double jitter;
   int32_t jitter_k;
   int32_t status;       // gpbo_status of this search

@@ -70,15 +70,26 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k)
 //                   their key here.
 //   kModePosterior: store var~ for the dense refine pass.
 //   kModeDebug:     store the phase's own values.
+// The group of `nthreads` threads (warps gw0.. of the block, one candidate each) synchronises
+// with named barrier `bar_id` (0 = the whole block).  force_refine: the fast phase could not
+// evaluate this candidate safely (e.g. float16 range) -> EI_hi = +inf.
 __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool valid,
                                             int64_t row0, int64_t row, double mu, float dmu,
-                                            float var, float dvar) {
-  const bool ok = valid && isfinite(mu) && isfinite(var);
+                                            float var, float dvar, bool force_refine = false,
+                                            uint32_t bar_id = 0, uint32_t nthreads = 0,
+                                            int gw0 = 0) {
+  if (nthreads == 0) nthreads = blockDim.x;
+  const bool ok = valid && (force_refine || (isfinite(mu) && isfinite(var)));
   const double best = p.best[s];
   float ei_lo = 0.f, ei_hi = 0.f;
   if (ok && p.mode != kModePosterior) {
-    ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
-    ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
+    if (force_refine) {
+      ei_hi = INFINITY;
+      ei_lo = 0.f;
+    } else {
+      ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
+      ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
+    }
   }
   if (p.mode == kModePosterior) {
     if (valid) p.out_var[row0 + row] = var;
@@ -103,9 +114,9 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
     const unsigned long long q = __shfl_xor_sync(0xffffffffu, zkey, o);
     zkey = q > zkey ? q : zkey;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - gw0, nw = nthreads >> 5;
   if (lane == 0) { s_thr[warp] = lo_bits; s_zk[warp] = zkey; }
-  __syncthreads();
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
   if (warp == 0) {
     unsigned int lb = lane < nw ? s_thr[lane] : 0u;
     unsigned long long zk = lane < nw ? s_zk[lane] : 0ull;
@@ -121,7 +132,7 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
       s_thr[0] = max(old, lb);
     }
   }
-  __syncthreads();
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
   const float thr = __uint_as_float(s_thr[0]);
   const bool flag = ok && ei_hi > 0.f && ei_hi >= thr;
   const unsigned int mask = __ballot_sync(0xffffffffu, flag);

@@ -1,14 +1,582 @@
-// tcgen05 scoring path -- placeholder until the tensor-core kernel lands.
+// Fast phase of H6-H9 on the 5th-generation tensor cores (tcgen05, TMEM, bulk-copy TMA).
+//
+// Per 128-candidate tile (M = 128, cta_group::1), per 32-wide panel p of training points:
+//   (1) distance MMA  h = A_aug . B_aug^T into a TMEM scratch stage, with the augmented operands
+//       A_aug = [x^*, |x^*|^2, 1], B_aug = [-2 x_j, 1, |x_j|^2] (x^ = x/l scaled so that h is
+//       the kernel argument: 5 r^2 for Matern-5/2, r^2/2 for RBF) -- the "GEMM-form squared
+//       distances on tensor cores" of the north star (a);
+//   (2) epilogue warps: tcgen05.ld the scratch, K* = k(h) (MUFU sqrt/ex2 + FMA polynomial),
+//       accumulate mu~ = K* alpha and sum |K* alpha| (mean error bound), split K* into
+//       float16 hi + lo and store the panel as the A operand of (3);
+//   (3) variance MMA  V[:, j >= 32p] += K*_p . (L^-1)[j, k in p]^T  into a TMEM accumulator of
+//       n16 columns: the triangular "panel TRSM" V = L^-1 K*^T of north star (c), with L^-1
+//       inverted at fit time; the k-step 16 of the panel only touches columns j >= 16 s.
+// After the last panel the epilogue drains V (sum V_j^2), forms s2~ = sf2 - |v|^2, EI and the
+// EI bracket, and flags the candidates that can still be the argmax for the float64 refine
+// phase (refine.cu) -- north star (d).
+//
+// Precision: every operand is split x = hi + lo in float16 (hi = x truncated to 11 bits, lo the
+// exact remainder rounded to float16) and each contraction issues hi.hi + hi.lo + lo.hi, giving
+// float32-level (22-bit) products with float32 accumulation; power-of-two scales (pack_tc) keep
+// the float16 operands in range.  1x float16/bf16/tf32 would break the 1e-4 parity
+// (SURVEY.md Appendix A).
+//
+// Warp roles (384 threads, one persistent CTA per SM, static contiguous tile ranges):
+//   warp 0      MMA issuer (one thread)          warps 2-3   candidate loader (X* -> A_aug)
+//   warp 1      TMEM allocator, image TMA        warps 4-11  epilogue (2 warps per TMEM lane
+//                                                            quarter, 16 columns each)
+// Shared memory: the per-search operand image (X^ rows, L^-1 panels, alpha, candidate scales)
+// is loaded once per search segment with one bulk copy and stays resident; the candidate tile
+// and two K* panel stages are the only per-tile operands.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "score_common.cuh"
 #include "score_tc.cuh"
+#include "tc_prims.cuh"
 
 namespace gpbo {
-bool tc_supported(const SearchMeta &) { return false; }
-int64_t tc_image_bytes(const SearchMeta &) { return 0; }
-cudaError_t launch_pack_tc(const SearchMeta *, int, const double *, const float *,
-                           const double *, unsigned char *, cudaStream_t) {
-  return cudaSuccess;
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kScratchCol = 256;
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
+
+enum { B_AFULL = 0, B_AEMPTY, B_DF0, B_DF1, B_DE0, B_DE1, B_KF0, B_KF1, B_KE0, B_KE1, B_VFULL,
+       B_VEMPTY, B_IMG, B_COUNT };
+
+enum : uint32_t { kFlagInvalid = 1u, kFlagUnsafe = 2u };
+
+struct TcGeom {
+  int n16, kb, npan, off_l, off_a, off_w, img;
+};
+
+__host__ __device__ inline int align1k(int v) { return (v + 1023) & ~1023; }
+
+__host__ __device__ inline TcGeom tc_geom(int n, int d) {
+  TcGeom g;
+  g.n16 = (n + 15) & ~15;
+  g.kb = (d + 2 + 15) / 16;
+  g.npan = (g.n16 + 31) / 32;
+  int lrows = 0;
+  for (int p = 0; p < g.npan; ++p) lrows += g.n16 - 32 * p;
+  g.off_l = align1k(g.kb * 2 * g.n16 * 32);
+  g.off_a = align1k(g.off_l + lrows * 128);
+  g.off_w = g.off_a + g.n16 * 8;
+  g.img = align1k(g.off_w + GPBO_MAX_D * 4);
+  return g;
 }
-cudaError_t launch_score_tc(const ScoreLaunch &, int, int, int, int, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+// dynamic shared memory of one launch: image | A tile | K* stages | staging | row info | partials
+struct TcSmem {
+  int img, a, k, stage, rowinfo, part_mu, part_a1, part_vv, bars, total;
+};
+
+__host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
+  TcSmem s;
+  s.img = 0;
+  s.a = img_max;
+  s.k = s.a + kb_max * 8192;
+  s.stage = s.k + 2 * kStageBytes;
+  s.rowinfo = s.stage + ((128 * d_max * 4 + 15) & ~15);
+  s.part_mu = s.rowinfo + 2 * 128 * 8;
+  s.part_a1 = s.part_mu + 2 * 128 * 8;
+  s.part_vv = s.part_a1 + 2 * 128 * 4;
+  s.bars = s.part_vv + 2 * 128 * 4;
+  s.total = s.bars + B_COUNT * 8 + 16 + 1024;  // + tmem slot, + alignment slack
+  return s;
 }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ int search_of(const int32_t *tile_first, int S, int t) {
+  int lo = 0, hi = S;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile_first[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, int d_max) {
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char *sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
+  const TcSmem L = tc_smem(img_max, kb_max, d_max);
+  unsigned char *img = sm + L.img;
+  unsigned char *Abuf = sm + L.a;
+  unsigned char *Kbuf = sm + L.k;
+  float *stage = reinterpret_cast<float *>(sm + L.stage);
+  float2 *rowinfo = reinterpret_cast<float2 *>(sm + L.rowinfo);
+  double *part_mu = reinterpret_cast<double *>(sm + L.part_mu);
+  float *part_a1 = reinterpret_cast<float *>(sm + L.part_a1);
+  float *part_vv = reinterpret_cast<float *>(sm + L.part_vv);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L.bars);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + B_COUNT);
+  auto bar = [&](int i) { return tc::smem_u32(bars + i); };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = (int)((long long)total_tiles * blockIdx.x / gridDim.x);
+  const int t1 = (int)((long long)total_tiles * (blockIdx.x + 1) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    tc::mbar_init(bar(B_AFULL), 64);
+    tc::mbar_init(bar(B_AEMPTY), 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(bar(B_DF0 + i), 1);
+      tc::mbar_init(bar(B_DE0 + i), 8);
+      tc::mbar_init(bar(B_KF0 + i), 8);
+      tc::mbar_init(bar(B_KE0 + i), 1);
+    }
+    tc::mbar_init(bar(B_VFULL), 1);
+    tc::mbar_init(bar(B_VEMPTY), 8);
+    tc::mbar_init(bar(B_IMG), 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tc::smem_u32(tmem_slot), kTmemCols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  uint32_t gi = 0;  // CTA-local tile counter
+  uint32_t gp = 0;  // distance-panel counter (TMEM scratch ring)
+  uint32_t kg = 0;  // K*-panel counter (shared-memory stage ring)
+  uint32_t img_phase = 0;
+  int cur_s = -1;
+
+  for (int t = t0; t < t1; ++t, ++gi) {
+    const int s = search_of(p.tile_first, p.S, t);
+    const SearchMeta &m = p.meta[s];
+    if (s != cur_s) {
+      // new search segment: every role has finished the previous one (the epilogue waited for
+      // the last MMA commit), so the resident image can be replaced
+      __syncthreads();
+      if (threadIdx.x == 32) {
+        tc::mbar_arrive_expect_tx(bar(B_IMG), (uint32_t)m.img_bytes);
+        tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off, (uint32_t)m.img_bytes, bar(B_IMG));
+      }
+      tc::mbar_wait(bar(B_IMG), img_phase);
+      img_phase ^= 1u;
+      cur_s = s;
+    }
+    const int n16 = m.n16, npan = m.npan, kb = m.kb;
+    const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
+    const int64_t row0 = (int64_t)(t - p.tile_first[s]) * 128;
+
+    if (warp == 0) {
+      // ===================================================== MMA issuer
+      if (lane == 0) {
+        tc::mbar_wait(bar(B_AFULL), gi & 1u);
+        tc::tc_fence_after();
+        const uint32_t a0 = tc::smem_u32(Abuf), x0 = tc::smem_u32(img);
+        const uint32_t l0 = tc::smem_u32(img + m.off_l), k0 = tc::smem_u32(Kbuf);
+        auto issue_dist = [&](int pp) {
+          const uint32_t st = gp & 1u;
+          tc::mbar_wait(bar(B_DE0 + st), ((gp >> 1) & 1u) ^ 1u);
+          tc::tc_fence_after();
+          const uint32_t N = (uint32_t)min(32, n16 - 32 * pp);
+          const uint32_t idn = tc::idesc_f16(N);
+          const uint32_t dt = tbase + kScratchCol + 32u * st;
+          for (int k = 0; k < kb; ++k) {
+            const uint32_t ab = a0 + k * 8192;                       // [hi 4096 | lo 4096]
+            const uint32_t bb = x0 + k * 2 * n16 * 32 + pp * 1024;   // rows 32 pp
+            const uint32_t blo = (uint32_t)(n16 * 32);
+            tc::mma_f16(dt, tc::make_sdesc(ab, 32), tc::make_sdesc(bb, 32), idn, k > 0);
+            tc::mma_f16(dt, tc::make_sdesc(ab, 32), tc::make_sdesc(bb + blo, 32), idn, 1u);
+            tc::mma_f16(dt, tc::make_sdesc(ab + 4096, 32), tc::make_sdesc(bb, 32), idn, 1u);
+          }
+          tc::mma_commit(bar(B_DF0 + st));
+          ++gp;
+        };
+        issue_dist(0);
+        if (npan > 1) issue_dist(1);
+        if (npan <= 2) tc::mma_commit(bar(B_AEMPTY));
+        for (int pp = 0; pp < npan; ++pp) {
+          const uint32_t ks = kg & 1u;
+          tc::mbar_wait(bar(B_KF0 + ks), (kg >> 1) & 1u);
+          tc::tc_fence_after();
+          if (pp == 0) {
+            tc::mbar_wait(bar(B_VEMPTY), (gi & 1u) ^ 1u);
+            tc::tc_fence_after();
+          }
+          const uint32_t kbs = k0 + ks * kStageBytes;
+          const int R = n16 - 32 * pp;
+          const uint32_t lp = l0 + (uint32_t)(pp * n16 - 16 * pp * (pp - 1)) * 128u;
+          for (int h = 0; h < 2; ++h) {
+            const int j0 = 32 * pp + 16 * h;
+            if (j0 >= n16) break;
+            const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
+            const uint32_t dt = tbase + (uint32_t)j0;
+            const uint32_t ka = kbs + h * 32;
+            const uint32_t lb = lp + h * 1024 + h * 32;
+            tc::mma_f16(dt, tc::make_sdesc(ka, 64), tc::make_sdesc(lb, 64), idn,
+                        (pp | h) ? 1u : 0u);
+            tc::mma_f16(dt, tc::make_sdesc(ka, 64), tc::make_sdesc(lb + R * 64, 64), idn, 1u);
+            tc::mma_f16(dt, tc::make_sdesc(ka + 8192, 64), tc::make_sdesc(lb, 64), idn, 1u);
+          }
+          tc::mma_commit(bar(B_KE0 + ks));
+          ++kg;
+          if (pp == npan - 1) tc::mma_commit(bar(B_VFULL));
+          if (pp + 2 < npan) {
+            issue_dist(pp + 2);
+            if (pp + 2 == npan - 1) tc::mma_commit(bar(B_AEMPTY));
+          }
+        }
+      }
+      __syncwarp();
+    } else if (warp == 2 || warp == 3) {
+      // ===================================================== candidate loader
+      const int lt = threadIdx.x - 64;
+      const int d = m.d;
+      tc::mbar_wait(bar(B_AEMPTY), (gi & 1u) ^ 1u);
+      const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);
+      const float *src = p.Xstar + p.x_off[s] + row0 * d;
+      for (int e = lt; e < rows * d; e += 64) stage[e] = __ldg(src + e);
+      tc::named_bar_sync(3, 64);
+      const float *w = reinterpret_cast<const float *>(img + m.off_w);
+      const uint32_t a0 = tc::smem_u32(Abuf);
+      for (int r = lt; r < 128; r += 64) {
+        const bool valid = r < rows;
+        float qh = 0.f;
+        bool nan = false;
+        if (valid)
+          for (int c = 0; c < d; ++c) {
+            const float x = stage[r * d + c];
+            nan |= !isfinite(x);
+            const float v = x * w[c];
+            qh = fmaf(v, v, qh);
+          }
+        const bool unsafe = !(qh <= 30000.f);
+        for (int k = 0; k < kb; ++k) {
+          uint32_t hw[8], lw[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float v2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int c = 16 * k + 2 * q + u;
+              float v = 0.f;
+              if (valid && !unsafe) {
+                if (c < d) v = stage[r * d + c] * w[c];
+                else if (c == d) v = qh;
+                else if (c == d + 1) v = 1.f;
+              }
+              v2[u] = v;
+            }
+            const __half2 h2 = __floats2half2_rn(v2[0], v2[1]);
+            const float2 hf = __half22float2(h2);
+            hw[q] = *reinterpret_cast<const uint32_t *>(&h2);
+            lw[q] = tc::pack_f16x2(v2[0] - hf.x, v2[1] - hf.y);
+          }
+          const uint32_t base = a0 + k * 8192;
+          sts128(base + tc::sw_offset(r, 0, 32), hw[0], hw[1], hw[2], hw[3]);
+          sts128(base + tc::sw_offset(r, 16, 32), hw[4], hw[5], hw[6], hw[7]);
+          sts128(base + 4096 + tc::sw_offset(r, 0, 32), lw[0], lw[1], lw[2], lw[3]);
+          sts128(base + 4096 + tc::sw_offset(r, 16, 32), lw[4], lw[5], lw[6], lw[7]);
+        }
+        const uint32_t flags = (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
+        rowinfo[(gi & 1u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
+      }
+      tc::fence_proxy_async();
+      tc::named_bar_sync(3, 64);
+      tc::mbar_arrive(bar(B_AFULL));
+    } else if (warp >= 4) {
+      // ===================================================== epilogue
+      const int lq = warp & 3, half = (warp - 4) >> 2;
+      const int row = 32 * lq + lane;
+      const uint32_t tl = tbase + ((uint32_t)(32 * lq) << 16);
+      const float2 *ap = reinterpret_cast<const float2 *>(img + m.off_a);
+      const int kind = m.kernel;
+      const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
+      const uint32_t k0 = tc::smem_u32(Kbuf);
+      double mu = 0.0;
+      float a1 = 0.f;
+      for (int pp = 0; pp < npan; ++pp) {
+        const uint32_t st = gp & 1u;
+        const int jb = 32 * pp + 16 * half;
+        const bool active = jb < n16;
+        tc::mbar_wait(bar(B_DF0 + st), (gp >> 1) & 1u);
+        tc::tc_fence_after();
+        uint32_t hr[16];
+        if (active) {
+          tc::tmem_ld16(tl + kScratchCol + 32u * st + 16u * half, hr);
+          tc::tmem_wait_ld();
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
+        ++gp;
+        const uint32_t ks = kg & 1u;
+        tc::mbar_wait(bar(B_KE0 + ks), ((kg >> 1) & 1u) ^ 1u);
+        if (active) {
+          float kv[16];
+          float muf = 0.f;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float h = fmaxf(__uint_as_float(hr[q]), 0.f);
+            float kq;
+            if (kind == GPBO_RBF) {
+              kq = ex2_approx(fmaf(h, c1, c0));
+            } else {
+              const float tq = sqrt_approx(h);
+              kq = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
+            }
+            kv[q] = kq;
+            const float2 a = ap[jb + q];
+            muf = fmaf(kq, a.x, muf);
+            a1 = fmaf(kq, a.y, a1);
+          }
+          mu += (double)muf;
+          uint32_t hw[8], lw[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float h0 = __uint_as_float(__float_as_uint(kv[2 * q]) & 0xFFFFE000u);
+            const float h1 = __uint_as_float(__float_as_uint(kv[2 * q + 1]) & 0xFFFFE000u);
+            hw[q] = tc::pack_f16x2(h0, h1);
+            lw[q] = tc::pack_f16x2(kv[2 * q] - h0, kv[2 * q + 1] - h1);
+          }
+          const uint32_t base = k0 + ks * kStageBytes;
+          const uint32_t o0 = tc::sw_offset(row, 32 * half, 64);
+          const uint32_t o1 = tc::sw_offset(row, 32 * half + 16, 64);
+          sts128(base + o0, hw[0], hw[1], hw[2], hw[3]);
+          sts128(base + o1, hw[4], hw[5], hw[6], hw[7]);
+          sts128(base + 8192 + o0, lw[0], lw[1], lw[2], lw[3]);
+          sts128(base + 8192 + o1, lw[4], lw[5], lw[6], lw[7]);
+          tc::fence_proxy_async();
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar(B_KF0 + ks));
+        ++kg;
+      }
+      // drain the V accumulator: sum of squares over this warp's half of the columns
+      tc::mbar_wait(bar(B_VFULL), gi & 1u);
+      tc::tc_fence_after();
+      float vv = 0.f;
+      const int hc = n16 >> 1;
+      for (int c = half * hc; c < (half + 1) * hc; c += 8) {
+        uint32_t r8[8];
+        tc::tmem_ld8(tl + (uint32_t)c, r8);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float v = __uint_as_float(r8[q]);
+          vv = fmaf(v, v, vv);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bar(B_VEMPTY));
+      const int pb = (gi & 1u) * 128;
+      if (half == 1) {
+        part_mu[pb + row] = mu;
+        part_a1[pb + row] = a1;
+        part_vv[pb + row] = vv;
+      }
+      tc::named_bar_sync(1, 256);
+      if (half == 0) {
+        mu += part_mu[pb + row];
+        a1 += part_a1[pb + row];
+        vv += part_vv[pb + row];
+        const float2 ri = rowinfo[pb + row];
+        const uint32_t flags = __float_as_uint(ri.y);
+        const bool valid = (row0 + row < Ms) && !(flags & kFlagInvalid);
+        const float u = 5.9604645e-8f;
+        const float s2 = vv * m.vunscale2;
+        const float sf2 = m.sf2;
+        const float var = fmaxf(sf2 - s2, 0.f);
+        // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for the
+        // float16x3 augmented GEMM; kappa 4 margin
+        const float dmu = u * a1 * (32.f * (ri.x + m.pmax_h) + 128.f);
+        const float dvar = 4.f * var_bound(u, sf2, s2, m.n, m.linv_rowsum);
+        finish_fast(p, s, valid, p.m_off[s], row0 + row, mu, dmu, var, dvar,
+                    (flags & kFlagUnsafe) != 0u, 2, 128, 4);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, kTmemCols);
+}
+
+// ------------------------------------------------------------------ operand images (fit time)
+__device__ double block_max_d(double v, double *red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+// One CTA per search.  Scales (powers of two, exact): x^ = g x/l 2^-e with g = sqrt5 (Matern)
+// or 1/sqrt2 (RBF) and e chosen so max(|x^*|^2 over the unit box, |x^_j|^2) <= 2^13;
+// K* 2^tK <= 2^13; L^-1 2^uL <= 2^14.  V = L^-1 K* then carries 2^(tK + uL).
+__global__ void __launch_bounds__(256)
+pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const double *alpha64,
+               const float *ls32, unsigned char *img_all) {
+  __shared__ double red[8];
+  __shared__ double sc[4];
+  const int s = blockIdx.x;
+  SearchMeta m = meta[s];
+  if (!m.tc_ok || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
+  const int n = m.n, d = m.d;
+  const TcGeom g = tc_geom(n, d);
+  unsigned char *img = img_all + m.img_off;
+  const double *Li = Linv64 + m.mat_off;
+  const double *X = Xs64 + m.x_off;
+  const double gk = m.kernel == GPBO_RBF ? 0.70710678118654752440 : 2.2360679774997896964;
+  double lmax = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) lmax = fmax(lmax, fabs(Li[e]));
+  lmax = block_max_d(lmax, red);
+  if (threadIdx.x == 0) {
+    double qbox = 0.0;
+    for (int c = 0; c < d; ++c) qbox += 1.0 / ((double)ls32[m.ls_off + c] * ls32[m.ls_off + c]);
+    const double Qm = fmax(gk * gk * qbox, gk * gk * (double)m.pmax);
+    const int e = (int)ceil(0.5 * log2(fmax(Qm, 1e-30) / 8192.0));
+    const int tK = (int)floor(log2(8192.0 / (double)m.sf2));
+    const int uL = (int)floor(log2(16384.0 / fmax(lmax, 1e-300)));
+    sc[0] = ldexp(gk, -e);   // x^ = x/l * sc0
+    sc[1] = (double)e;
+    sc[2] = (double)tK;
+    sc[3] = (double)uL;
+    const double sf2 = m.sf2;
+    const double log2e = 1.4426950408889634074;
+    const double c0 = ldexp(sf2, tK);
+    if (m.kernel == GPBO_RBF) {
+      m.c0 = (float)log2(c0);
+      m.c1 = (float)(-ldexp(1.0, 2 * e) * log2e);
+      m.c2 = m.c3 = 0.f;
+    } else {
+      m.c0 = (float)c0;
+      m.c1 = (float)(-ldexp(1.0, e) * log2e);
+      m.c2 = (float)ldexp(c0, e);
+      m.c3 = (float)(ldexp(c0, 2 * e) / 3.0);
+    }
+    m.hscale = (float)ldexp(1.0, 2 * e);
+    m.vunscale2 = (float)ldexp(1.0, -2 * (tK + uL));
+    m.pmax_h = (float)(gk * gk * (double)m.pmax);
+    meta[s] = m;
+  }
+  __syncthreads();
+  const double xs = sc[0];
+  const int e = (int)sc[1], tK = (int)sc[2], uL = (int)sc[3];
+  auto put = [&](unsigned char *base_hi, unsigned char *base_lo, uint32_t off, double v) {
+    const __half hi = __double2half(v);
+    const __half lo = __double2half(v - (double)__half2float(hi));
+    *reinterpret_cast<__half *>(base_hi + off) = hi;
+    *reinterpret_cast<__half *>(base_lo + off) = lo;
+  };
+  // augmented training operand [-2 x^_j, 1, |x^_j|^2], K blocks of 16, rows n16
+  for (int idx = threadIdx.x; idx < g.n16 * g.kb * 16; idx += blockDim.x) {
+    const int j = idx / (g.kb * 16), k = idx % (g.kb * 16);
+    double v = 0.0;
+    if (j < n) {
+      if (k < d) v = -2.0 * xs * X[j * d + k];
+      else if (k == d) v = 1.0;
+      else if (k == d + 1) {
+        double pj = 0.0;
+        for (int c = 0; c < d; ++c) pj += (xs * X[j * d + c]) * (xs * X[j * d + c]);
+        v = pj;
+      }
+    }
+    const int kblk = k >> 4;
+    unsigned char *hi = img + kblk * 2 * g.n16 * 32;
+    put(hi, hi + g.n16 * 32, tc::sw_offset(j, (k & 15) * 2, 32), v);
+  }
+  // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32)
+  for (int pp = 0; pp < g.npan; ++pp) {
+    const int R = g.n16 - 32 * pp;
+    unsigned char *hi = img + g.off_l + (pp * g.n16 - 16 * pp * (pp - 1)) * 128;
+    for (int idx = threadIdx.x; idx < R * 32; idx += blockDim.x) {
+      const int r = idx >> 5, k = idx & 31;
+      const int j = 32 * pp + r, kk = 32 * pp + k;
+      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)kk * n + j], uL) : 0.0;
+      put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
+    }
+  }
+  float2 *ap = reinterpret_cast<float2 *>(img + g.off_a);
+  for (int j = threadIdx.x; j < g.n16; j += blockDim.x) {
+    const double a = j < n ? alpha64[m.a_off + j] : 0.0;
+    ap[j] = make_float2((float)ldexp(a, -tK), (float)ldexp(fabs(a), -tK));
+  }
+  float *wp = reinterpret_cast<float *>(img + g.off_w);
+  for (int c = threadIdx.x; c < GPBO_MAX_D; c += blockDim.x)
+    wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
+  (void)e;
+}
+
+}  // namespace
+
+bool tc_supported(const SearchMeta &m) {
+  if (m.n16 > 256 || m.d + 2 > 64 || !m.tc_ok) return false;
+  const TcGeom g = tc_geom(m.n, m.d);
+  return tc_smem(g.img, g.kb, m.d).total <= kMaxSmem;
+}
+
+int64_t tc_image_bytes(const SearchMeta &m) {
+  const TcGeom g = tc_geom(m.n, m.d);
+  if (g.n16 > 256 || m.d + 2 > 64) return 0;
+  if (tc_smem(g.img, g.kb, m.d).total > kMaxSmem) return 0;
+  return g.img;
+}
+
+void tc_fill_geometry(SearchMeta &m) {
+  const TcGeom g = tc_geom(m.n, m.d);
+  m.n16 = g.n16;
+  m.kb = g.kb;
+  m.npan = g.npan;
+  m.img_bytes = g.img;
+  m.off_l = g.off_l;
+  m.off_a = g.off_a;
+  m.off_w = g.off_w;
+  m.tc_ok = tc_image_bytes(m) > 0;
+}
+
+cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64,
+                           const double *Xs64, const double *alpha64, const float *ls32,
+                           unsigned char *img, cudaStream_t stream) {
+  pack_tc_kernel<<<S, 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
+                                        alpha64, ls32, img);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int S,
+                            int total_tiles, int num_sms, cudaStream_t stream) {
+  int img_max = 0, kb_max = 1, d_max = 1;
+  for (int i = 0; i < S; ++i) {
+    img_max = std::max(img_max, meta_h[i].img_bytes);
+    kb_max = std::max(kb_max, meta_h[i].kb);
+    d_max = std::max(d_max, meta_h[i].d);
+  }
+  const int smem = tc_smem(img_max, kb_max, d_max).total;
+  if (smem > kMaxSmem) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(score_tc_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = std::min(num_sms, total_tiles);
+  score_tc_kernel<<<grid, kThreads, smem, stream>>>(p, total_tiles, img_max, kb_max, d_max);
+  return cudaGetLastError();
+}
+
 }  // namespace gpbo

@@ -66,6 +66,7 @@ def load():
         "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
         "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
         "gpbo_debug_fast_phase": (C.c_int, [vp, vp, i32, vp, i64] + [vp] * 6),
+        "gpbo_tc_selftest": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -81,7 +82,7 @@ def exported_symbols():
             "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
-            "gpbo_debug_fast_phase"]
+            "gpbo_debug_fast_phase", "gpbo_tc_selftest"]
 
 
 def _is_torch(a):
@@ -281,6 +282,18 @@ class Context:
             base.ctypes.data if base is not None else None,
             b.ctypes.data if b is not None else None, mem, idx.ctypes.data, ei.ctypes.data))
         return idx, ei
+
+
+def tc_selftest(A, B, row_bytes, b_row_off=0):
+    """D = A B^T through the tcgen05 path (A: 128 x K, B: N x K fp16 CUDA tensors)."""
+    import torch
+    N, K = B.shape
+    D = torch.empty(128, N, dtype=torch.float32, device=A.device)
+    st = load().gpbo_tc_selftest(A.data_ptr(), B.data_ptr(), D.data_ptr(), N, K, row_bytes,
+                                 b_row_off)
+    if st != OK:
+        raise GpboError(st, "tc_selftest failed")
+    return D
 
 
 def version():
