@@ -42,12 +42,18 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kScratchCol = 256;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
+constexpr int kDepth = 3;           // distance scratch stages (TMEM) issued ahead of the V MMAs
+constexpr int kVBufMaxN = 208;      // n16 <= 208: two V accumulators (2 x 208 + 3 x 32 = 512)
 
-enum { B_AFULL = 0, B_AEMPTY, B_DF0, B_DF1, B_DE0, B_DE1, B_KF0, B_KF1, B_KE0, B_KE1, B_VFULL,
-       B_VEMPTY, B_IMG, B_COUNT };
+enum {
+  B_AF0 = 0, B_AF1, B_AE0, B_AE1,           // candidate A tile (double buffer)
+  B_DF0, B_DF1, B_DF2, B_DE0, B_DE1, B_DE2, // distance scratch ring
+  B_KF0, B_KF1, B_KE0, B_KE1,               // K* panel stages
+  B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
+  B_IMG, B_COUNT
+};
 
 enum : uint32_t { kFlagInvalid = 1u, kFlagUnsafe = 2u };
 
@@ -71,7 +77,7 @@ __host__ __device__ inline TcGeom tc_geom(int n, int d) {
   return g;
 }
 
-// dynamic shared memory of one launch: image | A tile | K* stages | staging | row info | partials
+// dynamic shared memory: image | A tiles x2 | K* stages x2 | staging | row info x4 | partials x2
 struct TcSmem {
   int img, a, k, stage, rowinfo, part_mu, part_a1, part_vv, bars, total;
 };
@@ -80,10 +86,10 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   TcSmem s;
   s.img = 0;
   s.a = img_max;
-  s.k = s.a + kb_max * 8192;
+  s.k = s.a + 2 * kb_max * 8192;
   s.stage = s.k + 2 * kStageBytes;
   s.rowinfo = s.stage + ((128 * d_max * 4 + 15) & ~15);
-  s.part_mu = s.rowinfo + 2 * 128 * 8;
+  s.part_mu = s.rowinfo + 4 * 128 * 8;
   s.part_a1 = s.part_mu + 2 * 128 * 8;
   s.part_vv = s.part_a1 + 2 * 128 * 4;
   s.bars = s.part_vv + 2 * 128 * 4;
@@ -139,16 +145,18 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
   const int t1 = (int)((long long)total_tiles * (blockIdx.x + 1) / gridDim.x);
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(bar(B_AFULL), 64);
-    tc::mbar_init(bar(B_AEMPTY), 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(bar(B_DF0 + i), 1);
-      tc::mbar_init(bar(B_DE0 + i), 8);
+      tc::mbar_init(bar(B_AF0 + i), 64);
+      tc::mbar_init(bar(B_AE0 + i), 1);
       tc::mbar_init(bar(B_KF0 + i), 8);
       tc::mbar_init(bar(B_KE0 + i), 1);
+      tc::mbar_init(bar(B_VF0 + i), 1);
+      tc::mbar_init(bar(B_VE0 + i), 8);
     }
-    tc::mbar_init(bar(B_VFULL), 1);
-    tc::mbar_init(bar(B_VEMPTY), 8);
+    for (int i = 0; i < kDepth; ++i) {
+      tc::mbar_init(bar(B_DF0 + i), 1);
+      tc::mbar_init(bar(B_DE0 + i), 8);
+    }
     tc::mbar_init(bar(B_IMG), 1);
     tc::fence_mbar_init();
   }
@@ -158,75 +166,88 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
   tc::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  uint32_t gi = 0;  // CTA-local tile counter
-  uint32_t gp = 0;  // distance-panel counter (TMEM scratch ring)
-  uint32_t kg = 0;  // K*-panel counter (shared-memory stage ring)
+  // Counters are CTA-global across segments (mbarrier phases continue): tiles gi, distance
+  // panels gd, K* panels gk.  Every role advances them identically.
+  uint32_t gi = 0, gd_seg = 0, gk_seg = 0;
   uint32_t img_phase = 0;
-  int cur_s = -1;
 
-  for (int t = t0; t < t1; ++t, ++gi) {
-    const int s = search_of(p.tile_first, p.S, t);
+  for (int ta = t0; ta < t1;) {
+    // ---------------- segment [ta, tb): consecutive tiles of one search
+    const int s = search_of(p.tile_first, p.S, ta);
+    const int tb = min(t1, p.tile_first[s + 1]);
     const SearchMeta &m = p.meta[s];
-    if (s != cur_s) {
-      // new search segment: every role has finished the previous one (the epilogue waited for
-      // the last MMA commit), so the resident image can be replaced
-      __syncthreads();
-      if (threadIdx.x == 32) {
-        tc::mbar_arrive_expect_tx(bar(B_IMG), (uint32_t)m.img_bytes);
-        tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off, (uint32_t)m.img_bytes, bar(B_IMG));
-      }
-      tc::mbar_wait(bar(B_IMG), img_phase);
-      img_phase ^= 1u;
-      cur_s = s;
+    __syncthreads();  // previous segment fully drained (epilogue consumed the last commit)
+    if (threadIdx.x == 32) {
+      tc::mbar_arrive_expect_tx(bar(B_IMG), (uint32_t)m.img_bytes);
+      tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off, (uint32_t)m.img_bytes, bar(B_IMG));
     }
+    tc::mbar_wait(bar(B_IMG), img_phase);
+    img_phase ^= 1u;
     const int n16 = m.n16, npan = m.npan, kb = m.kb;
+    const int T = tb - ta;
+    const int P = T * npan;
+    const int nvbuf = n16 <= kVBufMaxN ? 2 : 1;
+    const uint32_t scratch0 = nvbuf == 2 ? 2u * kVBufMaxN : 256u;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
-    const int64_t row0 = (int64_t)(t - p.tile_first[s]) * 128;
+    const int tile0 = ta - p.tile_first[s];  // local index of the segment's first tile
 
     if (warp == 0) {
-      // ===================================================== MMA issuer
+      // ===================================================== MMA issuer (one thread)
       if (lane == 0) {
-        tc::mbar_wait(bar(B_AFULL), gi & 1u);
-        tc::tc_fence_after();
-        const uint32_t a0 = tc::smem_u32(Abuf), x0 = tc::smem_u32(img);
+        const uint32_t x0 = tc::smem_u32(img);
         const uint32_t l0 = tc::smem_u32(img + m.off_l), k0 = tc::smem_u32(Kbuf);
-        auto issue_dist = [&](int pp) {
-          const uint32_t st = gp & 1u;
-          tc::mbar_wait(bar(B_DE0 + st), ((gp >> 1) & 1u) ^ 1u);
-          tc::tc_fence_after();
-          const uint32_t N = (uint32_t)min(32, n16 - 32 * pp);
-          const uint32_t idn = tc::idesc_f16(N);
-          const uint32_t dt = tbase + kScratchCol + 32u * st;
-          for (int k = 0; k < kb; ++k) {
-            const uint32_t ab = a0 + k * 8192;                       // [hi 4096 | lo 4096]
-            const uint32_t bb = x0 + k * 2 * n16 * 32 + pp * 1024;   // rows 32 pp
-            const uint32_t blo = (uint32_t)(n16 * 32);
-            tc::mma_f16(dt, tc::make_sdesc(ab, 32), tc::make_sdesc(bb, 32), idn, k > 0);
-            tc::mma_f16(dt, tc::make_sdesc(ab, 32), tc::make_sdesc(bb + blo, 32), idn, 1u);
-            tc::mma_f16(dt, tc::make_sdesc(ab + 4096, 32), tc::make_sdesc(bb, 32), idn, 1u);
+        uint32_t gd = gd_seg, gk = gk_seg;
+        int nd = 0;  // next distance panel of the segment
+        for (int g = 0; g < P; ++g) {
+          // keep kDepth distance panels in flight ahead of the variance MMAs
+          while (nd < P && nd < g + kDepth) {
+            const int tl = nd / npan, pp = nd - tl * npan;
+            const uint32_t ti = gi + tl, ab = ti & 1u;
+            if (pp == 0) {
+              tc::mbar_wait(bar(B_AF0 + ab), (ti >> 1) & 1u);
+              tc::tc_fence_after();
+            }
+            const uint32_t st = gd % kDepth;
+            tc::mbar_wait(bar(B_DE0 + st), ((gd / kDepth) & 1u) ^ 1u);
+            tc::tc_fence_after();
+            const uint32_t N = (uint32_t)min(32, n16 - 32 * pp);
+            const uint32_t idn = tc::idesc_f16(N);
+            const uint32_t dt = tbase + scratch0 + 32u * st;
+            const uint32_t a0 = tc::smem_u32(Abuf) + ab * kb * 8192;
+            for (int k = 0; k < kb; ++k) {
+              const uint32_t aa = a0 + k * 8192;                       // [hi 4096 | lo 4096]
+              const uint32_t bb = x0 + k * 2 * n16 * 32 + pp * 1024;   // rows 32 pp
+              const uint32_t blo = (uint32_t)(n16 * 32);
+              tc::mma_f16(dt, tc::make_sdesc(aa, 32), tc::make_sdesc(bb, 32), idn, k > 0);
+              tc::mma_f16(dt, tc::make_sdesc(aa, 32), tc::make_sdesc(bb + blo, 32), idn, 1u);
+              tc::mma_f16(dt, tc::make_sdesc(aa + 4096, 32), tc::make_sdesc(bb, 32), idn, 1u);
+            }
+            tc::mma_commit(bar(B_DF0 + st));
+            if (pp == npan - 1) tc::mma_commit(bar(B_AE0 + ab));  // A tile consumed
+            ++gd;
+            ++nd;
           }
-          tc::mma_commit(bar(B_DF0 + st));
-          ++gp;
-        };
-        issue_dist(0);
-        if (npan > 1) issue_dist(1);
-        if (npan <= 2) tc::mma_commit(bar(B_AEMPTY));
-        for (int pp = 0; pp < npan; ++pp) {
-          const uint32_t ks = kg & 1u;
-          tc::mbar_wait(bar(B_KF0 + ks), (kg >> 1) & 1u);
+          // variance MMAs of panel g
+          const int tl = g / npan, pp = g - tl * npan;
+          const uint32_t ti = gi + tl;
+          const uint32_t vb = nvbuf == 2 ? (ti & 1u) : 0u;
+          const uint32_t vuse = nvbuf == 2 ? (ti >> 1) : ti;  // uses of this V buffer so far
+          const uint32_t ks = gk & 1u;
+          tc::mbar_wait(bar(B_KF0 + ks), (gk >> 1) & 1u);
           tc::tc_fence_after();
           if (pp == 0) {
-            tc::mbar_wait(bar(B_VEMPTY), (gi & 1u) ^ 1u);
+            tc::mbar_wait(bar(B_VE0 + vb), (vuse & 1u) ^ 1u);
             tc::tc_fence_after();
           }
           const uint32_t kbs = k0 + ks * kStageBytes;
           const int R = n16 - 32 * pp;
           const uint32_t lp = l0 + (uint32_t)(pp * n16 - 16 * pp * (pp - 1)) * 128u;
+          const uint32_t vcol = tbase + vb * kVBufMaxN;
           for (int h = 0; h < 2; ++h) {
             const int j0 = 32 * pp + 16 * h;
             if (j0 >= n16) break;
             const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
-            const uint32_t dt = tbase + (uint32_t)j0;
+            const uint32_t dt = vcol + (uint32_t)j0;
             const uint32_t ka = kbs + h * 32;
             const uint32_t lb = lp + h * 1024 + h * 32;
             tc::mma_f16(dt, tc::make_sdesc(ka, 64), tc::make_sdesc(lb, 64), idn,
@@ -235,12 +256,8 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             tc::mma_f16(dt, tc::make_sdesc(ka + 8192, 64), tc::make_sdesc(lb, 64), idn, 1u);
           }
           tc::mma_commit(bar(B_KE0 + ks));
-          ++kg;
-          if (pp == npan - 1) tc::mma_commit(bar(B_VFULL));
-          if (pp + 2 < npan) {
-            issue_dist(pp + 2);
-            if (pp + 2 == npan - 1) tc::mma_commit(bar(B_AEMPTY));
-          }
+          ++gk;
+          if (pp == npan - 1) tc::mma_commit(bar(B_VF0 + vb));
         }
       }
       __syncwarp();
@@ -248,89 +265,158 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
       // ===================================================== candidate loader
       const int lt = threadIdx.x - 64;
       const int d = m.d;
-      tc::mbar_wait(bar(B_AEMPTY), (gi & 1u) ^ 1u);
-      const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);
-      const float *src = p.Xstar + p.x_off[s] + row0 * d;
-      for (int e = lt; e < rows * d; e += 64) stage[e] = __ldg(src + e);
-      tc::named_bar_sync(3, 64);
       const float *w = reinterpret_cast<const float *>(img + m.off_w);
-      const uint32_t a0 = tc::smem_u32(Abuf);
-      for (int r = lt; r < 128; r += 64) {
-        const bool valid = r < rows;
-        float qh = 0.f;
-        bool nan = false;
-        if (valid)
-          for (int c = 0; c < d; ++c) {
-            const float x = stage[r * d + c];
-            nan |= !isfinite(x);
-            const float v = x * w[c];
-            qh = fmaf(v, v, qh);
-          }
-        const bool unsafe = !(qh <= 30000.f);
-        for (int k = 0; k < kb; ++k) {
-          uint32_t hw[8], lw[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float v2[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int c = 16 * k + 2 * q + u;
-              float v = 0.f;
-              if (valid && !unsafe) {
-                if (c < d) v = stage[r * d + c] * w[c];
-                else if (c == d) v = qh;
-                else if (c == d + 1) v = 1.f;
-              }
-              v2[u] = v;
+      for (int tl = 0; tl < T; ++tl) {
+        const uint32_t ti = gi + tl, ab = ti & 1u;
+        const int64_t row0 = (int64_t)(tile0 + tl) * 128;
+        tc::mbar_wait(bar(B_AE0 + ab), ((ti >> 1) & 1u) ^ 1u);
+        const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);
+        const float *src = p.Xstar + p.x_off[s] + row0 * d;
+        for (int e = lt; e < rows * d; e += 64) stage[e] = __ldg(src + e);
+        tc::named_bar_sync(3, 64);
+        const uint32_t a0 = tc::smem_u32(Abuf) + ab * kb * 8192;
+        for (int r = lt; r < 128; r += 64) {
+          const bool valid = r < rows;
+          float qh = 0.f;
+          bool nan = false;
+          if (valid)
+            for (int c = 0; c < d; ++c) {
+              const float x = stage[r * d + c];
+              nan |= !isfinite(x);
+              const float v = x * w[c];
+              qh = fmaf(v, v, qh);
             }
-            const __half2 h2 = __floats2half2_rn(v2[0], v2[1]);
-            const float2 hf = __half22float2(h2);
-            hw[q] = *reinterpret_cast<const uint32_t *>(&h2);
-            lw[q] = tc::pack_f16x2(v2[0] - hf.x, v2[1] - hf.y);
+          const bool unsafe = !(qh <= 30000.f);
+          for (int k = 0; k < kb; ++k) {
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float v2[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int c = 16 * k + 2 * q + u;
+                float v = 0.f;
+                if (valid && !unsafe) {
+                  if (c < d) v = stage[r * d + c] * w[c];
+                  else if (c == d) v = qh;
+                  else if (c == d + 1) v = 1.f;
+                }
+                v2[u] = v;
+              }
+              const __half2 h2 = __floats2half2_rn(v2[0], v2[1]);
+              const float2 hf = __half22float2(h2);
+              hw[q] = *reinterpret_cast<const uint32_t *>(&h2);
+              lw[q] = tc::pack_f16x2(v2[0] - hf.x, v2[1] - hf.y);
+            }
+            const uint32_t base = a0 + k * 8192;
+            sts128(base + tc::sw_offset(r, 0, 32), hw[0], hw[1], hw[2], hw[3]);
+            sts128(base + tc::sw_offset(r, 16, 32), hw[4], hw[5], hw[6], hw[7]);
+            sts128(base + 4096 + tc::sw_offset(r, 0, 32), lw[0], lw[1], lw[2], lw[3]);
+            sts128(base + 4096 + tc::sw_offset(r, 16, 32), lw[4], lw[5], lw[6], lw[7]);
           }
-          const uint32_t base = a0 + k * 8192;
-          sts128(base + tc::sw_offset(r, 0, 32), hw[0], hw[1], hw[2], hw[3]);
-          sts128(base + tc::sw_offset(r, 16, 32), hw[4], hw[5], hw[6], hw[7]);
-          sts128(base + 4096 + tc::sw_offset(r, 0, 32), lw[0], lw[1], lw[2], lw[3]);
-          sts128(base + 4096 + tc::sw_offset(r, 16, 32), lw[4], lw[5], lw[6], lw[7]);
+          const uint32_t flags =
+              (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
+          rowinfo[(ti & 3u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
         }
-        const uint32_t flags = (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
-        rowinfo[(gi & 1u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
+        tc::fence_proxy_async();
+        tc::named_bar_sync(3, 64);
+        tc::mbar_arrive(bar(B_AF0 + ab));
       }
-      tc::fence_proxy_async();
-      tc::named_bar_sync(3, 64);
-      tc::mbar_arrive(bar(B_AFULL));
     } else if (warp >= 4) {
       // ===================================================== epilogue
       const int lq = warp & 3, half = (warp - 4) >> 2;
       const int row = 32 * lq + lane;
-      const uint32_t tl = tbase + ((uint32_t)(32 * lq) << 16);
+      const uint32_t tl_addr = tbase + ((uint32_t)(32 * lq) << 16);
       const float2 *ap = reinterpret_cast<const float2 *>(img + m.off_a);
       const int kind = m.kernel;
       const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
       const uint32_t k0 = tc::smem_u32(Kbuf);
+      uint32_t gd = gd_seg, gk = gk_seg;
       double mu = 0.0;
       float a1 = 0.f;
-      for (int pp = 0; pp < npan; ++pp) {
-        const uint32_t st = gp & 1u;
+      // drain + finish of segment tile tl (V accumulator complete); called one panel late
+      auto drain_finish = [&](int tl, double mu_t, float a1_t) {
+        const uint32_t ti = gi + tl;
+        const uint32_t vb = nvbuf == 2 ? (ti & 1u) : 0u;
+        const uint32_t vuse = nvbuf == 2 ? (ti >> 1) : ti;
+        tc::mbar_wait(bar(B_VF0 + vb), vuse & 1u);
+        tc::tc_fence_after();
+        float vv = 0.f;
+        const int hc = n16 >> 1;
+        const uint32_t va = tl_addr + vb * kVBufMaxN;
+        int c = half * hc;
+        const int ce = c + hc;
+        for (; c + 16 <= ce; c += 16) {
+          uint32_t r16[16];
+          tc::tmem_ld16(va + (uint32_t)c, r16);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float v = __uint_as_float(r16[q]);
+            vv = fmaf(v, v, vv);
+          }
+        }
+        if (c < ce) {
+          uint32_t r8[8];
+          tc::tmem_ld8(va + (uint32_t)c, r8);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float v = __uint_as_float(r8[q]);
+            vv = fmaf(v, v, vv);
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar(B_VE0 + vb));
+        const int pb = (ti & 1u) * 128;
+        if (half == 1) {
+          part_mu[pb + row] = mu_t;
+          part_a1[pb + row] = a1_t;
+          part_vv[pb + row] = vv;
+        }
+        tc::named_bar_sync(1, 256);
+        if (half == 0) {
+          mu_t += part_mu[pb + row];
+          a1_t += part_a1[pb + row];
+          vv += part_vv[pb + row];
+          const float2 ri = rowinfo[(ti & 3u) * 128 + row];
+          const uint32_t flags = __float_as_uint(ri.y);
+          const int64_t rloc = (int64_t)(tile0 + tl) * 128 + row;
+          const bool valid = (rloc < Ms) && !(flags & kFlagInvalid);
+          const float u = 5.9604645e-8f;
+          const float s2 = vv * m.vunscale2;
+          const float sf2 = m.sf2;
+          const float var = fmaxf(sf2 - s2, 0.f);
+          // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for
+          // the float16x3 augmented GEMM; margin x4
+          const float dmu = u * a1_t * (32.f * (ri.x + m.pmax_h) + 128.f);
+          const float dvar = 4.f * var_bound(u, sf2, s2, m.n, m.linv_rowsum);
+          finish_fast(p, s, valid, p.m_off[s], rloc, mu_t, dmu, var, dvar,
+                      (flags & kFlagUnsafe) != 0u, 2, 128, 4);
+        }
+      };
+      for (int g = 0; g < P; ++g) {
+        const int tl = g / npan, pp = g - tl * npan;
+        const uint32_t st = gd % kDepth;
         const int jb = 32 * pp + 16 * half;
         const bool active = jb < n16;
-        tc::mbar_wait(bar(B_DF0 + st), (gp >> 1) & 1u);
+        tc::mbar_wait(bar(B_DF0 + st), (gd / kDepth) & 1u);
         tc::tc_fence_after();
         uint32_t hr[16];
         if (active) {
-          tc::tmem_ld16(tl + kScratchCol + 32u * st + 16u * half, hr);
+          tc::tmem_ld16(tl_addr + scratch0 + 32u * st + 16u * half, hr);
           tc::tmem_wait_ld();
         }
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
-        ++gp;
-        const uint32_t ks = kg & 1u;
-        tc::mbar_wait(bar(B_KE0 + ks), ((kg >> 1) & 1u) ^ 1u);
+        ++gd;
+        const uint32_t ks = gk & 1u;
+        tc::mbar_wait(bar(B_KE0 + ks), ((gk >> 1) & 1u) ^ 1u);
+        float muf = 0.f, a1f = 0.f;
         if (active) {
           float kv[16];
-          float muf = 0.f;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float h = fmaxf(__uint_as_float(hr[q]), 0.f);
@@ -344,9 +430,8 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             kv[q] = kq;
             const float2 a = ap[jb + q];
             muf = fmaf(kq, a.x, muf);
-            a1 = fmaf(kq, a.y, a1);
+            a1f = fmaf(kq, a.y, a1f);
           }
-          mu += (double)muf;
           uint32_t hw[8], lw[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -366,52 +451,23 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_KF0 + ks));
-        ++kg;
-      }
-      // drain the V accumulator: sum of squares over this warp's half of the columns
-      tc::mbar_wait(bar(B_VFULL), gi & 1u);
-      tc::tc_fence_after();
-      float vv = 0.f;
-      const int hc = n16 >> 1;
-      for (int c = half * hc; c < (half + 1) * hc; c += 8) {
-        uint32_t r8[8];
-        tc::tmem_ld8(tl + (uint32_t)c, r8);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float v = __uint_as_float(r8[q]);
-          vv = fmaf(v, v, vv);
+        ++gk;
+        if (pp == 0 && tl > 0) {
+          // tile tl-1 is complete: drain it now, one panel late, so the V MMAs never wait
+          drain_finish(tl - 1, mu, a1);
+          mu = (double)muf;
+          a1 = a1f;
+        } else {
+          mu += (double)muf;
+          a1 += a1f;
         }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(bar(B_VEMPTY));
-      const int pb = (gi & 1u) * 128;
-      if (half == 1) {
-        part_mu[pb + row] = mu;
-        part_a1[pb + row] = a1;
-        part_vv[pb + row] = vv;
-      }
-      tc::named_bar_sync(1, 256);
-      if (half == 0) {
-        mu += part_mu[pb + row];
-        a1 += part_a1[pb + row];
-        vv += part_vv[pb + row];
-        const float2 ri = rowinfo[pb + row];
-        const uint32_t flags = __float_as_uint(ri.y);
-        const bool valid = (row0 + row < Ms) && !(flags & kFlagInvalid);
-        const float u = 5.9604645e-8f;
-        const float s2 = vv * m.vunscale2;
-        const float sf2 = m.sf2;
-        const float var = fmaxf(sf2 - s2, 0.f);
-        // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for the
-        // float16x3 augmented GEMM; kappa 4 margin
-        const float dmu = u * a1 * (32.f * (ri.x + m.pmax_h) + 128.f);
-        const float dvar = 4.f * var_bound(u, sf2, s2, m.n, m.linv_rowsum);
-        finish_fast(p, s, valid, p.m_off[s], row0 + row, mu, dmu, var, dvar,
-                    (flags & kFlagUnsafe) != 0u, 2, 128, 4);
-      }
+      if (P > 0) drain_finish(T - 1, mu, a1);
     }
+    gi += (uint32_t)T;
+    gd_seg += (uint32_t)P;
+    gk_seg += (uint32_t)P;
+    ta = tb;
   }
   tc::tc_fence_before();
   __syncthreads();
