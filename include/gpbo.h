@@ -172,6 +172,15 @@ gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms
  * `b_row_off` (multiple of 8) of its shared-memory tile, accumulator in TMEM.  Synchronous. */
 gpbo_status gpbo_tc_selftest(const void *A, const void *B, float *D, int N, int K, int row_bytes,
                              int b_row_off);
+/* Same, followed by `reps` back-to-back accumulate MMAs of shape 128 x N x 16 issued by one warp;
+ * cycles[0] = clock64 cycles to issue them, cycles[1] = until the last one completed (host). */
+gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int N, int K, int row_bytes,
+                          int b_row_off, int reps, long long *cycles);
+
+/* Test hook: if dev_buf (device, >= 65536 uint64) is non-NULL, the tcgen05 kernel of later
+ * scoring calls records clock64 pipeline events of CTA 0 into it (entry 0 = count, then
+ * (tag << 56 | role << 48 | panel) / clock pairs).  NULL disables. */
+gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf);
 
 /* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,

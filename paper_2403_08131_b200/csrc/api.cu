@@ -40,7 +40,8 @@ struct gpbo_ctx {
   double kern_ms[4] = {0, 0, 0, 0};
   int64_t kern_count[4] = {0, 0, 0, 0};
   int64_t last_refine = 0;
-  int last_impl = 0;        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
+  int last_impl = 0;
+  unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05
 };
@@ -266,6 +267,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.list_cap = (uint32_t)std::min<size_t>(ctx->list_cap, 0xFFFFFFFFu);
   p.dbg_mu = out.dbg[0]; p.dbg_dmu = out.dbg[1]; p.dbg_var = out.dbg[2];
   p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
+  p.trace = ctx->trace;
   const int tiles = h_tiles[S];
   ctx->last_impl = use_tc ? 2 : 1;
   if (tiles == 0) return GPBO_OK;
@@ -384,6 +386,12 @@ int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_ref
 
 int gpbo_last_score_impl(const gpbo_ctx *ctx) { return ctx ? ctx->last_impl : -1; }
 
+gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf) {
+  if (!ctx) return GPBO_EINVAL;
+  ctx->trace = (unsigned long long *)dev_buf;
+  return GPBO_OK;
+}
+
 gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on) {
   if (!ctx) return GPBO_EINVAL;
   cudaStreamSynchronize(ctx->stream);
@@ -460,7 +468,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     gpbo::tc_fill_geometry(q);
     const int nr = (n + 1) & ~1;
     q.use_smem = n <= gpbo::kFitSmemMaxN;
-    const int smem = (3 * nr + (q.use_smem ? n * n : 0)) * 8;
+    const int smem = (3 * nr + (q.use_smem ? n * (n + 1) / 2 : 0)) * 8;
     smem_max = std::max(smem_max, smem);
     m->nmax = std::max(m->nmax, n);
     m->dmax = std::max(m->dmax, q.d_pad);

@@ -4,10 +4,11 @@
 // PAPER.md L249/L256 (§IV.D): the GP's "O(N^3) training complexity" is this factorisation.
 // The kernel/jitter/standardisation readings are R1, R2, R7, R9 of DESIGN.md.
 //
-// Layout: the working matrix A is n x n float64, column-major (column j contiguous), lower
-// triangle used.  For n <= kFitSmemMaxN it lives in shared memory; otherwise the CTA works in
-// place in the model's global Linv64 buffer (L2 resident).  All accesses go through generic
-// pointers, so the same code serves both cases.
+// Layout: the working matrix A is the lower triangle of an n x n float64 matrix, column-major
+// (column j contiguous from its diagonal down).  For n <= kFitSmemMaxN it lives in shared memory,
+// packed (column j starts at j n - j (j - 1) / 2, 216 KB at n = 232); otherwise the CTA works in
+// place, unpacked, in the model's global Linv64 buffer (L2 resident).  Accesses go through the
+// column-base function cb(j) and generic pointers, so the same code serves both cases.
 #include <cmath>
 
 #include "gpbo_internal.cuh"
@@ -70,6 +71,11 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   double *tmp = sm + nr;
   double *w = sm + 2 * nr;
   double *A = m.use_smem ? sm + 3 * nr : Linv64 + m.mat_off;
+  const bool packed = m.use_smem;
+  // A(i, j), i >= j, lives at A[cb(j) + i]
+  auto cb = [&](int j) -> size_t {
+    return packed ? (size_t)j * n - ((size_t)j * (j - 1)) / 2 - j : (size_t)j * n;
+  };
   const float *X = X32 + m.x_off;
   const float *ls = ls32 + m.ls_off;
   const double *y = y64 + m.y_off;
@@ -140,22 +146,24 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
         }
         double v = kernel_value(r2, sf2, m.kernel);
         if (i == j) v += sn2 + jit;
-        A[(size_t)j * n + i] = v;
+        A[cb(j) + i] = v;
       }
     }
     // right-looking column Cholesky, in place, lower triangle
     bool ok = true;
     for (int c = 0; c < n; ++c) {
       __syncthreads();
-      const double p = A[(size_t)c * n + c];
+      double *Ac = A + cb(c);
+      const double p = Ac[c];
       if (!(p > 0.0) || !isfinite(p)) { ok = false; break; }  // uniform across the CTA
       const double lcc = sqrt(p);
-      for (int i = c + 1 + tid; i < n; i += kFitThreads) A[(size_t)c * n + i] /= lcc;
+      for (int i = c + 1 + tid; i < n; i += kFitThreads) Ac[i] /= lcc;
       __syncthreads();
-      if (tid == 0) A[(size_t)c * n + c] = lcc;
+      if (tid == 0) Ac[c] = lcc;
       for (int j = c + 1 + warp; j < n; j += kWarps) {
-        const double ljc = A[(size_t)c * n + j];
-        for (int i = j + lane; i < n; i += 32) A[(size_t)j * n + i] -= A[(size_t)c * n + i] * ljc;
+        const double ljc = Ac[j];
+        double *Aj = A + cb(j);
+        for (int i = j + lane; i < n; i += 32) Aj[i] -= Ac[i] * ljc;
       }
     }
     if (ok) { jk = k; break; }
@@ -169,30 +177,31 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     }
     return;
   }
-  // keep L (col-major) for diagnostics
+  // keep L (col-major, full) for diagnostics
   for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
     const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
-    L64[m.mat_off + e] = (i >= j) ? A[e] : 0.0;
+    L64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
   }
 
   // ---- H4: in-place inverse of the lower-triangular factor (column sweep, right to left)
   for (int j = n - 1; j >= 0; --j) {
     __syncthreads();
-    const double dinv = 1.0 / A[(size_t)j * n + j];
-    for (int i = j + 1 + tid; i < n; i += kFitThreads) tmp[i] = A[(size_t)j * n + i];
+    double *Aj = A + cb(j);
+    const double dinv = 1.0 / Aj[j];
+    for (int i = j + 1 + tid; i < n; i += kFitThreads) tmp[i] = Aj[i];
     __syncthreads();
-    if (tid == 0) A[(size_t)j * n + j] = dinv;
+    if (tid == 0) Aj[j] = dinv;
     for (int i = j + 1 + tid; i < n; i += kFitThreads) {
       double acc2 = 0.0;
-      for (int k = j + 1; k <= i; ++k) acc2 += A[(size_t)k * n + i] * tmp[k];
-      A[(size_t)j * n + i] = -dinv * acc2;
+      for (int k = j + 1; k <= i; ++k) acc2 += A[cb(k) + i] * tmp[k];
+      Aj[i] = -dinv * acc2;
     }
   }
   __syncthreads();
   // w = L^-1 y~
   for (int i = tid; i < n; i += kFitThreads) {
     double a2 = 0.0;
-    for (int k = 0; k <= i; ++k) a2 += A[(size_t)k * n + i] * yt[k];
+    for (int k = 0; k <= i; ++k) a2 += A[cb(k) + i] * yt[k];
     w[i] = a2;
   }
   __syncthreads();
@@ -201,7 +210,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   for (int k = warp; k < m.n_pad; k += kWarps) {
     double a2 = 0.0;
     if (k < n)
-      for (int i = k + lane; i < n; i += 32) a2 += A[(size_t)k * n + i] * w[i];
+      for (int i = k + lane; i < n; i += 32) a2 += A[cb(k) + i] * w[i];
     a2 = warp_sum(a2);
     if (lane == 0) { alpha64[m.a_off + k] = a2; l1 += fabs(a2); amx = fmax(amx, fabs(a2)); }
   }
@@ -210,7 +219,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   double rs = 0.0;
   for (int j = tid; j < n; j += kFitThreads) {
     double a3 = 0.0;
-    for (int k = 0; k <= j; ++k) a3 += fabs(A[(size_t)k * n + j]);
+    for (int k = 0; k <= j; ++k) a3 += fabs(A[cb(k) + j]);
     rs = fmax(rs, a3);
   }
   rs = block_reduce(rs, red, MaxOp(), 0.0);
@@ -218,7 +227,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   if (m.use_smem)
     for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
       const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
-      Linv64[m.mat_off + e] = (i >= j) ? A[e] : 0.0;
+      Linv64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
     }
   else
     for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
@@ -227,7 +236,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     }
   for (size_t e = tid; e < (size_t)m.n_pad * m.n_pad; e += kFitThreads) {
     const int k = (int)(e / m.n_pad), j = (int)(e - (size_t)k * m.n_pad);
-    LT32[m.lt_off + e] = (k < n && j < n && j >= k) ? (float)A[(size_t)k * n + j] : 0.f;
+    LT32[m.lt_off + e] = (k < n && j < n && j >= k) ? (float)A[cb(k) + j] : 0.f;
   }
   if (tid == 0) {
     m.status = degenerate ? GPBO_WDEGENERATE : GPBO_OK;

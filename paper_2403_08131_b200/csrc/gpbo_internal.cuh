@@ -10,8 +10,9 @@ namespace gpbo {
 
 constexpr int kFitThreads = 512;
 constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
-// Largest n whose full n x n float64 matrix (+3 n-vectors) the fit keeps in shared memory.
-constexpr int kFitSmemMaxN = 160;
+// Largest n whose packed lower-triangular float64 matrix (+3 n-vectors) the fit keeps in shared
+// memory: 232 * 233 / 2 * 8 B = 216 KB.
+constexpr int kFitSmemMaxN = 232;
 
 // Per-search state of a fitted model (device copy in gpbo_model::meta_d, host copy in meta_h).
 struct SearchMeta {
@@ -88,6 +89,7 @@ struct ScoreLaunch {
   unsigned int *list_count;
   uint32_t list_cap;
   float *dbg_mu, *dbg_dmu, *dbg_var, *dbg_dvar, *dbg_eilo, *dbg_eihi;  // debug mode
+  unsigned long long *trace;   // optional clock64 event trace of CTA 0 (gpbo_debug_trace)
 };
 
 // Float64 refine phase (refine.cu).

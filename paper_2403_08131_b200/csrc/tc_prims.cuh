@@ -140,6 +140,53 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
       "r"(0u), "r"(0u)
       : "memory");
 }
+// Split descriptor: high word = SBO | version | layout (fixed per swizzle type), low word =
+// start address >> 4 | LBO(1) << 16; advancing an operand by `bytes` adds bytes >> 4 to the low
+// word (shared addresses < 256 KB never carry out of the 14-bit field).
+__host__ __device__ __forceinline__ uint32_t sdesc_hi(uint32_t row_bytes) {
+  return ((8u * row_bytes) >> 4) | (1u << 14) | (layout_code(row_bytes) << 29);
+}
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr) { return (saddr >> 4) | (1u << 16); }
+
+// D (+)= A B^T with pre-split descriptors; whole warp executes, one elected lane issues.
+__device__ __forceinline__ void mma_f16_split(uint32_t d_tmem, uint32_t alo, uint32_t ahi,
+                                              uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, {%7, %8, %9, %10}, p;\n\t}"
+      ::"r"(d_tmem), "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(accumulate),
+      "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+// Warp-uniform variants: the whole warp executes them, one elected lane issues.  Keeping the
+// issuer loop warp-uniform lets ptxas hold descriptors in uniform registers (no per-MMA
+// ELECT / R2UR.BROADCAST loop around UTCHMMA).
+__device__ __forceinline__ void mma_f16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u),
+      "r"(0u), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(bar)
+      : "memory");
+}
+
 // mbarrier arrives once every MMA previously issued by this thread has completed
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -12,7 +12,7 @@ namespace {
 
 __global__ void __launch_bounds__(128, 1)
 tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int row_bytes,
-                   int b_row_off) {
+                   int b_row_off, int timing, long long *cycles) {
   extern __shared__ unsigned char sm_raw[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -37,7 +37,7 @@ tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int
   }
   tc::fence_proxy_async();
   if (tid == 0) { tc::mbar_init(tc::smem_u32(&bar), 1); tc::fence_mbar_init(); }
-  if (warp == 0) tc::tmem_alloc(tc::smem_u32(&tmem_base), 256);
+  if (warp == 0) tc::tmem_alloc(tc::smem_u32(&tmem_base), 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -57,6 +57,21 @@ tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int
     tc::mma_commit(tc::smem_u32(&bar));
   }
   tc::mbar_wait(tc::smem_u32(&bar), 0);
+  if (timing && warp == 0) {
+    // issue-rate microbenchmark: `timing` repetitions of the same accumulate MMA by the whole
+    // warp (elected lane), clock64 after issue and after completion
+    const uint32_t H = tc::sdesc_hi(row_bytes);
+    const uint32_t alo = tc::sdesc_lo(tc::smem_u32(As)), blo = tc::sdesc_lo(tc::smem_u32(Bs));
+    const uint32_t idesc = tc::idesc_f16(N);
+    const long long c0 = clock64();
+    for (int r = 0; r < timing; ++r) tc::mma_f16_split(tbase + 256, alo, H, blo, H, idesc, 1u);
+    const long long c1 = clock64();
+    tc::mma_commit_warp(tc::smem_u32(&bar));
+    tc::mbar_wait(tc::smem_u32(&bar), 1);
+    const long long c2 = clock64();
+    if (lane == 0) { cycles[0] = c1 - c0; cycles[1] = c2 - c0; }
+  }
+  __syncthreads();
   tc::tc_fence_after();
   for (int c = 0; c < N; c += 8) {
     uint32_t r[8];
@@ -66,14 +81,22 @@ tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tbase, 256);
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
 }  // namespace
 }  // namespace gpbo
 
+extern "C" gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int N, int K,
+                                     int row_bytes, int b_row_off, int reps, long long *cycles);
+
 extern "C" gpbo_status gpbo_tc_selftest(const void *A, const void *B, float *D, int N, int K,
                                         int row_bytes, int b_row_off) {
+  return gpbo_tc_bench(A, B, D, N, K, row_bytes, b_row_off, 0, nullptr);
+}
+
+extern "C" gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int N, int K,
+                                     int row_bytes, int b_row_off, int reps, long long *cycles) {
   if (!A || !B || !D || N < 16 || N > 256 || N % 16 || K < 16 ||
       (row_bytes != 32 && row_bytes != 64 && row_bytes != 128) || K % (row_bytes / 2) ||
       b_row_off < 0 || b_row_off % 8)
@@ -83,7 +106,13 @@ extern "C" gpbo_status gpbo_tc_selftest(const void *A, const void *B, float *D, 
   if (cudaFuncSetAttribute(gpbo::tc_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem) != cudaSuccess)
     return GPBO_ECUDA;
+  long long *cyc = nullptr;
+  if (reps > 0 && cudaMalloc(&cyc, 16) != cudaSuccess) return GPBO_ECUDA;
   gpbo::tc_selftest_kernel<<<1, 128, smem>>>((const __half *)A, (const __half *)B, D, N, K,
-                                             row_bytes, b_row_off);
+                                             row_bytes, b_row_off, reps, cyc);
+  if (reps > 0) {
+    cudaMemcpy(cycles, cyc, 16, cudaMemcpyDeviceToHost);
+    cudaFree(cyc);
+  }
   return cudaDeviceSynchronize() == cudaSuccess ? GPBO_OK : GPBO_ECUDA;
 }

@@ -66,6 +66,8 @@ def load():
         "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
         "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
         "gpbo_debug_fast_phase": (C.c_int, [vp, vp, i32, vp, i64] + [vp] * 6),
+        "gpbo_debug_trace": (C.c_int, [vp, vp]),
+        "gpbo_tc_bench": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
         "gpbo_tc_selftest": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -82,7 +84,8 @@ def exported_symbols():
             "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
-            "gpbo_debug_fast_phase", "gpbo_tc_selftest"]
+            "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
+            "gpbo_tc_bench"]
 
 
 def _is_torch(a):
@@ -202,6 +205,10 @@ class Context:
     @property
     def last_impl(self):
         return int(load().gpbo_last_score_impl(self.handle))
+
+    def debug_trace(self, buf):
+        """buf: CUDA int64 tensor of >= 65536 entries, or None to disable."""
+        _check(self, load().gpbo_debug_trace(self.handle, None if buf is None else buf.data_ptr()))
 
     def set_profiling(self, on=True):
         _check(self, load().gpbo_set_profiling(self.handle, int(bool(on))))
