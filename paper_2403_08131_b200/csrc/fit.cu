@@ -55,13 +55,16 @@ __device__ __forceinline__ double kernel_value(double r2, double sf2, int kind) 
   return sf2 * (1.0 + s5 * r + (5.0 / 3.0) * r2) * exp(-s5 * r);
 }
 
-__global__ void __launch_bounds__(kFitThreads, 1)
-fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
-           const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
-           double *Linv64, float *Xs32, double *Xs64, float *LT32, double *alpha64,
-           SearchMeta *__restrict__ meta_out) {
-  extern __shared__ double sm[];
-  __shared__ double red[33];
+// The body is instantiated for a shared-memory (packed) and a global (unpacked) working matrix so
+// that every access to A compiles to LDS/STS or LDG/STG instead of generic loads.
+template <bool kSmem>
+__device__ __forceinline__ void fit_body(double *sm, double *red,
+                                         const SearchMeta *__restrict__ meta_in,
+                                         const float *__restrict__ X32,
+                                         const float *__restrict__ ls32,
+                                         const double *__restrict__ y64, double *L64,
+                                         double *Linv64, float *Xs32, double *Xs64, float *LT32,
+                                         double *alpha64, SearchMeta *__restrict__ meta_out) {
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   SearchMeta m = meta_in[s];
@@ -70,12 +73,9 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   double *yt = sm;
   double *tmp = sm + nr;
   double *w = sm + 2 * nr;
-  double *A = m.use_smem ? sm + 3 * nr : Linv64 + m.mat_off;
-  const bool packed = m.use_smem;
+  double *A = kSmem ? sm + 3 * nr : Linv64 + m.mat_off;
   // A(i, j), i >= j, lives at A[cb(j) + i]
-  auto cb = [&](int j) -> size_t {
-    return packed ? (size_t)j * n - ((size_t)j * (j - 1)) / 2 - j : (size_t)j * n;
-  };
+  auto cb = [&](int j) -> int { return kSmem ? j * n - (j * (j - 1)) / 2 - j : j * n; };
   const float *X = X32 + m.x_off;
   const float *ls = ls32 + m.ls_off;
   const double *y = y64 + m.y_off;
@@ -137,11 +137,13 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     jit = 1e-8 * p10 * sf2;
     __syncthreads();
     for (int j = warp; j < n; j += kWarps) {
+      const double *xj = Xs64 + m.x_off + (size_t)j * d;
       for (int i = j + lane; i < n; i += 32) {
+        // x / l precomputed in float64 above (the oracle's A / l, B / l then difference)
+        const double *xi = Xs64 + m.x_off + (size_t)i * d;
         double r2 = 0.0;
         for (int c = 0; c < d; ++c) {
-          const double li = (double)ls[c];
-          const double diff = (double)X[i * d + c] / li - (double)X[j * d + c] / li;
+          const double diff = xi[c] - xj[c];
           r2 += diff * diff;
         }
         double v = kernel_value(r2, sf2, m.kernel);
@@ -157,7 +159,8 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
       const double p = Ac[c];
       if (!(p > 0.0) || !isfinite(p)) { ok = false; break; }  // uniform across the CTA
       const double lcc = sqrt(p);
-      for (int i = c + 1 + tid; i < n; i += kFitThreads) Ac[i] /= lcc;
+      const double rl = 1.0 / lcc;
+      for (int i = c + 1 + tid; i < n; i += kFitThreads) Ac[i] *= rl;
       __syncthreads();
       if (tid == 0) Ac[c] = lcc;
       for (int j = c + 1 + warp; j < n; j += kWarps) {
@@ -183,18 +186,30 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     L64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
   }
 
-  // ---- H4: in-place inverse of the lower-triangular factor (column sweep, right to left)
-  for (int j = n - 1; j >= 0; --j) {
+  // ---- H4: in-place inverse X = L^-1 by a forward sweep over the rows of L (O(n) steps of
+  // parallel rank-1 updates; critical path O(n)):  at step k, row k of X is final after
+  // X[k][c] /= L[k][k]; then X[i][c] -= L[i][k] X[k][c] for i > k, c <= k (X[i][k] starts at 0).
+  for (int k = 0; k < n; ++k) {
     __syncthreads();
-    double *Aj = A + cb(j);
-    const double dinv = 1.0 / Aj[j];
-    for (int i = j + 1 + tid; i < n; i += kFitThreads) tmp[i] = Aj[i];
+    double *Ak = A + cb(k);
+    const double lkk = Ak[k];
+    for (int i = k + 1 + tid; i < n; i += kFitThreads) tmp[i] = Ak[i];  // column k of L
     __syncthreads();
-    if (tid == 0) Aj[j] = dinv;
-    for (int i = j + 1 + tid; i < n; i += kFitThreads) {
-      double acc2 = 0.0;
-      for (int k = j + 1; k <= i; ++k) acc2 += A[cb(k) + i] * tmp[k];
-      Aj[i] = -dinv * acc2;
+    const double inv = 1.0 / lkk;
+    // row k: X[k][c] = X[k][c] / L[k][k] for c < k (stored at (k, c)), X[k][k] = 1 / L[k][k]
+    for (int c = tid; c <= k; c += kFitThreads) {
+      double *p = A + cb(c) + k;
+      *p = c == k ? inv : *p * inv;
+    }
+    __syncthreads();
+    // rows i > k: X[i][c] = X[i][c] - L[i][k] X[k][c]  (c < k), X[i][k] = -L[i][k] X[k][k]
+    for (int c = warp; c <= k; c += kWarps) {
+      double *Ac = A + cb(c);
+      const double xkc = Ac[k];
+      if (c == k)
+        for (int i = k + 1 + lane; i < n; i += 32) Ac[i] = -tmp[i] * xkc;
+      else
+        for (int i = k + 1 + lane; i < n; i += 32) Ac[i] -= tmp[i] * xkc;
     }
   }
   __syncthreads();
@@ -224,7 +239,7 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
   }
   rs = block_reduce(rs, red, MaxOp(), 0.0);
   // write L^-1 (col-major) and the float32 (L^-1)^T scoring operand: LT[k][j] = Linv[j][k]
-  if (m.use_smem)
+  if (kSmem)
     for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
       const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
       Linv64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
@@ -245,6 +260,21 @@ fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32
     m.pmax = (float)pmax; m.alpha_max = (float)amx; m.linv_rowsum = (float)rs;
     meta_out[s] = m;
   }
+}
+
+__global__ void __launch_bounds__(kFitThreads, 1)
+fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
+           const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
+           double *Linv64, float *Xs32, double *Xs64, float *LT32, double *alpha64,
+           SearchMeta *__restrict__ meta_out) {
+  extern __shared__ double sm[];
+  __shared__ double red[33];
+  if (meta_in[blockIdx.x].use_smem)
+    fit_body<true>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs32, Xs64, LT32, alpha64,
+                   meta_out);
+  else
+    fit_body<false>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs32, Xs64, LT32, alpha64,
+                    meta_out);
 }
 
 }  // namespace
