@@ -150,6 +150,66 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
                             const int64_t *m_off, const int64_t *m_global_base,
                             const double *best, gpbo_mem mem, int64_t *idx, float *ei);
 
+/* ---------------------------------------------------------------- spaces and suggestions
+ * (H0 encoding, H5 candidate generation, bo_suggest_batch)
+ * A search space (Table IV, constraints L391): P parameters in
+ * declaration order, each
+ *   GPBO_P_REAL        [lo, hi)            encoded (v - lo)/(hi - lo)
+ *   GPBO_P_INT         lo..hi (step 1)     encoded (v - lo)/(hi - lo)
+ *   GPBO_P_ORDINAL     K numeric values    encoded rank/(K-1) (K = 1 -> 0)
+ *   GPBO_P_CATEGORICAL K labels 0..K-1     encoded one-hot (K columns)
+ * (reading R8), plus constrained blocks: a block names >= 1 discrete parameters and lists its
+ * valid value-index tuples; the generator draws one tuple uniformly (no rejection), so every
+ * candidate satisfies the caller's constraints.  Encoded dimension d = number of
+ * non-categorical parameters + sum of categorical K (<= GPBO_MAX_D).
+ * Generator: Philox4x32-10, key = seed, word u of global candidate i of search s at iteration t
+ * = output[u % 4] of Philox(ctr = (i, s, t, u / 4)), u over free parameters (declaration order)
+ * then blocks; real: (w >> 8) 2^-24, K values: (u64(w >> 8) K) >> 24. */
+typedef enum { GPBO_P_REAL = 0, GPBO_P_INT = 1, GPBO_P_ORDINAL = 2, GPBO_P_CATEGORICAL = 3 }
+    gpbo_param_kind;
+typedef struct gpbo_space gpbo_space;
+typedef struct {
+  int32_t P;
+  const int32_t *kind;        /* [P] gpbo_param_kind                                          */
+  const int32_t *nvals;       /* [P] K for ORDINAL / CATEGORICAL (ignored otherwise)          */
+  const double *lo, *hi;      /* [P] range for REAL / INT (ignored otherwise)                 */
+  const int32_t *val_off;     /* [P] offset of the ORDINAL value list in values (may be NULL  */
+  const double *values;       /*     when there is no ORDINAL parameter)                      */
+  int32_t nblocks;
+  const int32_t *block_off;   /* [nblocks+1] offsets into block_params                        */
+  const int32_t *block_params;/* parameter indices; each discrete, in at most one block       */
+  const int32_t *tuple_off;   /* [nblocks+1] offsets in tuples (counted in tuples)            */
+  const int32_t *tuples;      /* block b: tuple_off[b+1]-tuple_off[b] tuples of block-size     */
+} gpbo_space_desc;            /* value indices, blocks concatenated                            */
+
+/* All host arrays; copied (the space is immutable).  GPBO_ESAMPLING if a block has no valid
+ * tuple (an unsatisfiable constraint). */
+gpbo_status gpbo_space_create(gpbo_ctx *ctx, const gpbo_space_desc *desc, gpbo_space **out);
+void gpbo_space_free(gpbo_space *space);
+int32_t gpbo_space_dim(const gpbo_space *space);
+/* Host helper (H0): encode one raw configuration raw[P] -> enc[d] exactly as the generator does
+ * (callers encode their observation history with it).  GPBO_EINVAL for out-of-domain values. */
+gpbo_status gpbo_space_encode(const gpbo_space *space, const double *raw, float *enc);
+/* H5 alone (tests): encoded candidates first_idx .. first_idx+count-1 of (seed, search,
+ * iteration) -> enc[count * d] float32 in `mem` space. */
+gpbo_status gpbo_space_sample(gpbo_ctx *ctx, const gpbo_space *space, uint64_t seed,
+                              int32_t search, int32_t iteration, int64_t first_idx,
+                              int64_t count, gpbo_mem mem, float *enc);
+/* One BO suggestion per sub-search (the acquisition step of P:L72): for every search s, draw the
+ * M[s] candidates of (seed, s, iteration) on the device (this rank scores its contiguous shard
+ * of each pool, global indices as in ei_score_argmax), optionally mask candidates equal to an
+ * observed configuration of the model (dedup != 0, reading R14), score them (H6-H9, float64
+ * refine), combine across ranks (H10) and decode the winner (H11).  Outputs (host):
+ *   idx[S]     global candidate index (-1 if none), identical on every rank
+ *   x_raw[sum P_s]  the winner's raw parameter values (concatenated per search; REAL exact to
+ *              float64, others the chosen value / label index)
+ *   ei[S]      its EI in raw units
+ * spaces[s] must have dimension d_s of the model. */
+gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
+                             const gpbo_space *const *spaces, const int64_t *M, uint64_t seed,
+                             int32_t iteration, int32_t dedup, int64_t *idx, double *x_raw,
+                             float *ei);
+
 /* Number of CUDA kernels the library launched on ctx since creation (for bench accounting). */
 int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 

@@ -13,6 +13,7 @@
 
 #include "gpbo_internal.cuh"
 #include "score_tc.cuh"
+#include "space_internal.cuh"
 
 using gpbo::SearchMeta;
 
@@ -306,6 +307,43 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     CK(gpbo::launch_refine(r, rows, ctx->num_sms, ctx->stream));
   }
   ctx->launches += 1;
+  return GPBO_OK;
+}
+
+// Fast phase + refine + cross-rank max + decode (shared by ei_score_argmax / bo_suggest_batch).
+gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
+                        const int64_t *m_off, const int64_t *m_base, const double *best_std,
+                        int64_t *idx, float *ei) {
+  const int S = model->S;
+  gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_base, best_std, gpbo::kModeArgmax,
+                             Outputs());
+  if (st) return st;
+  if (ctx->nranks > 1)
+    NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->keys_h, ctx->keys_d, S * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned int *count_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap) + ctx->keys_cap;
+  CK(cudaMemcpyAsync(ctx->keys_h + ctx->keys_cap, count_d, 4, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  harvest_events(ctx);
+  ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
+  for (int s = 0; s < S; ++s) {
+    const unsigned long long k = ctx->keys_h[s];
+    const SearchMeta &q = model->meta[s];
+    if (k == 0ull) {
+      if (idx) idx[s] = -1;
+      if (ei) ei[s] = 0.f;
+      continue;
+    }
+    const uint32_t lo = (uint32_t)(k & 0xFFFFFFFFull);
+    const uint32_t bits = (uint32_t)(k >> 32);
+    float e;
+    std::memcpy(&e, &bits, 4);
+    if (idx) idx[s] = (int64_t)(0xFFFFFFFFu - lo);
+    if (ei) ei[s] = (float)(q.std * (double)e);
+  }
   return GPBO_OK;
 }
 
@@ -690,34 +728,90 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
                        ctx->stream));
     xd = (const float *)ctx->stage_d;
   }
-  gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_global_base, best_std.data(),
-                             gpbo::kModeArgmax, Outputs());
-  if (st) return st;
-  if (ctx->nranks > 1)
-    NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->keys_h, ctx->keys_d, S * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  unsigned int *count_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap) + ctx->keys_cap;
-  CK(cudaMemcpyAsync(ctx->keys_h + ctx->keys_cap, count_d, 4, cudaMemcpyDeviceToHost,
-                     ctx->stream));
+  return argmax_tail(ctx, model, xd, m_off, m_global_base, best_std.data(), idx, ei);
+}
+
+gpbo_status gpbo_space_sample(gpbo_ctx *ctx, const gpbo_space *space, uint64_t seed,
+                              int32_t search, int32_t iteration, int64_t first_idx,
+                              int64_t count, gpbo_mem mem, float *enc) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!space || !enc || count < 0 || first_idx < 0 || first_idx + count > 0xFFFFFFFFll)
+    return fail(ctx, GPBO_EINVAL, "bad space/sample arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int d = gpbo_space_dim(space);
+  float *out = enc;
+  if (mem == GPBO_HOST) {
+    gpbo_status st = ensure_stage(ctx, (size_t)count * d * 4 + 16);
+    if (st) return st;
+    out = (float *)ctx->stage_d;
+  }
+  CK(gpbo::launch_gen(gpbo::space_dev(space), seed, (uint32_t)search, (uint32_t)iteration,
+                      first_idx, count, out, nullptr, 0, ctx->stream));
+  ctx->launches += 1;
+  if (mem == GPBO_HOST)
+    CK(cudaMemcpyAsync(enc, out, (size_t)count * d * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaGetLastError());
-  harvest_events(ctx);
-  ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
+  return GPBO_OK;
+}
+
+gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
+                             const gpbo_space *const *spaces, const int64_t *M, uint64_t seed,
+                             int32_t iteration, int32_t dedup, int64_t *idx, double *x_raw,
+                             float *ei) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model || !spaces || !M) return fail(ctx, GPBO_EINVAL, "null model/spaces/M");
+  CK(cudaSetDevice(ctx->device));
+  const int S = model->S;
+  std::vector<int64_t> off(S + 1, 0), base(S, 0), xoff(S + 1, 0);
+  std::vector<double> best_std(S);
   for (int s = 0; s < S; ++s) {
-    const unsigned long long k = ctx->keys_h[s];
+    if (!spaces[s] || gpbo_space_dim(spaces[s]) != model->meta[s].d)
+      return fail(ctx, GPBO_EINVAL, "space dimension does not match the model");
+    if (M[s] < 0 || M[s] >= 0xFFFFFFFFll) return fail(ctx, GPBO_EINVAL, "bad pool size");
+    const int64_t per = (M[s] + ctx->nranks - 1) / ctx->nranks;
+    const int64_t a = std::min<int64_t>(M[s], per * ctx->rank);
+    const int64_t b = std::min<int64_t>(M[s], per * (ctx->rank + 1));
+    base[s] = a;
+    off[s + 1] = off[s] + (b - a);
+    xoff[s + 1] = xoff[s] + (b - a) * model->meta[s].d;
+    best_std[s] = model->meta[s].best;
+  }
+  gpbo_status st = ensure_stage(ctx, (size_t)xoff[S] * 4 + 16);
+  if (st) return st;
+  float *X = (float *)ctx->stage_d;
+  for (int s = 0; s < S; ++s) {
     const SearchMeta &q = model->meta[s];
-    if (k == 0ull) {
-      if (idx) idx[s] = -1;
-      if (ei) ei[s] = 0.f;
-      continue;
+    CK(gpbo::launch_gen(gpbo::space_dev(spaces[s]), seed, (uint32_t)s, (uint32_t)iteration,
+                        base[s], off[s + 1] - off[s], X + xoff[s],
+                        dedup ? model->X32 + q.x_off : nullptr, q.n, ctx->stream));
+    ctx->launches += 1;
+  }
+  std::vector<float> eiv(S);
+  st = argmax_tail(ctx, model, X, off.data(), base.data(), best_std.data(), idx, eiv.data());
+  if (st) return st;
+  int64_t po = 0;
+  for (int s = 0; s < S; ++s) {
+    const gpbo::SpaceView &v = gpbo::space_host(spaces[s]);
+    if (ei) ei[s] = eiv[s];
+    if (x_raw) {
+      if (idx[s] >= 0) {
+        std::vector<float> enc(v.d);
+        std::vector<double> vals(v.P);
+        gpbo::sample_candidate_host(v, seed, (uint32_t)s, (uint32_t)iteration,
+                                    (uint32_t)idx[s], enc.data(), vals.data());
+        for (int i = 0; i < v.P; ++i) {
+          const int k = v.kind[i];
+          double r = vals[i];
+          if (k == GPBO_P_REAL) r = v.lo[i] + (v.hi[i] - v.lo[i]) * vals[i];
+          else if (k == GPBO_P_INT) r = v.lo[i] + vals[i];
+          else if (k == GPBO_P_ORDINAL) r = v.values[v.val_off[i] + (int)vals[i]];
+          x_raw[po + i] = r;
+        }
+      } else {
+        for (int i = 0; i < v.P; ++i) x_raw[po + i] = NAN;
+      }
     }
-    const uint32_t lo = (uint32_t)(k & 0xFFFFFFFFull);
-    const uint32_t bits = (uint32_t)(k >> 32);
-    float e;
-    std::memcpy(&e, &bits, 4);
-    if (idx) idx[s] = (int64_t)(0xFFFFFFFFu - lo);
-    if (ei) ei[s] = (float)(q.std * (double)e);
+    po += v.P;
   }
   return GPBO_OK;
 }

@@ -28,6 +28,13 @@ class GpboError(RuntimeError):
         self.status = status
 
 
+class SpaceDesc(C.Structure):
+    _fields_ = [("P", C.c_int32), ("kind", C.c_void_p), ("nvals", C.c_void_p), ("lo", C.c_void_p),
+                ("hi", C.c_void_p), ("val_off", C.c_void_p), ("values", C.c_void_p),
+                ("nblocks", C.c_int32), ("block_off", C.c_void_p), ("block_params", C.c_void_p),
+                ("tuple_off", C.c_void_p), ("tuples", C.c_void_p)]
+
+
 class FitArgs(C.Structure):
     _fields_ = [("S", C.c_int32), ("n", C.c_void_p), ("d", C.c_void_p), ("X", C.c_void_p),
                 ("y", C.c_void_p), ("lengthscale", C.c_void_p), ("signal_var", C.c_void_p),
@@ -69,6 +76,12 @@ def load():
         "gpbo_debug_trace": (C.c_int, [vp, vp]),
         "gpbo_tc_bench": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
         "gpbo_tc_selftest": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "gpbo_space_create": (C.c_int, [vp, C.POINTER(SpaceDesc), C.POINTER(vp)]),
+        "gpbo_space_free": (None, [vp]),
+        "gpbo_space_dim": (i32, [vp]),
+        "gpbo_space_encode": (C.c_int, [vp, vp, vp]),
+        "gpbo_space_sample": (C.c_int, [vp, vp, C.c_uint64, i32, i32, i64, i64, C.c_int, vp]),
+        "bo_suggest_batch": (C.c_int, [vp, vp, vp, vp, C.c_uint64, i32, i32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -85,7 +98,8 @@ def exported_symbols():
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
-            "gpbo_tc_bench"]
+            "gpbo_tc_bench", "gpbo_space_create", "gpbo_space_free", "gpbo_space_dim",
+            "gpbo_space_encode", "gpbo_space_sample", "bo_suggest_batch"]
 
 
 def _is_torch(a):
@@ -301,6 +315,87 @@ def tc_selftest(A, B, row_bytes, b_row_off=0):
     if st != OK:
         raise GpboError(st, "tc_selftest failed")
     return D
+
+
+class Space:
+    """gpbo_space from a parameter list (dicts with kind REAL/INT {lo, hi}, ORDINAL {values},
+    CATEGORICAL {K}) and constrained blocks ({params: [...], tuples: [[value indices]...]})."""
+
+    def __init__(self, ctx, params, blocks=()):
+        P = len(params)
+        kind = np.array([p["kind"] for p in params], np.int32)
+        nv = np.array([len(p["values"]) if p["kind"] == 2 else p.get("K", 0) for p in params],
+                      np.int32)
+        lo = np.array([float(p.get("lo", 0.0)) for p in params])
+        hi = np.array([float(p.get("hi", 1.0)) for p in params])
+        vals, voff = [], []
+        for p in params:
+            voff.append(len(vals))
+            if p["kind"] == 2:
+                vals.extend(float(v) for v in p["values"])
+        voff = np.array(voff, np.int32)
+        vals = np.array(vals + [0.0])
+        boff, bpar, toff, tup = [0], [], [0], []
+        for b in blocks:
+            bpar.extend(b["params"])
+            boff.append(len(bpar))
+            t = np.asarray(b["tuples"], np.int32).reshape(len(b["tuples"]), len(b["params"]))
+            tup.extend(t.ravel().tolist())
+            toff.append(toff[-1] + t.shape[0])
+        self._keep = [kind, nv, lo, hi, voff, vals] + [np.array(x + [0], np.int32)
+                                                       for x in (boff, bpar, toff, tup)]
+        k = self._keep
+        desc = SpaceDesc(P, k[0].ctypes.data, k[1].ctypes.data, k[2].ctypes.data,
+                         k[3].ctypes.data, k[4].ctypes.data, k[5].ctypes.data, len(blocks),
+                         k[6].ctypes.data, k[7].ctypes.data, k[8].ctypes.data, k[9].ctypes.data)
+        h = C.c_void_p()
+        _check(ctx, load().gpbo_space_create(ctx.handle, C.byref(desc), C.byref(h)))
+        self.handle, self.ctx, self.P = h, ctx, P
+        self.dim = int(load().gpbo_space_dim(h))
+
+    def encode(self, raw):
+        """H0 on the host: raw (n x P) float64 -> encoded (n x d) float32."""
+        raw = np.atleast_2d(np.asarray(raw, np.float64))
+        out = np.zeros((raw.shape[0], self.dim), np.float32)
+        for i in range(raw.shape[0]):
+            r = np.ascontiguousarray(raw[i])
+            _check(self.ctx, load().gpbo_space_encode(self.handle, r.ctypes.data,
+                                                      out[i:].ctypes.data))
+        return out
+
+    def sample(self, seed, search, iteration, first, count):
+        """H5 on the device: encoded candidates first..first+count-1 (host numpy)."""
+        out = np.zeros((count, self.dim), np.float32)
+        _check(self.ctx, load().gpbo_space_sample(self.ctx.handle, self.handle, seed, search,
+                                                  iteration, first, count, HOST,
+                                                  out.ctypes.data))
+        return out
+
+    def __del__(self):
+        try:
+            if self.handle:
+                load().gpbo_space_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def suggest(ctx, model, spaces, M, seed, iteration, dedup=True):
+    """bo_suggest_batch -> (idx int64[S], x_raw list of float64[P_s], ei float32[S])."""
+    S = model.S
+    arr = (C.c_void_p * S)(*[sp.handle.value for sp in spaces])
+    Ma = np.ascontiguousarray(M, dtype=np.int64)
+    idx = np.zeros(S, np.int64)
+    ei = np.zeros(S, np.float32)
+    xr = np.zeros(sum(sp.P for sp in spaces))
+    _check(ctx, load().bo_suggest_batch(ctx.handle, model.handle, arr, Ma.ctypes.data, seed,
+                                        iteration, int(bool(dedup)), idx.ctypes.data,
+                                        xr.ctypes.data, ei.ctypes.data))
+    out, o = [], 0
+    for sp in spaces:
+        out.append(xr[o:o + sp.P])
+        o += sp.P
+    return idx, out, ei
 
 
 def version():

@@ -1,0 +1,139 @@
+"""H0/H5 + bo_suggest_batch on the GPU against the oracle (oracle/space.py, oracle/gp.py).
+
+Candidate coordinates are compared bit-exactly (both sides implement the documented Philox
+mapping independently); the suggestion follows the argmax rule R11 on the same candidates.
+"""
+import numpy as np
+import pytest
+
+from oracle import gp
+from oracle import space as osp
+from tests import helpers as H
+from workloads import rttddft
+
+pytestmark = pytest.mark.gpu
+
+MIXED = [{"kind": 0, "lo": -50.0, "hi": 50.0}, {"kind": 1, "lo": 1, "hi": 32},
+         {"kind": 2, "values": [1, 2, 4, 8, 16]}, {"kind": 3, "K": 4},
+         {"kind": 0, "lo": 0.0, "hi": 1.0}]
+MIXED_BLOCKS = [{"params": [1, 2], "tuples": [(a, b) for a in range(32) for b in range(5)
+                                              if (a + 1) * [1, 2, 4, 8, 16][b] <= 64]}]
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_08131_b200 import gpbo
+    ctx = gpbo.Context(device=0)
+    yield gpbo, ctx
+    ctx.close()
+
+
+@pytest.mark.parametrize("which", ["table_iv", "mixed"])
+def test_generation_is_bit_exact(G, which):
+    gpbo, ctx = G
+    if which == "table_iv":
+        params, blocks, _ = rttddft.table_iv()
+    else:
+        params, blocks = MIXED, MIXED_BLOCKS
+    sp = gpbo.Space(ctx, params, blocks)
+    ref = osp.Space(params, blocks)
+    assert sp.dim == ref.dim
+    for seed, s, t, first in ((1, 0, 0, 0), (0xDEADBEEF12345678, 3, 17, 123456), (7, 1, 2, 2 ** 31)):
+        got = sp.sample(seed, s, t, first, 3000)
+        exp = ref.sample(seed, s, t, np.arange(first, first + 3000))
+        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), (seed, s, t)
+    # host-side encoding of decoded raw values reproduces the generator's encoding (H0)
+    vals = ref.sample_values(5, 0, 1, np.arange(200))
+    raw = ref.raw_values(vals)
+    assert np.array_equal(sp.encode(raw), ref.encode_values(vals))
+
+
+def _history(params, blocks, n0, seed):
+    vidx = rttddft.initial_design(params, blocks, n0, seed)
+    y = rttddft.objective(vidx, params)
+    ref = osp.Space(params, blocks)
+    return vidx, y, ref.encode_values(vidx.astype(float))
+
+
+def test_suggest_matches_oracle_and_decodes(G):
+    gpbo, ctx = G
+    params, blocks, _ = rttddft.table_iv()
+    sp = gpbo.Space(ctx, params, blocks)
+    ref = osp.Space(params, blocks)
+    vidx, y, X = _history(params, blocks, 24, 3)
+    d = X.shape[1]
+    ls = np.full(d, 0.4 * np.sqrt(d), np.float32)
+    m = ctx.fit([len(y)], [d], np.ascontiguousarray(X.ravel()), y, ls, np.ones(1, np.float32),
+                np.full(1, 1e-4, np.float32))
+    M, seed, it = 8192, 42, 7
+    idx, xr, ei = gpbo.suggest(ctx, m, [sp], [M], seed, it, dedup=True)
+    cand = ref.sample(seed, 0, it, np.arange(M))
+    om = gp.fit(X, y, ls, 1.0, 1e-4)
+    res = gp.score(om, cand)
+    H.check_argmax(res, int(idx[0]), "suggest")
+    assert abs(ei[0] / om.std - res.ei) <= H.TOL * max(res.ei, 1e-30)
+    vals = ref.sample_values(seed, 0, it, [int(idx[0])])
+    assert np.array_equal(xr[0], ref.raw_values(vals)[0])
+    # the suggestion satisfies the Table IV constraints
+    nstb, nkpb, nspb = xr[0][0], xr[0][1], xr[0][2]
+    assert nstb * nkpb * nspb <= 40
+    for j in range(5):
+        assert xr[0][4 + 3 * j] * xr[0][5 + 3 * j] <= 2048
+
+
+def test_dedup_masks_observed_configurations(G):
+    """R14 / S:L432: a candidate identical to an observation is skipped (next-best EI)."""
+    gpbo, ctx = G
+    sp = gpbo.Space(ctx, MIXED, MIXED_BLOCKS)
+    ref = osp.Space(MIXED, MIXED_BLOCKS)
+    seed, it, M = 11, 2, 2048
+    cand = ref.sample(seed, 0, it, np.arange(M))
+    g = np.random.default_rng(0)
+    X = np.concatenate([g.random((10, ref.dim)).astype(np.float32), cand[[5, 900]]])
+    y = g.standard_normal(12)
+    y[10:] = y.min() - 1.0  # the duplicated points are the best observations
+    ls = np.full(ref.dim, 0.5, np.float32)
+    m = ctx.fit([12], [ref.dim], np.ascontiguousarray(X.ravel()), y, ls, np.ones(1, np.float32),
+                np.full(1, 1e-4, np.float32))
+    idx, _, _ = gpbo.suggest(ctx, m, [sp], [M], seed, it, dedup=True)
+    om = gp.fit(X, y, ls, 1.0, 1e-4)
+    mu, var = gp.posterior(om, cand)
+    ei = gp.expected_improvement(mu, var, om.best)
+    ei[[5, 900]] = -1.0  # masked
+    assert int(idx[0]) not in (5, 900)
+    top = int(np.argmax(ei))
+    srt = np.sort(ei)[::-1]
+    if (srt[0] - srt[1]) > 1e-3 * srt[0]:
+        assert int(idx[0]) == top
+
+
+def test_replay_teacher_forced(G):
+    """Config-5 style replay (reduced): 12 BO iterations on the Table IV space; at every iteration
+    the oracle scores the same candidates from the same history (teacher forcing)."""
+    gpbo, ctx = G
+    params, blocks, _ = rttddft.table_iv()
+    sp = gpbo.Space(ctx, params, blocks)
+    ref = osp.Space(params, blocks)
+    vidx, y, X = _history(params, blocks, 5, 9)
+    d = X.shape[1]
+    ls = np.full(d, 0.4 * np.sqrt(d), np.float32)
+    M, seed = 2048, 1234
+    for it in range(12):
+        m = ctx.fit([len(y)], [d], np.ascontiguousarray(X.ravel()), y, ls,
+                    np.ones(1, np.float32), np.full(1, 1e-4, np.float32))
+        idx, xr, _ = gpbo.suggest(ctx, m, [sp], [M], seed, it, dedup=True)
+        cand = ref.sample(seed, 0, it, np.arange(M))
+        om = gp.fit(X, y, ls, 1.0, 1e-4)
+        mu, var = gp.posterior(om, cand)
+        ei = gp.expected_improvement(mu, var, om.best)
+        dup = (cand[:, None, :] == X[None, :, :]).all(-1).any(-1)
+        ei[dup] = -1.0
+        srt = np.sort(ei)[::-1]
+        if srt[0] >= 1e-30 and (srt[0] - srt[1]) > 1e-3 * srt[0]:
+            assert int(idx[0]) == int(np.argmax(ei)), it
+        v = ref.sample_values(seed, 0, it, [int(idx[0])]).astype(np.int64)
+        X = np.concatenate([X, ref.encode_values(v.astype(float))])
+        y = np.concatenate([y, rttddft.objective(v, params)])
