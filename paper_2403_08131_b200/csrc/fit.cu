@@ -121,7 +121,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     double q = 0.0;
     for (int c = 0; c < d; ++c) {
       const double v = (double)X[i * d + c] / (double)ls[c];
-      Xs64[m.x_off + i * d + c] = v;
+      Xs64[m.x_off + (size_t)c * n + i] = v;  // column-major: x/l of point i, dim c
       q += v * v;
     }
     pm = fmax(pm, q);
@@ -137,13 +137,12 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     jit = 1e-8 * p10 * sf2;
     __syncthreads();
     for (int j = warp; j < n; j += kWarps) {
-      const double *xj = Xs64 + m.x_off + (size_t)j * d;
+      const double *xc = Xs64 + m.x_off;  // column-major (d x n): coalesced across lanes
       for (int i = j + lane; i < n; i += 32) {
         // x / l precomputed in float64 above (the oracle's A / l, B / l then difference)
-        const double *xi = Xs64 + m.x_off + (size_t)i * d;
         double r2 = 0.0;
         for (int c = 0; c < d; ++c) {
-          const double diff = xi[c] - xj[c];
+          const double diff = xc[(size_t)c * n + i] - xc[(size_t)c * n + j];
           r2 += diff * diff;
         }
         double v = kernel_value(r2, sf2, m.kernel);
@@ -231,13 +230,18 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   }
   l1 = block_reduce(l1, red, AddOp(), 0.0);
   amx = block_reduce(amx, red, MaxOp(), 0.0);
-  double rs = 0.0;
+  double rs = 0.0, lam = 0.0;
   for (int j = tid; j < n; j += kFitThreads) {
     double a3 = 0.0;
-    for (int k = 0; k <= j; ++k) a3 += fabs(A[cb(k) + j]);
+    for (int k = 0; k <= j; ++k) {
+      const double v = fabs(A[cb(k) + j]);
+      a3 += v;
+      lam = fmax(lam, v);
+    }
     rs = fmax(rs, a3);
   }
   rs = block_reduce(rs, red, MaxOp(), 0.0);
+  lam = block_reduce(lam, red, MaxOp(), 0.0);
   // write L^-1 (col-major) and the float32 (L^-1)^T scoring operand: LT[k][j] = Linv[j][k]
   if (kSmem)
     for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
@@ -258,6 +262,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     m.jitter_k = jk; m.jitter = jit;
     m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = l1;
     m.pmax = (float)pmax; m.alpha_max = (float)amx; m.linv_rowsum = (float)rs;
+    m.linv_absmax = lam;
     meta_out[s] = m;
   }
 }

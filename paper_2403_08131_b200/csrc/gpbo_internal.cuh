@@ -33,6 +33,7 @@ struct SearchMeta {
   float pmax;           // max_j |x_j / l|^2 (error-bound input of the fast phase)
   float alpha_max;      // max_j |alpha_j|
   float linv_rowsum;    // max_j sum_k |(L^-1)_jk| (variance error-bound input)
+  double linv_absmax;   // max |(L^-1)_jk| (operand scaling of the tcgen05 image)
   // ---- tcgen05 fast phase (score_tc.cu); valid when tc_ok
   int32_t tc_ok;
   int32_t n16;          // n rounded up to 16 (V accumulator columns)

@@ -13,7 +13,7 @@
 // rounding and independent of how the candidates were sharded.
 //
 // gp_posterior runs the same code densely over all rows (posterior mode).
-// One warp per candidate; lanes stride over the training points.
+// One CTA per candidate; threads stride over training points, then over rows of L^-1.
 #include <algorithm>
 #include <cmath>
 
@@ -23,7 +23,7 @@
 namespace gpbo {
 namespace {
 
-constexpr int kRefineWarps = 8;
+constexpr int kRefineThreads = 256;
 
 __device__ __forceinline__ double kernel64(double r2, double sf2, int kind) {
   if (kind == GPBO_RBF) return sf2 * exp(-0.5 * r2);
@@ -41,59 +41,75 @@ __device__ __forceinline__ double tau64(double z) {
   return exp(-0.5 * z * z) * (inv_sqrt2pi - 0.5 * x * erfcx(x * inv_sqrt2));
 }
 
-__global__ void __launch_bounds__(kRefineWarps * 32)
+__device__ __forceinline__ double block_sum2(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kRefineThreads / 32; ++i) t += red[i];
+  return t;
+}
+
+// One CTA per candidate: lanes over training points for K*, rows of L^-1 for v = L^-1 k*.
+__global__ void __launch_bounds__(kRefineThreads)
 refine_kernel(const RefineLaunch p) {
-  __shared__ double xsh[kRefineWarps][GPBO_MAX_D];
-  __shared__ double ksh[kRefineWarps][GPBO_MAX_N];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double xsh[GPBO_MAX_D];
+  __shared__ double ksh[GPBO_MAX_N];
+  __shared__ double red[kRefineThreads / 32];
+  const int tid = threadIdx.x;
   const int64_t nent = p.list ? (int64_t)*p.list_count : p.dense_rows;
-  for (int64_t e = (int64_t)blockIdx.x * kRefineWarps + warp; e < nent;
-       e += (int64_t)gridDim.x * kRefineWarps) {
+  for (int64_t e = blockIdx.x; e < nent; e += gridDim.x) {
     int s;
     uint32_t row;
-    float var;
     if (p.list) {
       const RefineEntry en = p.list[e];
-      if (en.ei_hi < __uint_as_float(p.thr[en.s])) continue;  // cannot be the argmax
-      s = en.s; row = en.row; var = en.var;
+      if (en.ei_hi < __uint_as_float(p.thr[en.s])) continue;  // cannot be the argmax (uniform)
+      s = en.s; row = en.row;
     } else {
-      s = p.dense_s; row = (uint32_t)e; var = p.dense_var[e];
+      s = p.dense_s; row = (uint32_t)e;
     }
     const SearchMeta &m = p.meta[s];
     const int n = m.n, d = m.d;
     const float *x = p.Xstar + p.x_off[s] + (int64_t)row * d;
     const float *ls = p.ls32 + m.ls_off;
-    for (int c = lane; c < d; c += 32) xsh[warp][c] = (double)x[c] / (double)ls[c];
-    __syncwarp();
+    __syncthreads();  // previous candidate done with xsh / ksh
+    for (int c = tid; c < d; c += kRefineThreads) xsh[c] = (double)x[c] / (double)ls[c];
+    __syncthreads();
     const double *Xj = p.Xs64 + m.x_off;
     const double *alpha = p.alpha64 + m.a_off;
     double mu = 0.0;
-    for (int j = lane; j < n; j += 32) {
+    for (int j = tid; j < n; j += kRefineThreads) {
       double r2 = 0.0;
       for (int c = 0; c < d; ++c) {
-        const double diff = xsh[warp][c] - Xj[j * d + c];
+        const double diff = xsh[c] - Xj[(size_t)c * n + j];  // column-major x/l
         r2 += diff * diff;
       }
       const double k = kernel64(r2, (double)m.sf2, m.kernel);
-      ksh[warp][j] = k;
+      ksh[j] = k;
       mu += k * alpha[j];
     }
-    __syncwarp();
-    // v = L^-1 k*: lane owns rows j; Linv64 is column-major (column k contiguous over j)
+    mu = block_sum2(mu, red);  // includes the barrier that publishes ksh
+    // v = L^-1 k*: thread owns rows j; Linv64 is column-major (column k contiguous over j)
     const double *Li = p.Linv64 + m.mat_off;
     double vv = 0.0;
-    for (int j = lane; j < n; j += 32) {
-      double v = 0.0;
-      for (int k = 0; k <= j; ++k) v = fma(Li[(size_t)k * n + j], ksh[warp][k], v);
+    for (int j = tid; j < n; j += kRefineThreads) {
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      int k = 0;
+      for (; k + 3 <= j; k += 4) {
+        v0 = fma(Li[(size_t)k * n + j], ksh[k], v0);
+        v1 = fma(Li[(size_t)(k + 1) * n + j], ksh[k + 1], v1);
+        v2 = fma(Li[(size_t)(k + 2) * n + j], ksh[k + 2], v2);
+        v3 = fma(Li[(size_t)(k + 3) * n + j], ksh[k + 3], v3);
+      }
+      for (; k <= j; ++k) v0 = fma(Li[(size_t)k * n + j], ksh[k], v0);
+      const double v = (v0 + v1) + (v2 + v3);
       vv = fma(v, v, vv);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mu += __shfl_xor_sync(0xffffffffu, mu, o);
-      vv += __shfl_xor_sync(0xffffffffu, vv, o);
-    }
-    (void)var;
-    if (lane == 0) {
+    vv = block_sum2(vv, red);
+    if (tid == 0) {
       const double var64 = fmax((double)m.sf2 - vv, 0.0);
       const double sig = sqrt(var64);
       const double imp = p.best[s] - mu;
@@ -107,7 +123,6 @@ refine_kernel(const RefineLaunch p) {
         if (p.out_ei) p.out_ei[e] = (float)(m.std * ei);
       }
     }
-    __syncwarp();
   }
 }
 
@@ -116,9 +131,8 @@ refine_kernel(const RefineLaunch p) {
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
                           cudaStream_t stream) {
   if (max_entries <= 0) return cudaSuccess;
-  const int64_t want = (max_entries + kRefineWarps - 1) / kRefineWarps;
-  const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * 8);
-  refine_kernel<<<grid, kRefineWarps * 32, 0, stream>>>(p);
+  const int grid = (int)std::min<int64_t>(max_entries, (int64_t)num_sms * 4);
+  refine_kernel<<<grid, kRefineThreads, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

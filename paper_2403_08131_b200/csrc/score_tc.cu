@@ -558,9 +558,9 @@ __device__ double block_max_d(double v, double *red) {
 __global__ void __launch_bounds__(256)
 pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const double *alpha64,
                const float *ls32, unsigned char *img_all) {
-  __shared__ double red[8];
   __shared__ double sc[4];
   const int s = blockIdx.x;
+  const int nch = gridDim.y, ch = blockIdx.y;  // blocks of one search split every loop below
   SearchMeta m = meta[s];
   if (!m.tc_ok || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
   const int n = m.n, d = m.d;
@@ -569,9 +569,8 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
   const double *Li = Linv64 + m.mat_off;
   const double *X = Xs64 + m.x_off;
   const double gk = m.kernel == GPBO_RBF ? 0.70710678118654752440 : 2.2360679774997896964;
-  double lmax = 0.0;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) lmax = fmax(lmax, fabs(Li[e]));
-  lmax = block_max_d(lmax, red);
+  const double lmax = m.linv_absmax;
+  const int t0 = ch * blockDim.x + threadIdx.x, tstep = nch * blockDim.x;
   if (threadIdx.x == 0) {
     double qbox = 0.0;
     for (int c = 0; c < d; ++c) qbox += 1.0 / ((double)ls32[m.ls_off + c] * ls32[m.ls_off + c]);
@@ -599,7 +598,7 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
     m.hscale = (float)ldexp(1.0, 2 * e);
     m.vunscale2 = (float)ldexp(1.0, -2 * (tK + uL));
     m.pmax_h = (float)(gk * gk * (double)m.pmax);
-    meta[s] = m;
+    if (ch == 0) meta[s] = m;
   }
   __syncthreads();
   const double xs = sc[0];
@@ -611,15 +610,15 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
     *reinterpret_cast<__half *>(base_lo + off) = lo;
   };
   // augmented training operand [-2 x^_j, 1, |x^_j|^2], K blocks of 16, rows n16
-  for (int idx = threadIdx.x; idx < g.n16 * g.kb * 16; idx += blockDim.x) {
+  for (int idx = t0; idx < g.n16 * g.kb * 16; idx += tstep) {
     const int j = idx / (g.kb * 16), k = idx % (g.kb * 16);
     double v = 0.0;
     if (j < n) {
-      if (k < d) v = -2.0 * xs * X[j * d + k];
+      if (k < d) v = -2.0 * xs * X[(size_t)k * n + j];
       else if (k == d) v = 1.0;
       else if (k == d + 1) {
         double pj = 0.0;
-        for (int c = 0; c < d; ++c) pj += (xs * X[j * d + c]) * (xs * X[j * d + c]);
+        for (int c = 0; c < d; ++c) pj += (xs * X[(size_t)c * n + j]) * (xs * X[(size_t)c * n + j]);
         v = pj;
       }
     }
@@ -631,7 +630,7 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
   for (int pp = 0; pp < g.npan; ++pp) {
     const int R = g.n16 - 32 * pp;
     unsigned char *hi = img + g.off_l + (pp * g.n16 - 16 * pp * (pp - 1)) * 128;
-    for (int idx = threadIdx.x; idx < R * 32; idx += blockDim.x) {
+    for (int idx = t0; idx < R * 32; idx += tstep) {
       const int r = idx >> 5, k = idx & 31;
       const int j = 32 * pp + r, kk = 32 * pp + k;
       const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)kk * n + j], uL) : 0.0;
@@ -639,12 +638,12 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
     }
   }
   float2 *ap = reinterpret_cast<float2 *>(img + g.off_a);
-  for (int j = threadIdx.x; j < g.n16; j += blockDim.x) {
+  for (int j = t0; j < g.n16; j += tstep) {
     const double a = j < n ? alpha64[m.a_off + j] : 0.0;
     ap[j] = make_float2((float)ldexp(a, -tK), (float)ldexp(fabs(a), -tK));
   }
   float *wp = reinterpret_cast<float *>(img + g.off_w);
-  for (int c = threadIdx.x; c < GPBO_MAX_D; c += blockDim.x)
+  for (int c = t0; c < GPBO_MAX_D; c += tstep)
     wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
   (void)e;
 }
@@ -679,8 +678,8 @@ void tc_fill_geometry(SearchMeta &m) {
 cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64,
                            const double *Xs64, const double *alpha64, const float *ls32,
                            unsigned char *img, cudaStream_t stream) {
-  pack_tc_kernel<<<S, 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
-                                        alpha64, ls32, img);
+  pack_tc_kernel<<<dim3(S, 16), 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
+                                                   alpha64, ls32, img);
   return cudaGetLastError();
 }
 
