@@ -46,13 +46,18 @@ constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
-constexpr int kDepth = 3;           // distance scratch stages (TMEM) issued ahead of the V MMAs
-constexpr int kVBufMaxN = 208;      // n16 <= 208: two V accumulators (2 x 208 + 3 x 32 = 512)
+constexpr int kDepth = 2;           // 64-column distance scratch stages (TMEM), issued ahead
+constexpr int kKStages = 4;         // K* operand stages (TMEM)
+// TMEM columns: V accumulator [0, n16 <= 256), distance scratch 2 x 64 [256, 384), K* operand
+// stages 4 x 32 [384, 512) (per stage: hi k-steps 0/1 at +0/+8, lo at +16/+24; lane = row, one
+// column packs the fp16 pair k = 2c, 2c+1).
+constexpr uint32_t kScratch0 = 256;
+constexpr uint32_t kKstar0 = 384;
 
 enum {
   B_AF0 = 0, B_AF1, B_AE0, B_AE1,           // candidate A tile (double buffer)
-  B_DF0, B_DF1, B_DF2, B_DE0, B_DE1, B_DE2, // distance scratch ring
-  B_KF0, B_KF1, B_KE0, B_KE1,               // K* panel stages
+  B_DF0, B_DF1, B_DE0, B_DE1,               // distance scratch ring
+  B_KF0, B_KF1, B_KF2, B_KF3, B_KE0, B_KE1, B_KE2, B_KE3,  // K* panel stages
   B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
   B_SF0, B_SF1,                             // raw candidate rows landed in staging (TMA)
   B_IMG, B_COUNT
@@ -80,7 +85,7 @@ __host__ __device__ inline TcGeom tc_geom(int n, int d) {
   return g;
 }
 
-// dynamic shared memory: image | A tiles x2 | K* stages x2 | staging x2 | row info x4 | partials x2
+// dynamic shared memory: image | A tiles x2 | staging x2 | row info x4 | partials x2
 struct TcSmem {
   int img, a, k, stage, rowinfo, part_mu, part_a1, part_vv, bars, total;
 };
@@ -90,7 +95,7 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   s.img = 0;
   s.a = img_max;
   s.k = s.a + 2 * kb_max * 8192;
-  s.stage = s.k + 2 * kStageBytes;
+  s.stage = s.k;
   s.rowinfo = s.stage + 2 * ((128 * d_max * 4 + 127) & ~127);
   s.part_mu = s.rowinfo + 4 * 128 * 8;
   s.part_a1 = s.part_mu + 2 * 128 * 8;
@@ -148,7 +153,6 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
   const TcSmem L = tc_smem(img_max, kb_max, d_max);
   unsigned char *img = sm + L.img;
   unsigned char *Abuf = sm + L.a;
-  unsigned char *Kbuf = sm + L.k;
   float *stage = reinterpret_cast<float *>(sm + L.stage);
   float2 *rowinfo = reinterpret_cast<float2 *>(sm + L.rowinfo);
   double *part_mu = reinterpret_cast<double *>(sm + L.part_mu);
@@ -166,8 +170,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(bar(B_AF0 + i), 64);
       tc::mbar_init(bar(B_AE0 + i), 1);
-      tc::mbar_init(bar(B_KF0 + i), 8);
-      tc::mbar_init(bar(B_KE0 + i), 1);
+
       tc::mbar_init(bar(B_VF0 + i), 1);
       tc::mbar_init(bar(B_VE0 + i), 8);
       tc::mbar_init(bar(B_SF0 + i), 1);
@@ -175,6 +178,10 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
     for (int i = 0; i < kDepth; ++i) {
       tc::mbar_init(bar(B_DF0 + i), 1);
       tc::mbar_init(bar(B_DE0 + i), 8);
+    }
+    for (int i = 0; i < kKStages; ++i) {
+      tc::mbar_init(bar(B_KF0 + i), 8);
+      tc::mbar_init(bar(B_KE0 + i), 1);
     }
     tc::mbar_init(bar(B_IMG), 1);
     tc::fence_mbar_init();
@@ -187,7 +194,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
 
   // Counters are CTA-global across segments (mbarrier phases continue): tiles gi, distance
   // panels gd, K* panels gk.  Every role advances them identically.
-  uint32_t gi = 0, gd_seg = 0, gk_seg = 0;
+  uint32_t gi = 0, gc_seg = 0, gk_seg = 0;
   uint32_t trc = 0;  // trace event count of this thread
   uint32_t img_phase = 0;
 
@@ -206,40 +213,40 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
     const int n16 = m.n16, npan = m.npan, kb = m.kb;
     const int T = tb - ta;
     const int P = T * npan;
-    const int nvbuf = n16 <= kVBufMaxN ? 2 : 1;
-    const uint32_t scratch0 = nvbuf == 2 ? 2u * kVBufMaxN : 256u;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
     const int tile0 = ta - p.tile_first[s];  // local index of the segment's first tile
 
     if (warp == 11) {
       // ===================================================== MMA issuer (warp 11, warp-uniform)
+      // Distance MMAs come in 64-wide chunks (one chunk feeds two K* panels; a tcgen05.mma costs
+      // max(40, N/2) cycles, so N = 64 halves the distance issue cost of N = 32 panels), kept up to
+      // two chunks ahead of the variance MMAs in a 3-stage TMEM ring.  Counters advance
+      // incrementally (no divisions on the issue path).
       {
         const uint32_t H32 = tc::sdesc_hi(32), H64 = tc::sdesc_hi(64);
         const uint32_t x0 = tc::sdesc_lo(tc::smem_u32(img));
         const uint32_t l0 = tc::sdesc_lo(tc::smem_u32(img + m.off_l));
-        const uint32_t k0 = tc::sdesc_lo(tc::smem_u32(Kbuf));
         const uint32_t abase = tc::sdesc_lo(tc::smem_u32(Abuf));
         const uint32_t xlo = (uint32_t)(n16 * 32) >> 4;  // hi -> lo block of the X^ operand
-        uint32_t gd = gd_seg, gk = gk_seg;
-        int nd = 0;  // next distance panel of the segment
+        const int ndc = (npan + 1) >> 1;                 // distance chunks per tile
+        uint32_t gc = gc_seg, gk = gk_seg;
+        int d_tl = 0, d_q = 0, d_st = (int)(gc % kDepth);  // next chunk to issue
+        uint32_t d_ph = (gc / kDepth) & 1u;
+        int issued_panels = 0;                           // panels covered by issued chunks
+        int v_tl = 0, v_pp = 0;
         for (int g = 0; g < P; ++g) {
-          // keep kDepth distance panels in flight ahead of the variance MMAs
-          while (nd < P && nd < g + kDepth) {
-            const int tl = nd / npan, pp = nd - tl * npan;
-            const uint32_t ti = gi + tl, ab = ti & 1u;
-            if (pp == 0) {
+          while (d_tl < T && issued_panels < g + 4) {
+            const uint32_t ti = gi + d_tl, ab = ti & 1u;
+            if (d_q == 0) {
               tc::mbar_wait(bar(B_AF0 + ab), (ti >> 1) & 1u);
               tc::tc_fence_after();
             }
-            const uint32_t st = gd % kDepth;
-            if (lane == 0) trace_ev(p.trace, 12, 11, gd, trc);
-            tc::mbar_wait(bar(B_DE0 + st), ((gd / kDepth) & 1u) ^ 1u);
-            if (lane == 0) trace_ev(p.trace, 13, 11, gd, trc);
+            tc::mbar_wait(bar(B_DE0 + d_st), d_ph ^ 1u);
             tc::tc_fence_after();
-            const uint32_t idn = tc::idesc_f16((uint32_t)min(32, n16 - 32 * pp));
-            const uint32_t dt = tbase + scratch0 + 32u * st;
+            const uint32_t idn = tc::idesc_f16((uint32_t)min(64, n16 - 64 * d_q));
+            const uint32_t dt = tbase + kScratch0 + 64u * (uint32_t)d_st;
             uint32_t a = abase + ab * (uint32_t)kb * 512u;     // 8192 B per K block
-            uint32_t bq = x0 + (uint32_t)pp * 64u;             // rows 32 pp (1024 B)
+            uint32_t bq = x0 + (uint32_t)d_q * 128u;           // rows 64 q (2048 B)
             for (int k = 0; k < kb; ++k) {
               tc::mma_f16_split(dt, a, H32, bq, H32, idn, k > 0);
               tc::mma_f16_split(dt, a, H32, bq + xlo, H32, idn, 1u);
@@ -247,49 +254,50 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
               a += 512u;
               bq += 2u * xlo;
             }
-            tc::mma_commit_warp(bar(B_DF0 + st));
-            if (lane == 0) trace_ev(p.trace, 4, 11, gd, trc);
-            if (pp == npan - 1) tc::mma_commit_warp(bar(B_AE0 + ab));  // A tile consumed
-            ++gd;
-            ++nd;
-          }
-          // variance MMAs of panel g
-          const int tl = g / npan, pp = g - tl * npan;
-          const uint32_t ti = gi + tl;
-          const uint32_t vb = nvbuf == 2 ? (ti & 1u) : 0u;
-          const uint32_t vuse = nvbuf == 2 ? (ti >> 1) : ti;  // uses of this V buffer so far
-          const uint32_t ks = gk & 1u;
-          if (lane == 0) trace_ev(p.trace, 1, 11, gk, trc);
-          tc::mbar_wait(bar(B_KF0 + ks), (gk >> 1) & 1u);
-          if (lane == 0) trace_ev(p.trace, 2, 11, gk, trc);
-          tc::tc_fence_after();
-          if (pp == 0) {
-            tc::mbar_wait(bar(B_VE0 + vb), (vuse & 1u) ^ 1u);
-            tc::tc_fence_after();
-          }
-          if (lane == 0) trace_ev(p.trace, 15, 11, gk, trc);
-          const uint32_t kbs = k0 + ks * (kStageBytes >> 4);
-          const uint32_t R16 = (uint32_t)(n16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
-          const uint32_t lp = l0 + (uint32_t)(pp * n16 - 16 * pp * (pp - 1)) * 8u;
-          const uint32_t vcol = tbase + vb * kVBufMaxN;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j0 = 32 * pp + 16 * h;
-            if (j0 < n16) {
-              const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
-              const uint32_t dt = vcol + (uint32_t)j0;
-              const uint32_t ka = kbs + 2u * h;        // +32 B k-advance
-              const uint32_t lb = lp + 66u * h;        // +1024 B rows, +32 B k-advance
-              tc::mma_f16_split(dt, ka, H64, lb, H64, idn, (pp | h) ? 1u : 0u);
-              tc::mma_f16_split(dt, ka, H64, lb + R16, H64, idn, 1u);
-              tc::mma_f16_split(dt, ka + 512u, H64, lb, H64, idn, 1u);  // K* lo: +8192 B
+            tc::mma_commit_warp(bar(B_DF0 + d_st));
+            if (lane == 0) trace_ev(p.trace, 4, 11, gc, trc);
+            issued_panels += min(2, npan - 2 * d_q);
+            if (++d_st == kDepth) { d_st = 0; d_ph ^= 1u; }
+            if (++d_q == ndc) {
+              tc::mma_commit_warp(bar(B_AE0 + ab));  // A tile consumed
+              d_q = 0;
+              ++d_tl;
             }
           }
-          if (lane == 0) trace_ev(p.trace, 14, 11, gk, trc);
+          // variance MMAs of panel g = (v_tl, v_pp)
+          const uint32_t ks = gk % kKStages;
+          if (lane == 0) trace_ev(p.trace, 1, 11, gk, trc);
+          tc::mbar_wait(bar(B_KF0 + ks), (gk / kKStages) & 1u);
+          if (lane == 0) trace_ev(p.trace, 2, 11, gk, trc);
+          tc::tc_fence_after();
+          if (v_pp == 0) {
+            tc::mbar_wait(bar(B_VE0), ((gi + v_tl) & 1u) ^ 1u);
+            tc::tc_fence_after();
+          }
+          const uint32_t kt = tbase + kKstar0 + 32u * ks;  // K* stage in TMEM
+          const uint32_t R16 = (uint32_t)(n16 - 32 * v_pp) * 4u;  // R * 64 B >> 4: hi -> lo
+          const uint32_t lp = l0 + (uint32_t)(v_pp * n16 - 16 * v_pp * (v_pp - 1)) * 8u;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j0 = 32 * v_pp + 16 * h;
+            if (j0 < n16) {
+              const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
+              const uint32_t dt = tbase + (uint32_t)j0;
+              const uint32_t ka = kt + 8u * h;         // k step h: hi at +8h, lo at +16 + 8h
+              const uint32_t lb = lp + 66u * h;        // +1024 B rows, +32 B k-advance
+              tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | h) ? 1u : 0u);
+              tc::mma_f16_ts(dt, ka, lb + R16, H64, idn, 1u);
+              tc::mma_f16_ts(dt, ka + 16u, lb, H64, idn, 1u);
+            }
+          }
           tc::mma_commit_warp(bar(B_KE0 + ks));
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
-          if (pp == npan - 1) tc::mma_commit_warp(bar(B_VF0 + vb));
+          if (++v_pp == npan) {
+            tc::mma_commit_warp(bar(B_VF0));
+            v_pp = 0;
+            ++v_tl;
+          }
         }
       }
       __syncwarp();
@@ -387,20 +395,19 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
       const float2 *ap = reinterpret_cast<const float2 *>(img + m.off_a);
       const int kind = m.kernel;
       const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
-      const uint32_t k0 = tc::smem_u32(Kbuf);
-      uint32_t gd = gd_seg, gk = gk_seg;
+      uint32_t gk = gk_seg;
+      uint32_t ec = gc_seg;  // distance chunk counter
       double mu = 0.0;
       float a1 = 0.f;
       // drain + finish of segment tile tl (V accumulator complete); called one panel late
       auto drain_finish = [&](int tl, double mu_t, float a1_t) {
         const uint32_t ti = gi + tl;
-        const uint32_t vb = nvbuf == 2 ? (ti & 1u) : 0u;
-        const uint32_t vuse = nvbuf == 2 ? (ti >> 1) : ti;
-        tc::mbar_wait(bar(B_VF0 + vb), vuse & 1u);
+        const uint32_t vb = 0u;
+        tc::mbar_wait(bar(B_VF0), ti & 1u);
         tc::tc_fence_after();
         float vv = 0.f;
         const int hc = n16 >> 1;
-        const uint32_t va = tl_addr + vb * kVBufMaxN;
+        const uint32_t va = tl_addr;
         int c = half * hc;
         const int ce = c + hc;
         for (; c + 16 <= ce; c += 16) {
@@ -425,7 +432,8 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_VE0 + vb));
+        if (lane == 0) tc::mbar_arrive(bar(B_VE0));
+        (void)vb;
         const int pb = (ti & 1u) * 128;
         if (half == 1) {
           part_mu[pb + row] = mu_t;
@@ -453,27 +461,30 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
                       (flags & kFlagUnsafe) != 0u, 2, 128, 0);
         }
       };
+      int tl = 0, pp = 0;
       for (int g = 0; g < P; ++g) {
-        const int tl = g / npan, pp = g - tl * npan;
-        const uint32_t st = gd % kDepth;
+        const uint32_t st = ec % kDepth;
         const int jb = 32 * pp + 16 * half;
         const bool active = jb < n16;
         const bool trw = (warp == 0 || warp == 7) && lane == 0;
         if (trw) trace_ev(p.trace, 5, warp, gk, trc);
-        tc::mbar_wait(bar(B_DF0 + st), (gd / kDepth) & 1u);
+        tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
         if (trw) trace_ev(p.trace, 6, warp, gk, trc);
         tc::tc_fence_after();
         uint32_t hr[16];
         if (active) {
-          tc::tmem_ld16(tl_addr + scratch0 + 32u * st + 16u * half, hr);
+          tc::tmem_ld16(tl_addr + kScratch0 + 64u * st + 32u * (pp & 1) + 16u * half, hr);
           tc::tmem_wait_ld();
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
-        ++gd;
-        const uint32_t ks = gk & 1u;
-        tc::mbar_wait(bar(B_KE0 + ks), ((gk >> 1) & 1u) ^ 1u);
+        if ((pp & 1) || pp == npan - 1) {  // both panels of the chunk loaded: free the stage
+          if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
+          ++ec;
+        }
+        const uint32_t ks = gk % kKStages;
+        tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
+        tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
         if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         float muf = 0.f, a1f = 0.f;
         if (active) {
@@ -506,21 +517,19 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             hw[q] = tc::pack_f16x2(h0, h1);
             lw[q] = tc::pack_f16x2(kv[2 * q] - h0, kv[2 * q + 1] - h1);
           }
-          const uint32_t base = k0 + ks * kStageBytes;
-          const uint32_t o0 = tc::sw_offset(row, 32 * half, 64);
-          const uint32_t o1 = tc::sw_offset(row, 32 * half + 16, 64);
-          sts128(base + o0, hw[0], hw[1], hw[2], hw[3]);
-          sts128(base + o1, hw[4], hw[5], hw[6], hw[7]);
-          sts128(base + 8192 + o0, lw[0], lw[1], lw[2], lw[3]);
-          sts128(base + 8192 + o1, lw[4], lw[5], lw[6], lw[7]);
-          tc::fence_proxy_async();
+          // this warp's 16 k values are k step `half` of the panel
+          const uint32_t kt = tl_addr + kKstar0 + 32u * ks + 8u * half;
+          tc::tmem_st8(kt, hw);
+          tc::tmem_st8(kt + 16u, lw);
+          tc::tmem_wait_st();
         }
+        tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_KF0 + ks));
         if (trw) trace_ev(p.trace, 8, warp, gk, trc);
         ++gk;
         if (pp == 0 && tl > 0) {
-          // tile tl-1 is complete: drain it now, one panel late, so the V MMAs never wait
+          // tile tl-1 is complete: drain it now, one panel late
           drain_finish(tl - 1, mu, a1);
           mu = (double)muf;
           a1 = a1f;
@@ -528,11 +537,12 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           mu += (double)muf;
           a1 += a1f;
         }
+        if (++pp == npan) { pp = 0; ++tl; }
       }
       if (P > 0) drain_finish(T - 1, mu, a1);
     }
     gi += (uint32_t)T;
-    gd_seg += (uint32_t)P;
+    gc_seg += (uint32_t)(T * ((npan + 1) >> 1));
     gk_seg += (uint32_t)P;
     ta = tb;
   }

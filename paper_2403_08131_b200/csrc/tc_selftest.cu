@@ -42,7 +42,37 @@ tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base;
-  if (tid == 0) {
+  if (timing < 0) {
+    // A operand from TMEM: thread = row, 16 fp16 of one k step packed in 8 columns (k = 2c, 2c+1)
+    const int row = warp * 32 + lane;
+    for (int s = 0; s < K / 16; ++s) {
+      uint32_t r[8];
+      for (int c = 0; c < 8; ++c) {
+        const __half lo = A[row * K + 16 * s + 2 * c], hi = A[row * K + 16 * s + 2 * c + 1];
+        r[c] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+      }
+      tc::tmem_st8(tbase + ((uint32_t)(warp * 32) << 16) + 256 + 8 * s, r);
+    }
+    tc::tmem_wait_st();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 0) {
+      const uint32_t b0 = tc::smem_u32(Bs);
+      const uint32_t H = tc::sdesc_hi(row_bytes);
+      const uint32_t idesc = tc::idesc_f16(N);
+      int first = 1;
+      for (int kb = 0; kb < nkb; ++kb)
+        for (int s = 0; s < kpb / 16; ++s) {
+          const uint32_t blo = tc::sdesc_lo(b0 + kb * Nb * row_bytes +
+                                            (b_row_off / 8) * 8 * row_bytes + s * 32);
+          tc::mma_f16_ts(tbase, tbase + 256 + 8 * (kb * (kpb / 16) + s), blo, H, idesc,
+                         first ? 0u : 1u);
+          first = 0;
+        }
+      tc::mma_commit_warp(tc::smem_u32(&bar));
+    }
+  } else if (tid == 0) {
     const uint32_t a0 = tc::smem_u32(As), b0 = tc::smem_u32(Bs);
     const uint32_t idesc = tc::idesc_f16(N);
     int first = 1;
@@ -57,7 +87,7 @@ tc_selftest_kernel(const __half *A, const __half *B, float *D, int N, int K, int
     tc::mma_commit(tc::smem_u32(&bar));
   }
   tc::mbar_wait(tc::smem_u32(&bar), 0);
-  if (timing && warp == 0) {
+  if (timing > 0 && warp == 0) {
     // issue-rate microbenchmark: `timing` repetitions of the same accumulate MMA by the whole
     // warp (elected lane), clock64 after issue and after completion
     const uint32_t H = tc::sdesc_hi(row_bytes);
@@ -108,6 +138,7 @@ extern "C" gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int
     return GPBO_ECUDA;
   long long *cyc = nullptr;
   if (reps > 0 && cudaMalloc(&cyc, 16) != cudaSuccess) return GPBO_ECUDA;
+  // reps < 0: A operand staged in TMEM (tcgen05.st) and read by the MMA from TMEM
   gpbo::tc_selftest_kernel<<<1, 128, smem>>>((const __half *)A, (const __half *)B, D, N, K,
                                              row_bytes, b_row_off, reps, cyc);
   if (reps > 0) {
