@@ -87,8 +87,25 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
       ei_hi = INFINITY;
       ei_lo = 0.f;
     } else {
-      ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
-      ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
+      // Cheap screen (argmax mode): for z = (best - mu_lo)/s_hi < 0, Gordon's inequality
+      // Phi(-x) >= x phi(x)/(1 + x^2) gives EI <= s_hi phi(z)/(1 + z^2) -- one exp instead of
+      // the two erfc-based bracket ends.  A candidate whose screen is below the running
+      // threshold cannot be the argmax: EI_hi := screen, EI_lo := 0 (both still valid bounds).
+      bool screened = false;
+      if (p.mode == kModeArgmax) {
+        const float thr = __uint_as_float(*(volatile const unsigned int *)(p.thr + s));
+        const float s_hi = sqrtf(var + dvar);
+        const float z = (float)(best - (mu - (double)dmu)) / s_hi;
+        if (s_hi > 0.f && z < 0.f) {
+          const float ub = s_hi * 0.398942280401432678f * __expf(-0.5f * z * z) /
+                           fmaf(z, z, 1.f) * 1.001f;
+          if (ub < thr) { ei_hi = ub; ei_lo = 0.f; screened = true; }
+        }
+      }
+      if (!screened) {
+        ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
+        ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
+      }
     }
   }
   if (p.mode == kModePosterior) {
@@ -105,6 +122,7 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
   }
   __shared__ unsigned int s_thr[32];
   __shared__ unsigned long long s_zk[32];
+  const unsigned int thr_entry = *(volatile const unsigned int *)(p.thr + s);
   const uint64_t gidx = (uint64_t)(p.m_base[s] + row);
   unsigned int lo_bits = ok ? __float_as_uint(fmaxf(ei_lo, 0.f)) : 0u;
   unsigned long long zkey = (ok && !(ei_hi > 0.f)) ? make_key(0.f, gidx) : 0ull;
@@ -127,9 +145,11 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
       zk = q > zk ? q : zk;
     }
     if (lane == 0) {
-      const unsigned int old = atomicMax(p.thr + s, lb);
+      // fire-and-forget threshold update; the decision uses the global value read at entry
+      // (any stale value <= the final threshold only flags more candidates)
+      atomicMax(p.thr + s, lb);
       if (zk) atomicMax(p.keys + s, zk);
-      s_thr[0] = max(old, lb);
+      s_thr[0] = max(thr_entry, lb);
     }
   }
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");

@@ -135,6 +135,9 @@ __device__ __forceinline__ int search_of(const int32_t *tile_first, int S, int t
 // 16384 entries (fire-and-forget stores, no atomics): slot = role slice + 2 * local count
 __device__ __forceinline__ void trace_ev(unsigned long long *tr, uint32_t tag, uint32_t role,
                                          uint32_t idx, uint32_t &cnt) {
+#ifndef GPBO_TC_TRACE
+  return;  // compiled out unless built with -DGPBO_TC_TRACE (tools/trace_tc.py)
+#endif
   if (tr == nullptr || blockIdx.x != 0) return;
   const unsigned long long c = clock64();
   const uint32_t slice = role == 11 ? 0u : role == 8 ? 1u : role == 0 ? 2u : 3u;
@@ -410,7 +413,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         const uint32_t va = tl_addr;
         int c = half * hc;
         const int ce = c + hc;
-        for (; c + 16 <= ce; c += 16) {
+        for (; c + 16 <= ce; c += 16) {  // (x32 batching spills at the 168-register cap)
           uint32_t r16[16];
           tc::tmem_ld16(va + (uint32_t)c, r16);
           tc::tmem_wait_ld();
@@ -462,26 +465,35 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         }
       };
       int tl = 0, pp = 0;
-      for (int g = 0; g < P; ++g) {
+      // Software pipeline: the distances of panel g+1 are loaded from TMEM (tcgen05.ld) before
+      // panel g is computed, so the TMEM load latency overlaps the MUFU/FMA work.
+      uint32_t hbuf[2][16];
+      auto load_dist = [&](int ppn, uint32_t chunk, uint32_t (&dst)[16]) {
+        const uint32_t st = chunk % kDepth;
+        tc::mbar_wait(bar(B_DF0 + st), (chunk / kDepth) & 1u);
+        tc::tc_fence_after();
+        if (32 * ppn + 16 * half < n16)
+          tc::tmem_ld16(tl_addr + kScratch0 + 64u * st + 32u * (ppn & 1) + 16u * half, dst);
+      };
+      // two register buffers swapped by alternating calls (no dynamic register indexing)
+      auto step = [&](int g, uint32_t (&hr)[16], uint32_t (&nx)[16]) {
         const uint32_t st = ec % kDepth;
         const int jb = 32 * pp + 16 * half;
         const bool active = jb < n16;
         const bool trw = (warp == 0 || warp == 7) && lane == 0;
-        if (trw) trace_ev(p.trace, 5, warp, gk, trc);
-        tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
-        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
-        tc::tc_fence_after();
-        uint32_t hr[16];
-        if (active) {
-          tc::tmem_ld16(tl_addr + kScratch0 + 64u * st + 32u * (pp & 1) + 16u * half, hr);
-          tc::tmem_wait_ld();
-        }
+        tc::tmem_wait_ld();  // panel g's distances are in hr
         tc::tc_fence_before();
         __syncwarp();
-        if ((pp & 1) || pp == npan - 1) {  // both panels of the chunk loaded: free the stage
+        const bool chunk_done = (pp & 1) || pp == npan - 1;
+        if (chunk_done) {  // both panels of the chunk loaded: free the stage
           if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
           ++ec;
         }
+        if (g + 1 < P) {  // prefetch panel g+1
+          const int np = pp + 1 == npan ? 0 : pp + 1;
+          load_dist(np, ec, nx);
+        }
+        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
         const uint32_t ks = gk % kKStages;
         tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
         tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
@@ -538,6 +550,11 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           a1 += a1f;
         }
         if (++pp == npan) { pp = 0; ++tl; }
+      };
+      if (P > 0) load_dist(0, ec, hbuf[0]);
+      for (int g = 0; g < P; g += 2) {
+        step(g, hbuf[0], hbuf[1]);
+        if (g + 1 < P) step(g + 1, hbuf[1], hbuf[0]);
       }
       if (P > 0) drain_finish(T - 1, mu, a1);
     }

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpbo.so")
+# GPBO_LIB selects an alternative in-tree build (A/B kernel experiments); default: the package copy
+LIB_PATH = os.environ.get("GPBO_LIB") or os.path.join(_HERE, "libgpbo.so")
 
 OK, EINVAL, ENOTPD, WDEGENERATE, ESAMPLING, ECUDA, ENCCL, ENOMEM, ENOTSUP = range(9)
 RBF, MATERN52 = 0, 1
