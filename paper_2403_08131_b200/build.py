@@ -41,6 +41,9 @@ def build(verbose=False, force=False):
     hdr_t = max(os.path.getmtime(h) for h in headers)
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "-Xptxas", "-v", "-I", inc, "-I", os.path.join(ROOT, "include")]
+    if os.environ.get("GPBO_FIT_TIMING"):  # fit phase clocks (printf from CTA 0)
+        common += ["-DGPBO_FIT_TIMING"]
+        force = True
     if os.environ.get("GPBO_TC_TRACE"):  # clock64 pipeline trace hooks (tools/trace_tc.py)
         common += ["-DGPBO_TC_TRACE"]
         force = True

@@ -61,6 +61,7 @@ struct gpbo_model {
   double *Xs64 = nullptr;
   unsigned char *img = nullptr;  // tcgen05 operand images
   int64_t img_bytes = 0;
+  mutable bool simt_ready = false;  // Xs32 / LT32 built (on first CUDA-core scoring call)
 };
 
 namespace {
@@ -215,6 +216,12 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   if (ctx->score_impl == 2 && !use_tc)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
   const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;
+  if (!use_tc && !model->simt_ready) {
+    CK(gpbo::launch_simt_operands(model->meta_d, model->S, model->X32, model->ls32,
+                                  model->Linv64, model->Xs32, model->LT32, ctx->stream));
+    ctx->launches += 1;
+    model->simt_ready = true;
+  }
   h_tiles[0] = 0;
   int64_t xo = 0;
   for (int i = 0; i < S; ++i) {
@@ -480,7 +487,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   m->device = ctx->device;
   m->stream = ctx->stream;
   m->meta.resize(S);
-  int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0;
+  int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0, nscr = 0;
   int smem_max = 0;
   for (int s = 0; s < S; ++s) {
     const int n = a->n[s], d = a->d[s];
@@ -504,9 +511,9 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     q.a_off = na; na += q.n_pad;
     q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
     gpbo::tc_fill_geometry(q);
-    const int nr = (n + 1) & ~1;
     q.use_smem = n <= gpbo::kFitSmemMaxN;
-    const int smem = (3 * nr + (q.use_smem ? n * (n + 1) / 2 : 0)) * 8;
+    if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
+    const int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
     smem_max = std::max(smem_max, smem);
     m->nmax = std::max(m->nmax, n);
     m->dmax = std::max(m->dmax, q.d_pad);
@@ -532,7 +539,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   const size_t o_x = take(nx * 4), o_ls = take(nls * 4), o_xs = take(nxs * 4);
   const size_t o_lt = take(nlt * 4), o_y = take(ny * 8), o_L = take(nmat * 8);
   const size_t o_Li = take(nmat * 8), o_a = take(na * 8), o_img = take(nimg);
-  const size_t o_x64 = take(nx * 8);
+  const size_t o_x64 = take(nx * 8), o_scr = take(nscr * 8);
   cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
   if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
   m->meta_d = (SearchMeta *)(m->block + o_meta);
@@ -547,6 +554,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   m->alpha64 = (double *)(m->block + o_a);
   m->img = (unsigned char *)(m->block + o_img);
   m->Xs64 = (double *)(m->block + o_x64);
+  double *Wscr64 = (double *)(m->block + o_scr);
   m->img_bytes = nimg;
   const cudaMemcpyKind kind = a->mem == GPBO_HOST ? cudaMemcpyHostToDevice
                                                   : cudaMemcpyDeviceToDevice;
@@ -569,7 +577,7 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   {
     KernTimer t(ctx, kKernFit);
     CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
-                         m->Xs32, m->Xs64, m->LT32, m->alpha64, m->meta_d, ctx->stream));
+                         m->Xs64, m->alpha64, Wscr64, m->meta_d, ctx->stream));
   }
   ctx->launches += 1;
   if (nimg > 0) {
@@ -628,8 +636,8 @@ gpbo_status gp_model_export(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, d
     CK(cudaMemcpyAsync(buf.data(), srcs[w] + q.mat_off, buf.size() * 8, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    for (int j = 0; j < n; ++j)      // col-major device -> row-major caller
-      for (int i = 0; i < n; ++i) outs[w][(size_t)i * n + j] = buf[(size_t)j * n + i];
+    for (int j = 0; j < n; ++j)  // col-major device (lower part) -> row-major caller
+      for (int i = 0; i < n; ++i) outs[w][(size_t)i * n + j] = i >= j ? buf[(size_t)j * n + i] : 0.0;
   }
   if (alpha) {
     CK(cudaMemcpyAsync(alpha, model->alpha64 + q.a_off, n * 8, cudaMemcpyDeviceToHost,

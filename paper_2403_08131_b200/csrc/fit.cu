@@ -4,12 +4,29 @@
 // PAPER.md L249/L256 (§IV.D): the GP's "O(N^3) training complexity" is this factorisation.
 // The kernel/jitter/standardisation readings are R1, R2, R7, R9 of DESIGN.md.
 //
-// Layout: the working matrix A is the lower triangle of an n x n float64 matrix, column-major
-// (column j contiguous from its diagonal down).  For n <= kFitSmemMaxN it lives in shared memory,
-// packed (column j starts at j n - j (j - 1) / 2, 216 KB at n = 232); otherwise the CTA works in
-// place, unpacked, in the model's global Linv64 buffer (L2 resident).  Accesses go through the
-// column-base function cb(j) and generic pointers, so the same code serves both cases.
+// Layout: the working matrix W is the lower triangle of an n x n float64 matrix stored as the
+// lower triangle of 8 x 8 tiles, each tile row-major (= the DMMA accumulator fragment order).
+// For n <= kFitSmemMaxN it lives in shared memory (189 KB at n = 216); otherwise in a global
+// scratch buffer of the model (L2 resident).
+//
+// Factorisation (H3) and inversion (H4) are ONE elimination sweep: the row operations that reduce
+// K to L^T, applied to I, give L^-1 ([K | I] -> [L^T | L^-1] up to the row scaling).  Both halves
+// share one lower triangle W: after step j, W(i, k) holds L^-1 for k <= j and the reduced K for
+// k > j.  Step j (pivot p = W(j, j), column c_i = W(i, j), i > j; g = row j left of j and column
+// j below it):  W(i, k) -= (c_i / p) g_k for i > j with W(i, j) := -c_i / p;  row j *= 1/sqrt(p);
+// L(i, j) = c_i / sqrt(p).  Blocked by kFitB = 8 steps (block [J, J + 8)):
+//   D  the 8 x 8 diagonal block, sequentially in one warp (registers + shuffles).  The steps act
+//      linearly on any other row's 8 block entries x and on any block column w left of the
+//      block, so the same warp also runs them on unit vectors and records three 8 x 8 maps:
+//        row i below the block:  L(i, J + u) = (x N)_u,   new W(i, J + k) = (x M)_k
+//        column k left of it:    new W(J + t, k) = (R w)_t  (= L^-1(J + t, k), final)
+//   C  those two products for all rows below / columns left of the block on the FP64 tensor
+//      cores (DMMA m8n8k4); the L panel and the final block rows of L^-1 go to G[u][.];
+//   T  the rest: W(i, k) -= sum_u G[u][i] G[u][k] over rows below the block x (columns left of
+//      it and the trailing triangle), 8 x 8 DMMA tiles dealt to the warps.  Warp 0 updates the
+//      next diagonal block first and runs its D while the other warps finish T (look-ahead).
 #include <cmath>
+#include <cstdio>
 
 #include "gpbo_internal.cuh"
 
@@ -17,6 +34,13 @@ namespace gpbo {
 namespace {
 
 constexpr int kWarps = kFitThreads / 32;
+static_assert(kFitB == 8, "the DMMA tiling of fit.cu assumes 8-step panels");
+
+#ifdef GPBO_FIT_TIMING  // phase clocks of CTA 0 printed at exit (tools/fit_phases.py)
+#define FIT_T(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) fit_t[slot] += clock64() - fit_t0; fit_t0 = clock64(); } while (0)
+#else
+#define FIT_T(slot) do { } while (0)
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -48,6 +72,20 @@ struct AddOp { __device__ double operator()(double a, double b) const { return a
 struct MaxOp { __device__ double operator()(double a, double b) const { return fmax(a, b); } };
 struct MinOp { __device__ double operator()(double a, double b) const { return fmin(a, b); } };
 
+// 1 / sqrt(p): the MUFU approximation refined by two Newton steps (quadratic convergence from
+// ~2^-22 to the float64 rounding level) -- short latency, no special-case branches (a failed
+// pivot is flagged by the caller and its values discarded).
+__device__ __forceinline__ double rsqrt_fast(double p) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-p, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
 __device__ __forceinline__ double kernel_value(double r2, double sf2, int kind) {
   if (kind == GPBO_RBF) return sf2 * exp(-0.5 * r2);
   const double r = sqrt(r2);
@@ -55,27 +93,58 @@ __device__ __forceinline__ double kernel_value(double r2, double sf2, int kind) 
   return sf2 * (1.0 + s5 * r + (5.0 / 3.0) * r2) * exp(-s5 * r);
 }
 
-// The body is instantiated for a shared-memory (packed) and a global (unpacked) working matrix so
-// that every access to A compiles to LDS/STS or LDG/STG instead of generic loads.
+// D = A B + D on the FP64 tensor cores, m8n8k4: lane l holds A[l/4][l%4], B[l%4][l/4] and
+// D[l/4][2 (l%4)], D[l/4][2 (l%4) + 1].
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// Tile (R, C), C <= R, of the tile-packed lower triangle: 64 doubles, row-major.  The
+// row-major 8 x 8 order IS the DMMA accumulator fragment order (lane l holds elements 2l and
+// 2l + 1), so accumulator tiles move with one 16-byte access per lane.
+__device__ __forceinline__ int tb(int R, int C) { return (R * (R + 1) / 2 + C) * 64; }
+
+// Tile index e -> (R, C) of the lower triangle, row-major.
+__device__ __forceinline__ void tile_rc(int e, int &R, int &C) {
+  R = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);
+  while ((R + 1) * (R + 2) / 2 <= e) ++R;
+  while (R * (R + 1) / 2 > e) --R;
+  C = e - R * (R + 1) / 2;
+}
+
+// The body is instantiated for a shared-memory and a global working matrix so that every access
+// to W compiles to LDS/STS or LDG/STG instead of generic loads.
 template <bool kSmem>
 __device__ __forceinline__ void fit_body(double *sm, double *red,
                                          const SearchMeta *__restrict__ meta_in,
                                          const float *__restrict__ X32,
                                          const float *__restrict__ ls32,
                                          const double *__restrict__ y64, double *L64,
-                                         double *Linv64, float *Xs32, double *Xs64, float *LT32,
-                                         double *alpha64, SearchMeta *__restrict__ meta_out) {
+                                         double *Linv64, double *Xs64, double *alpha64,
+                                         double *Wscr64, SearchMeta *__restrict__ meta_out) {
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;  // DMMA fragment coordinates
   SearchMeta m = meta_in[s];
   const int n = m.n, d = m.d;
-  const int nr = (n + 1) & ~1;
-  double *yt = sm;
-  double *tmp = sm + nr;
-  double *w = sm + 2 * nr;
-  double *A = kSmem ? sm + 3 * nr : Linv64 + m.mat_off;
-  // A(i, j), i >= j, lives at A[cb(j) + i]
-  auto cb = [&](int j) -> int { return kSmem ? j * n - (j * (j - 1)) / 2 - j : j * n; };
+#ifdef GPBO_FIT_TIMING
+  long long fit_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long fit_t0 = clock64();
+  long long fit_tw = 0, fit_tD = 0;
+#endif
+  const int nr8 = fit_nr8(n), gs = fit_gstride(n), nt = (n + 7) / 8;
+  double *yt = sm;                     // y~ (n)
+  double *w = sm + nr8;                // L^-1 y~ (n)
+  double *piv = sm + 2 * nr8;          // [16]: the last D's fail flag (rest spare)
+  double *Mm = piv + 24;               // the block maps M, N, R (8 x 8 each, row-major)
+  double *Nm = Mm + 64;
+  double *Rm = Nm + 64;
+  double *G = Rm + 64;                 // G[u][.], 8 rows of gs
+  double *W = kSmem ? G + 8 * gs : Wscr64 + m.scr_off;
+  // element (i, k), i >= k
+  auto at = [&](int i, int k) -> int { return tb(i >> 3, k >> 3) + 8 * (i & 7) + (k & 7); };
+  double *Lg = L64 + m.mat_off;        // L, col-major (lower part; export zeroes the rest)
   const float *X = X32 + m.x_off;
   const float *ls = ls32 + m.ls_off;
   const double *y = y64 + m.y_off;
@@ -110,65 +179,243 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   }
   const double best = block_reduce(bmin, red, MinOp(), INFINITY);
 
-  // ---- scoring operands: X / l in float32 (IEEE division), zero padded to n_pad x d_pad,
-  // and in float64 (n x d) for the refine phase; pmax = max_j |x_j / l|^2
-  for (int e = tid; e < m.n_pad * m.d_pad; e += kFitThreads) {
-    const int i = e / m.d_pad, c = e - i * m.d_pad;
-    Xs32[m.xs_off + e] = (i < n && c < d) ? __fdiv_rn(X[i * d + c], ls[c]) : 0.f;
-  }
+  // ---- x / l in float64, column-major (d x n), for the Gram, the refine phase and the
+  // tcgen05 image; pmax = max_j |x_j / l|^2
   double pm = 0.0;
   for (int i = tid; i < n; i += kFitThreads) {
     double q = 0.0;
     for (int c = 0; c < d; ++c) {
       const double v = (double)X[i * d + c] / (double)ls[c];
-      Xs64[m.x_off + (size_t)c * n + i] = v;  // column-major: x/l of point i, dim c
+      Xs64[m.x_off + (size_t)c * n + i] = v;
       q += v * v;
     }
     pm = fmax(pm, q);
   }
   const double pmax = block_reduce(pm, red, MaxOp(), 0.0);
 
-  // ---- H2 + H3: Gram matrix and Cholesky with the jitter ladder j_k = 1e-8 10^k sf2
+  // ---- H2 + H3 + H4 along the jitter ladder j_k = 1e-8 10^k sf2
   const double sf2 = m.sf2, sn2 = m.sn2;
+  const double *xc = Xs64 + m.x_off;
+  const int ntiles = nt * (nt + 1) / 2;
+
+  // D (warp 0): the diagonal block A11 = W[J..J+8, J..J+8) (padded with identity rows for a
+  // ragged last block).  Lane 0 factors it in registers, L11 = chol(A11) and X = L11^-1 (in
+  // place, column by column); then the warp forms the maps C applies (see the header):
+  //   N = X^T  (L21 = A21 L11^-T),  M = -X^T X  (= -A11^-1),  R = X.
+  // The diagonal block of W becomes X (its final L^-1 entries); piv[16] flags a pivot <= 0.
+  auto diag_block = [&](int J) {
+    const int bb = min(kFitB, n - J);
+    double *Wd = W + tb(J >> 3, J >> 3);
+    if (lane == 0) {
+      double a[36];  // packed lower, row-major: (i, k) at i (i + 1) / 2 + k
+      double rr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k <= i; ++k)
+          a[i * (i + 1) / 2 + k] = i < bb ? Wd[8 * i + k] : (i == k ? 1.0 : 0.0);
+      bool fail = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // right-looking Cholesky
+        const double p = a[j * (j + 1) / 2 + j];
+        fail |= !(p > 0.0) || !isfinite(p);
+        const double r = rsqrt_fast(p);
+        rr[j] = r;
+        a[j * (j + 1) / 2 + j] = p * r;
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i) a[i * (i + 1) / 2 + j] *= r;
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i)
+#pragma unroll
+          for (int k = j + 1; k <= i; ++k)
+            a[i * (i + 1) / 2 + k] = fma(-a[i * (i + 1) / 2 + j], a[k * (k + 1) / 2 + j],
+                                         a[i * (i + 1) / 2 + k]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)  // L11 -> Nm (scratch until the maps are formed)
+#pragma unroll
+        for (int k = 0; k <= i; ++k) Nm[8 * i + k] = a[i * (i + 1) / 2 + k];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // X = L^-1 in place: X_ij = -r_i sum_{k=j}^{i-1} L_ik X_kj
+        a[j * (j + 1) / 2 + j] = rr[j];
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = j; k < i; ++k) t = fma(a[i * (i + 1) / 2 + k], a[k * (k + 1) / 2 + j], t);
+          a[i * (i + 1) / 2 + j] = -rr[i] * t;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)  // X -> Rm (lower part)
+#pragma unroll
+        for (int k = 0; k <= i; ++k) Rm[8 * i + k] = a[i * (i + 1) / 2 + k];
+      piv[16] = fail ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    // the warp spreads the outputs: L11 to L64, X to the diagonal tile, R = X, N = X^T
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h, i = e >> 3, k = e & 7;
+      if (k <= i && i < bb) Lg[(size_t)(J + k) * n + J + i] = Nm[e];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h, i = e >> 3, k = e & 7;
+      const double v = k <= i ? Rm[e] : 0.0;
+      Wd[e] = v;
+      Nm[8 * k + i] = v;
+      if (k > i) Rm[e] = 0.0;
+    }
+    __syncwarp();
+    // M = -X^T X: lane -> entries (mr, mc) = (e / 8, e % 8), e = lane, lane + 32
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h, mr = e >> 3, mc = e & 7;
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t = fma(Rm[q * 8 + mr], Rm[q * 8 + mc], t);
+      Mm[e] = -t;
+    }
+  };
+
   int jk = -1;
   double jit = 0.0;
   double p10 = 1.0;
-  for (int k = 0; k < 7; ++k, p10 *= 10.0) {
+  FIT_T(0);
+  for (int k = 0; k < 7 && jk < 0; ++k, p10 *= 10.0) {
     jit = 1e-8 * p10 * sf2;
     __syncthreads();
-    for (int j = warp; j < n; j += kWarps) {
-      const double *xc = Xs64 + m.x_off;  // column-major (d x n): coalesced across lanes
-      for (int i = j + lane; i < n; i += 32) {
-        // x / l precomputed in float64 above (the oracle's A / l, B / l then difference)
-        double r2 = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double diff = xc[(size_t)c * n + i] - xc[(size_t)c * n + j];
-          r2 += diff * diff;
+    // H2: one 8 x 8 tile per warp item, two entries per lane (its accumulator-fragment slots):
+    // squared distances of x / l by direct differences (reading R1), the kernel, + sn2 + jitter
+    // on the diagonal; entries outside the matrix are stored as 0
+    for (int e = warp; e < ntiles; e += kWarps) {
+      int R, C;
+      tile_rc(e, R, C);
+      const int i = 8 * R + gid, kc = 8 * C + 2 * tig;
+      const int ia = min(i, n - 1), k0 = min(kc, n - 1), k1 = min(kc + 1, n - 1);
+      double r0 = 0.0, r1 = 0.0;
+      for (int c = 0; c < d; ++c) {
+        const double *col = xc + (size_t)c * n;
+        const double xi = __ldg(col + ia);
+        const double d0 = xi - __ldg(col + k0), d1 = xi - __ldg(col + k1);
+        r0 = fma(d0, d0, r0);
+        r1 = fma(d1, d1, r1);
+      }
+      double v0 = 0.0, v1 = 0.0;
+      if (i < n && kc <= i) v0 = kernel_value(r0, sf2, m.kernel) + (kc == i ? sn2 + jit : 0.0);
+      if (i < n && kc + 1 <= i) v1 = kernel_value(r1, sf2, m.kernel) + (kc + 1 == i ? sn2 + jit : 0.0);
+      *reinterpret_cast<double2 *>(W + tb(R, C) + 2 * lane) = make_double2(v0, v1);
+    }
+    __syncthreads();
+    FIT_T(1);
+    if (warp == kWarps - 1) diag_block(0);
+    __syncthreads();
+    FIT_T(2);
+    bool ok = piv[16] == 0.0;
+    for (int J = 0; J < n && ok; J += kFitB) {
+      const int Jb = min(J + kFitB, n), bb = Jb - J, JT = J >> 3;
+      // -- C: rows below the block (tile rows R > JT: [x N | x M]) and columns left of it (tile
+      // columns C < JT: R w), on DMMA
+      {
+        const int nrt = nt - JT - 1;
+        for (int it = warp; it < nrt + JT; it += kWarps) {
+          double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+          if (it < nrt) {
+            const int R = JT + 1 + it, i = 8 * R + gid;
+            double *Wt = W + tb(R, JT);
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+              const double a = Wt[8 * gid + kk + tig];
+              dmma(d0, d1, a, Nm[(kk + tig) * 8 + gid]);
+              dmma(e0, e1, a, Mm[(kk + tig) * 8 + gid]);
+            }
+            const int u = 2 * tig;
+            G[u * gs + i] = d0;
+            G[(u + 1) * gs + i] = d1;
+            if (i < n) {
+              Lg[(size_t)(J + u) * n + i] = d0;
+              Lg[(size_t)(J + u + 1) * n + i] = d1;
+            }
+            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
+          } else {
+            const int C = it - nrt;
+            double *Wt = W + tb(JT, C);
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+              const int mrow = kk + tig;
+              const double b = mrow < bb ? Wt[8 * mrow + gid] : 0.0;
+              dmma(d0, d1, Rm[gid * 8 + mrow], b);
+            }
+            const int kc = 8 * C + 2 * tig;
+            G[gid * gs + kc] = d0;
+            G[gid * gs + kc + 1] = d1;
+            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
+          }
         }
-        double v = kernel_value(r2, sf2, m.kernel);
-        if (i == j) v += sn2 + jit;
-        A[cb(j) + i] = v;
       }
-    }
-    // right-looking column Cholesky, in place, lower triangle
-    bool ok = true;
-    for (int c = 0; c < n; ++c) {
       __syncthreads();
-      double *Ac = A + cb(c);
-      const double p = Ac[c];
-      if (!(p > 0.0) || !isfinite(p)) { ok = false; break; }  // uniform across the CTA
-      const double lcc = sqrt(p);
-      const double rl = 1.0 / lcc;
-      for (int i = c + 1 + tid; i < n; i += kFitThreads) Ac[i] *= rl;
-      __syncthreads();
-      if (tid == 0) Ac[c] = lcc;
-      for (int j = c + 1 + warp; j < n; j += kWarps) {
-        const double ljc = Ac[j];
-        double *Aj = A + cb(j);
-        for (int i = j + lane; i < n; i += 32) Aj[i] -= Ac[i] * ljc;
+      FIT_T(3);
+      // -- T: W(i, k) -= sum_u G[u][i] G[u][k]: tile rows R > JT, tile columns C < JT and
+      // JT < C <= R; items of up to 4 consecutive tiles of one tile row share the A fragments
+      if (Jb < n) {
+        auto quad = [&](int R, int C0, int cnt) {
+          const int i = 8 * R + gid;
+          const double a0 = -G[tig * gs + i], a1 = -G[(4 + tig) * gs + i];
+          double *Wt = W + tb(R, C0) + 2 * lane;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < cnt) {
+              const int kq = 8 * (C0 + q) + gid;
+              double2 c = *reinterpret_cast<double2 *>(Wt + 64 * q);
+              dmma(c.x, c.y, a0, G[tig * gs + kq]);
+              dmma(c.x, c.y, a1, G[(4 + tig) * gs + kq]);
+              *reinterpret_cast<double2 *>(Wt + 64 * q) = c;
+            }
+          }
+        };
+        const int nrt = nt - JT - 1, nlq = (JT + 3) / 4;
+        if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D (the
+          // highest warp id: the schedulers favour it while the other warps run T)
+          quad(JT + 1, JT + 1, 1);
+          __syncwarp();
+#ifdef GPBO_FIT_TIMING
+          const long long td0 = clock64();
+#endif
+          diag_block(Jb);
+#ifdef GPBO_FIT_TIMING
+          if (blockIdx.x == 0 && lane == 0) fit_tD += clock64() - td0;
+#endif
+        } else {
+#ifdef GPBO_FIT_TIMING
+          const long long tw0 = clock64();
+#endif
+          // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
+          // (row 0's right quad is the diagonal tile -- warp 0's)
+          int r = 0, q = warp;
+          for (;;) {
+            while (r < nrt && q >= nlq + r / 4 + 1) { q -= nlq + r / 4 + 1; ++r; }
+            if (r >= nrt) break;
+            const int R = JT + 1 + r;
+            if (q < nlq) {
+              quad(R, 4 * q, min(4, JT - 4 * q));
+            } else {
+              const int c0 = 4 * (q - nlq), cnt = min(4, r + 1 - c0);
+              if (r > 0 || c0 > 0) quad(R, JT + 1 + c0, cnt);
+            }
+            q += kWarps - 1;
+          }
+#ifdef GPBO_FIT_TIMING
+          if (blockIdx.x == 0 && threadIdx.x == 0) fit_tw += clock64() - tw0;
+#endif
+        }
       }
+      __syncthreads();
+      FIT_T(4);
+      ok = piv[16] == 0.0;  // the next block's D (uniform)
     }
-    if (ok) { jk = k; break; }
+    if (ok) jk = k;
   }
   __syncthreads();
   if (jk < 0) {
@@ -179,84 +426,52 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     }
     return;
   }
-  // keep L (col-major, full) for diagnostics
-  for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
-    const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
-    L64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
-  }
-
-  // ---- H4: in-place inverse X = L^-1 by a forward sweep over the rows of L (O(n) steps of
-  // parallel rank-1 updates; critical path O(n)):  at step k, row k of X is final after
-  // X[k][c] /= L[k][k]; then X[i][c] -= L[i][k] X[k][c] for i > k, c <= k (X[i][k] starts at 0).
-  for (int k = 0; k < n; ++k) {
-    __syncthreads();
-    double *Ak = A + cb(k);
-    const double lkk = Ak[k];
-    for (int i = k + 1 + tid; i < n; i += kFitThreads) tmp[i] = Ak[i];  // column k of L
-    __syncthreads();
-    const double inv = 1.0 / lkk;
-    // row k: X[k][c] = X[k][c] / L[k][k] for c < k (stored at (k, c)), X[k][k] = 1 / L[k][k]
-    for (int c = tid; c <= k; c += kFitThreads) {
-      double *p = A + cb(c) + k;
-      *p = c == k ? inv : *p * inv;
-    }
-    __syncthreads();
-    // rows i > k: X[i][c] = X[i][c] - L[i][k] X[k][c]  (c < k), X[i][k] = -L[i][k] X[k][k]
-    for (int c = warp; c <= k; c += kWarps) {
-      double *Ac = A + cb(c);
-      const double xkc = Ac[k];
-      if (c == k)
-        for (int i = k + 1 + lane; i < n; i += 32) Ac[i] = -tmp[i] * xkc;
-      else
-        for (int i = k + 1 + lane; i < n; i += 32) Ac[i] -= tmp[i] * xkc;
-    }
-  }
-  __syncthreads();
-  // w = L^-1 y~
+  // ---- W now holds L^-1 (lower).  w = L^-1 y~, row abs sums and abs max (thread per row)
+  double rs = 0.0, lam = 0.0;
   for (int i = tid; i < n; i += kFitThreads) {
-    double a2 = 0.0;
-    for (int k = 0; k <= i; ++k) a2 += A[cb(k) + i] * yt[k];
+    double a2 = 0.0, a3 = 0.0;
+    const int R = i >> 3;
+    for (int C = 0; C <= R; ++C) {
+      const double *row = W + tb(R, C) + 8 * (i & 7);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int kk = 8 * C + q;
+        const double v = kk <= i ? row[q] : 0.0;
+        a2 = fma(v, yt[min(kk, n - 1)], a2);
+        a3 += fabs(v);
+        lam = fmax(lam, fabs(v));
+      }
+    }
     w[i] = a2;
+    rs = fmax(rs, a3);
   }
   __syncthreads();
   // alpha = L^-T w  (warp per k, lanes over i >= k)
   double l1 = 0.0, amx = 0.0;
-  for (int k = warp; k < m.n_pad; k += kWarps) {
+  for (int kk = warp; kk < m.n_pad; kk += kWarps) {
     double a2 = 0.0;
-    if (k < n)
-      for (int i = k + lane; i < n; i += 32) a2 += A[cb(k) + i] * w[i];
+    if (kk < n)
+      for (int i = kk + lane; i < n; i += 32) a2 += W[at(i, kk)] * w[i];
     a2 = warp_sum(a2);
-    if (lane == 0) { alpha64[m.a_off + k] = a2; l1 += fabs(a2); amx = fmax(amx, fabs(a2)); }
+    if (lane == 0) { alpha64[m.a_off + kk] = a2; l1 += fabs(a2); amx = fmax(amx, fabs(a2)); }
+  }
+  // L^-1, lower part, col-major (the refine phase and the tcgen05 image read only i >= j)
+  for (int j = warp; j < n; j += kWarps) {
+    double *Ic = Linv64 + m.mat_off + (size_t)j * n;
+    for (int i = j + lane; i < n; i += 32) Ic[i] = W[at(i, j)];
   }
   l1 = block_reduce(l1, red, AddOp(), 0.0);
   amx = block_reduce(amx, red, MaxOp(), 0.0);
-  double rs = 0.0, lam = 0.0;
-  for (int j = tid; j < n; j += kFitThreads) {
-    double a3 = 0.0;
-    for (int k = 0; k <= j; ++k) {
-      const double v = fabs(A[cb(k) + j]);
-      a3 += v;
-      lam = fmax(lam, v);
-    }
-    rs = fmax(rs, a3);
-  }
   rs = block_reduce(rs, red, MaxOp(), 0.0);
   lam = block_reduce(lam, red, MaxOp(), 0.0);
-  // write L^-1 (col-major) and the float32 (L^-1)^T scoring operand: LT[k][j] = Linv[j][k]
-  if (kSmem)
-    for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
-      const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
-      Linv64[m.mat_off + e] = (i >= j) ? A[cb(j) + i] : 0.0;
-    }
-  else
-    for (size_t e = tid; e < (size_t)n * n; e += kFitThreads) {
-      const int j = (int)(e / n), i = (int)(e - (size_t)j * n);
-      if (i < j) A[e] = 0.0;
-    }
-  for (size_t e = tid; e < (size_t)m.n_pad * m.n_pad; e += kFitThreads) {
-    const int k = (int)(e / m.n_pad), j = (int)(e - (size_t)k * m.n_pad);
-    LT32[m.lt_off + e] = (k < n && j < n && j >= k) ? (float)A[cb(k) + j] : 0.f;
-  }
+  FIT_T(5);
+#ifdef GPBO_FIT_TIMING
+  if (blockIdx.x == 0 && tid == 0)
+    printf("FIT_PHASES n=%d setup=%lld gram=%lld diag0=%lld panelC=%lld trailingT=%lld tail=%lld"
+           " [warp0 T tiles: %lld]\n", n, fit_t[0], fit_t[1], fit_t[2], fit_t[3], fit_t[4],
+           fit_t[5], fit_tw);
+  if (blockIdx.x == 0 && tid == kFitThreads - 32) printf("FIT_PHASES D in T: %lld\n", fit_tD);
+#endif
   if (tid == 0) {
     m.status = degenerate ? GPBO_WDEGENERATE : GPBO_OK;
     m.jitter_k = jk; m.jitter = jit;
@@ -270,29 +485,59 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
 __global__ void __launch_bounds__(kFitThreads, 1)
 fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
            const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
-           double *Linv64, float *Xs32, double *Xs64, float *LT32, double *alpha64,
+           double *Linv64, double *Xs64, double *alpha64, double *Wscr64,
            SearchMeta *__restrict__ meta_out) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
   if (meta_in[blockIdx.x].use_smem)
-    fit_body<true>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs32, Xs64, LT32, alpha64,
+    fit_body<true>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs64, alpha64, Wscr64,
                    meta_out);
   else
-    fit_body<false>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs32, Xs64, LT32, alpha64,
+    fit_body<false>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs64, alpha64, Wscr64,
                     meta_out);
+}
+
+// CUDA-core scoring operands, built on first use of that path (score_simt.cu): X / l in float32
+// (IEEE division of the float32 inputs), zero padded to n_pad x d_pad, and the float32
+// (L^-1)^T, LT[k][j] = Linv[j][k] for j >= k, n_pad x n_pad.
+__global__ void __launch_bounds__(256)
+simt_operands_kernel(const SearchMeta *__restrict__ meta, const float *__restrict__ X32,
+                     const float *__restrict__ ls32, const double *__restrict__ Linv64,
+                     float *Xs32, float *LT32) {
+  const SearchMeta m = meta[blockIdx.x];
+  if (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE) return;
+  const int n = m.n, d = m.d;
+  for (int e = threadIdx.x; e < m.n_pad * m.d_pad; e += blockDim.x) {
+    const int i = e / m.d_pad, c = e - i * m.d_pad;
+    Xs32[m.xs_off + e] = (i < n && c < d)
+                             ? __fdiv_rn(X32[m.x_off + i * d + c], ls32[m.ls_off + c]) : 0.f;
+  }
+  const double *Li = Linv64 + m.mat_off;
+  for (int k = threadIdx.x >> 5; k < m.n_pad; k += blockDim.x >> 5) {
+    float *row = LT32 + m.lt_off + (size_t)k * m.n_pad;
+    for (int j = threadIdx.x & 31; j < m.n_pad; j += 32)
+      row[j] = (k < n && j < n && j >= k) ? (float)Li[(size_t)k * n + j] : 0.f;
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
                        const float *ls32, const double *y64, double *L64, double *Linv64,
-                       float *Xs32, double *Xs64, float *LT32, double *alpha64,
-                       SearchMeta *meta_out, cudaStream_t stream) {
+                       double *Xs64, double *alpha64, double *Wscr64, SearchMeta *meta_out,
+                       cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_bytes);
   if (e != cudaSuccess) return e;
-  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, X32, ls32, y64, L64, Linv64, Xs32,
-                                                     Xs64, LT32, alpha64, meta_out);
+  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, X32, ls32, y64, L64, Linv64, Xs64,
+                                                     alpha64, Wscr64, meta_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
+                                 const float *ls32, const double *Linv64, float *Xs32,
+                                 float *LT32, cudaStream_t stream) {
+  simt_operands_kernel<<<S, 256, 0, stream>>>(meta_d, X32, ls32, Linv64, Xs32, LT32);
   return cudaGetLastError();
 }
 

@@ -10,9 +10,21 @@ namespace gpbo {
 
 constexpr int kFitThreads = 512;
 constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
-// Largest n whose packed lower-triangular float64 matrix (+3 n-vectors) the fit keeps in shared
-// memory: 232 * 233 / 2 * 8 B = 216 KB.
-constexpr int kFitSmemMaxN = 232;
+// Panel width of the fit's blocked factorisation (fit.cu) and its shared-memory plan:
+// y~, w (n-vectors), spare/flags, the block maps M, N, R, 8 panel rows G of stride gs, and -- for
+// n <= kFitSmemMaxN -- the working matrix as the lower triangle of 8 x 8 tiles, each row-major
+// (27 * 28 / 2 tiles * 512 B = 189 KB at n = 216).
+constexpr int kFitB = 8;
+constexpr int kFitSmemMaxN = 216;
+__host__ __device__ constexpr int fit_nr8(int n) { return (n + 7) & ~7; }
+// G row stride: = 8 (mod 16) doubles, so DMMA fragment loads of 4 rows hit distinct banks
+__host__ __device__ constexpr int fit_gstride(int n) { return ((n + 15) & ~15) + 8; }
+__host__ __device__ constexpr int fit_tile_doubles(int n) {
+  return ((n + 7) / 8) * ((n + 7) / 8 + 1) / 2 * 64;
+}
+__host__ __device__ constexpr int fit_smem_doubles(int n, bool in_smem) {
+  return 2 * fit_nr8(n) + 24 + 3 * 64 + 8 * fit_gstride(n) + (in_smem ? fit_tile_doubles(n) : 0);
+}
 
 // Per-search state of a fitted model (device copy in gpbo_model::meta_d, host copy in meta_h).
 struct SearchMeta {
@@ -48,8 +60,9 @@ struct SearchMeta {
   double jitter;
   int32_t jitter_k;
   int32_t status;       // gpbo_status of this search
-  int32_t use_smem;     // fit keeps its matrix in shared memory
+  int32_t use_smem;     // fit keeps its working matrix in shared memory
   int32_t pad_;
+  int64_t scr_off;      // else: its tile-packed working matrix (fit_tile_doubles) in model.Wscr64
 };
 
 // Candidate flagged by the fast phase for the float64 refine phase.
@@ -119,8 +132,11 @@ struct RefineLaunch {
 namespace gpbo {
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
                        const float *ls32, const double *y64, double *L64, double *Linv64,
-                       float *Xs32, double *Xs64, float *LT32, double *alpha64,
-                       SearchMeta *meta_out, cudaStream_t stream);
+                       double *Xs64, double *alpha64, double *Wscr64, SearchMeta *meta_out,
+                       cudaStream_t stream);
+cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
+                                 const float *ls32, const double *Linv64, float *Xs32,
+                                 float *LT32, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, int nmax,
                               cudaStream_t stream);
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,

@@ -32,8 +32,9 @@ IMPLS = [0, 1]  # auto (tcgen05 where supported), CUDA-core
 
 
 # ------------------------------------------------------------------ fit (H1-H4)
-@pytest.mark.parametrize("n,d", [(1, 1), (2, 3), (16, 2), (17, 5), (33, 8), (100, 5), (160, 20),
-                                 (161, 9), (200, 20), (255, 35), (500, 60)])
+@pytest.mark.parametrize("n,d", [(1, 1), (2, 3), (8, 2), (9, 3), (16, 2), (17, 5), (33, 8), (64, 4),
+                                 (100, 5), (160, 20), (161, 9), (200, 20), (224, 12), (225, 7),
+                                 (255, 35), (500, 60)])
 @pytest.mark.parametrize("kernel", [gp.MATERN52, gp.RBF])
 def test_fit_matches_oracle(G, n, d, kernel):
     w = gen.random_case(n * 7 + d, n, d, 4, kernel=kernel)
