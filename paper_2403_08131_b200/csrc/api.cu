@@ -32,6 +32,8 @@ struct gpbo_ctx {
   size_t stage_cap = 0;
   void *aux_d = nullptr;    // per-call small arrays (offsets, bases, best, tile prefix)
   void *aux_h = nullptr;    // pinned mirror
+  void *meta_h = nullptr;   // pinned staging of the fit's meta records
+  size_t meta_cap = 0;
   size_t aux_cap = 0;
   int64_t launches = 0;
   // optional per-kernel CUDA-event timing (gpbo_set_profiling): kinds fit / fast / refine / pack
@@ -154,6 +156,17 @@ gpbo_status ensure_aux(gpbo_ctx *ctx, size_t bytes) {
   CK(cudaMalloc(&ctx->aux_d, cap));
   CK(cudaMallocHost(&ctx->aux_h, cap));
   ctx->aux_cap = cap;
+  return GPBO_OK;
+}
+
+gpbo_status ensure_meta_h(gpbo_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->meta_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->meta_h) CK(cudaFreeHost(ctx->meta_h));
+  ctx->meta_h = nullptr;
+  const size_t cap = std::max<size_t>(bytes, 1 << 14);
+  CK(cudaMallocHost(&ctx->meta_h, cap));
+  ctx->meta_cap = cap;
   return GPBO_OK;
 }
 
@@ -414,6 +427,7 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->stage_d) cudaFree(ctx->stage_d);
   if (ctx->aux_d) cudaFree(ctx->aux_d);
   if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
+  if (ctx->meta_h) cudaFreeHost(ctx->meta_h);
   if (ctx->keys_d) cudaFree(ctx->keys_d);
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
   if (ctx->list_d) cudaFree(ctx->list_d);
@@ -513,25 +527,16 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     gpbo::tc_fill_geometry(q);
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
-    const int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
+    int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
+    q.xs_smem = smem + n * d * 8 <= gpbo::kFitSmemBudget;
+    if (q.xs_smem) smem += n * d * 8;
     smem_max = std::max(smem_max, smem);
     m->nmax = std::max(m->nmax, n);
     m->dmax = std::max(m->dmax, q.d_pad);
   }
-  // hyper-parameters into the meta records (read from host, or from device if mem == DEVICE)
-  std::vector<float> sf2(S), sn2(S);
-  if (a->mem == GPBO_HOST) {
-    std::memcpy(sf2.data(), a->signal_var, S * 4);
-    std::memcpy(sn2.data(), a->noise_var, S * 4);
-  } else {
-    cudaError_t e1 = cudaMemcpy(sf2.data(), a->signal_var, S * 4, cudaMemcpyDeviceToHost);
-    cudaError_t e2 = cudaMemcpy(sn2.data(), a->noise_var, S * 4, cudaMemcpyDeviceToHost);
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
-      delete m;
-      return fail(ctx, GPBO_EINVAL, "signal_var/noise_var are not device pointers");
-    }
-  }
-  for (int s = 0; s < S; ++s) { m->meta[s].sf2 = sf2[s]; m->meta[s].sn2 = sn2[s]; }
+  // hyper-parameters: host arrays go into the meta records; device arrays are read by the kernel
+  if (a->mem == GPBO_HOST)
+    for (int s = 0; s < S; ++s) { m->meta[s].sf2 = a->signal_var[s]; m->meta[s].sn2 = a->noise_var[s]; }
   // one device block: meta | X | ls | Xs | LT | y | L | Linv | alpha | img
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += round_up((int64_t)bytes, 256); return o; };
@@ -569,15 +574,27 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     if (e_ != cudaSuccess)                                                              \
       return cleanup_fail(GPBO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-  CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
-  CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));
-  CKM(cudaMemcpyAsync(m->y64, a->y, ny * 8, kind, ctx->stream));
-  CKM(cudaMemcpyAsync(meta_in, m->meta.data(), sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
+  gpbo::FitIO io{};
+  io.X32 = m->X32; io.ls32 = m->ls32; io.y64 = m->y64;
+  io.L64 = m->L64; io.Linv64 = m->Linv64; io.Xs64 = m->Xs64; io.alpha64 = m->alpha64;
+  io.Wscr64 = Wscr64;
+  if (a->mem == GPBO_HOST) {  // stage into the model's arrays
+    CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
+    CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));
+    CKM(cudaMemcpyAsync(m->y64, a->y, ny * 8, kind, ctx->stream));
+    io.X_src = m->X32; io.ls_src = m->ls32; io.y_src = m->y64;
+  } else {  // the kernel reads the caller's arrays and copies them
+    io.X_src = a->X; io.ls_src = a->lengthscale; io.y_src = a->y;
+    io.sf2_src = a->signal_var; io.sn2_src = a->noise_var;
+  }
+  gpbo_status pst = ensure_meta_h(ctx, sizeof(SearchMeta) * S);
+  if (pst) { gp_model_free(m); return pst; }
+  std::memcpy(ctx->meta_h, m->meta.data(), sizeof(SearchMeta) * S);
+  CKM(cudaMemcpyAsync(meta_in, ctx->meta_h, sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
                       ctx->stream));
   {
     KernTimer t(ctx, kKernFit);
-    CKM(gpbo::launch_fit(meta_in, S, smem_max, m->X32, m->ls32, m->y64, m->L64, m->Linv64,
-                         m->Xs64, m->alpha64, Wscr64, m->meta_d, ctx->stream));
+    CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream));
   }
   ctx->launches += 1;
   if (nimg > 0) {
@@ -586,9 +603,10 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
                              ctx->stream));
     ctx->launches += 1;
   }
-  CKM(cudaMemcpyAsync(m->meta.data(), m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
+  CKM(cudaMemcpyAsync(ctx->meta_h, m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
                       ctx->stream));
   CKM(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(m->meta.data(), ctx->meta_h, sizeof(SearchMeta) * S);
   harvest_events(ctx);
 #undef CKM
   gpbo_status worst = GPBO_OK;

@@ -117,16 +117,15 @@ __device__ __forceinline__ void tile_rc(int e, int &R, int &C) {
 // to W compiles to LDS/STS or LDG/STG instead of generic loads.
 template <bool kSmem>
 __device__ __forceinline__ void fit_body(double *sm, double *red,
-                                         const SearchMeta *__restrict__ meta_in,
-                                         const float *__restrict__ X32,
-                                         const float *__restrict__ ls32,
-                                         const double *__restrict__ y64, double *L64,
-                                         double *Linv64, double *Xs64, double *alpha64,
-                                         double *Wscr64, SearchMeta *__restrict__ meta_out) {
+                                         const SearchMeta *__restrict__ meta_in, const FitIO &io,
+                                         SearchMeta *__restrict__ meta_out) {
+  double *L64 = io.L64, *Linv64 = io.Linv64, *Xs64 = io.Xs64, *alpha64 = io.alpha64;
+  double *Wscr64 = io.Wscr64;
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;  // DMMA fragment coordinates
   SearchMeta m = meta_in[s];
+  if (io.sf2_src) { m.sf2 = io.sf2_src[s]; m.sn2 = io.sn2_src[s]; }
   const int n = m.n, d = m.d;
 #ifdef GPBO_FIT_TIMING
   long long fit_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -145,15 +144,26 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   // element (i, k), i >= k
   auto at = [&](int i, int k) -> int { return tb(i >> 3, k >> 3) + 8 * (i & 7) + (k & 7); };
   double *Lg = L64 + m.mat_off;        // L, col-major (lower part; export zeroes the rest)
-  const float *X = X32 + m.x_off;
-  const float *ls = ls32 + m.ls_off;
-  const double *y = y64 + m.y_off;
+  const float *X = io.X_src + m.x_off;
+  const float *ls = io.ls_src + m.ls_off;
+  const double *y = io.y_src + m.y_off;
 
-  // ---- input validation (GPBO_EINVAL on any non-finite / out-of-domain value)
+  // ---- input validation (GPBO_EINVAL on any non-finite / out-of-domain value), copying the
+  // inputs into the model when they come from the caller's device arrays
+  const bool copy = io.X_src != io.X32;
   int bad = 0;
-  for (int i = tid; i < n * d; i += kFitThreads) bad |= !isfinite(X[i]);
-  for (int i = tid; i < n; i += kFitThreads) bad |= !isfinite(y[i]);
-  for (int i = tid; i < d; i += kFitThreads) bad |= !(ls[i] > 0.f) || !isfinite(ls[i]);
+  for (int i = tid; i < n * d; i += kFitThreads) {
+    bad |= !isfinite(X[i]);
+    if (copy) io.X32[m.x_off + i] = X[i];
+  }
+  for (int i = tid; i < n; i += kFitThreads) {
+    bad |= !isfinite(y[i]);
+    if (copy) io.y64[m.y_off + i] = y[i];
+  }
+  for (int i = tid; i < d; i += kFitThreads) {
+    bad |= !(ls[i] > 0.f) || !isfinite(ls[i]);
+    if (copy) io.ls32[m.ls_off + i] = ls[i];
+  }
   bad |= !(m.sf2 > 0.f) || !isfinite(m.sf2) || !(m.sn2 >= 0.f) || !isfinite(m.sn2);
   bad = __syncthreads_or(bad);
   if (bad) {
@@ -181,12 +191,14 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
 
   // ---- x / l in float64, column-major (d x n), for the Gram, the refine phase and the
   // tcgen05 image; pmax = max_j |x_j / l|^2
+  double *xsm = sm + fit_smem_doubles(n, kSmem);  // x / l in shared memory when m.xs_smem
   double pm = 0.0;
   for (int i = tid; i < n; i += kFitThreads) {
     double q = 0.0;
     for (int c = 0; c < d; ++c) {
       const double v = (double)X[i * d + c] / (double)ls[c];
       Xs64[m.x_off + (size_t)c * n + i] = v;
+      if (m.xs_smem) xsm[c * n + i] = v;
       q += v * v;
     }
     pm = fmax(pm, q);
@@ -290,24 +302,29 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     // H2: one 8 x 8 tile per warp item, two entries per lane (its accumulator-fragment slots):
     // squared distances of x / l by direct differences (reading R1), the kernel, + sn2 + jitter
     // on the diagonal; entries outside the matrix are stored as 0
-    for (int e = warp; e < ntiles; e += kWarps) {
-      int R, C;
-      tile_rc(e, R, C);
-      const int i = 8 * R + gid, kc = 8 * C + 2 * tig;
-      const int ia = min(i, n - 1), k0 = min(kc, n - 1), k1 = min(kc + 1, n - 1);
-      double r0 = 0.0, r1 = 0.0;
-      for (int c = 0; c < d; ++c) {
-        const double *col = xc + (size_t)c * n;
-        const double xi = __ldg(col + ia);
-        const double d0 = xi - __ldg(col + k0), d1 = xi - __ldg(col + k1);
-        r0 = fma(d0, d0, r0);
-        r1 = fma(d1, d1, r1);
+    auto gram = [&](const double *xs) {
+      for (int e = warp; e < ntiles; e += kWarps) {
+        int R, C;
+        tile_rc(e, R, C);
+        const int i = 8 * R + gid, kc = 8 * C + 2 * tig;
+        const int ia = min(i, n - 1), k0 = min(kc, n - 1), k1 = min(kc + 1, n - 1);
+        double r0 = 0.0, r1 = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < d; ++c) {
+          const double *col = xs + c * n;
+          const double xi = col[ia];
+          const double d0 = xi - col[k0], d1 = xi - col[k1];
+          r0 = fma(d0, d0, r0);
+          r1 = fma(d1, d1, r1);
+        }
+        double v0 = 0.0, v1 = 0.0;
+        if (i < n && kc <= i) v0 = kernel_value(r0, sf2, m.kernel) + (kc == i ? sn2 + jit : 0.0);
+        if (i < n && kc + 1 <= i)
+          v1 = kernel_value(r1, sf2, m.kernel) + (kc + 1 == i ? sn2 + jit : 0.0);
+        *reinterpret_cast<double2 *>(W + tb(R, C) + 2 * lane) = make_double2(v0, v1);
       }
-      double v0 = 0.0, v1 = 0.0;
-      if (i < n && kc <= i) v0 = kernel_value(r0, sf2, m.kernel) + (kc == i ? sn2 + jit : 0.0);
-      if (i < n && kc + 1 <= i) v1 = kernel_value(r1, sf2, m.kernel) + (kc + 1 == i ? sn2 + jit : 0.0);
-      *reinterpret_cast<double2 *>(W + tb(R, C) + 2 * lane) = make_double2(v0, v1);
-    }
+    };
+    if (m.xs_smem) gram(xsm); else gram(xc);
     __syncthreads();
     FIT_T(1);
     if (warp == kWarps - 1) diag_block(0);
@@ -364,16 +381,27 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
           const int i = 8 * R + gid;
           const double a0 = -G[tig * gs + i], a1 = -G[(4 + tig) * gs + i];
           double *Wt = W + tb(R, C0) + 2 * lane;
+          const double *g0 = G + tig * gs + 8 * C0 + gid, *g1 = g0 + 4 * gs;
+          // all operands first (the stores below would otherwise fence the next tile's loads)
+          double2 c[4];
+          double b0[4], b1[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (q < cnt) {
-              const int kq = 8 * (C0 + q) + gid;
-              double2 c = *reinterpret_cast<double2 *>(Wt + 64 * q);
-              dmma(c.x, c.y, a0, G[tig * gs + kq]);
-              dmma(c.x, c.y, a1, G[(4 + tig) * gs + kq]);
-              *reinterpret_cast<double2 *>(Wt + 64 * q) = c;
+              c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
+              b0[q] = g0[8 * q];
+              b1[q] = g1[8 * q];
             }
           }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) dmma(c[q].x, c[q].y, a0, b0[q]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) dmma(c[q].x, c[q].y, a1, b1[q]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
         };
         const int nrt = nt - JT - 1, nlq = (JT + 3) / 4;
         if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D (the
@@ -392,19 +420,19 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
           const long long tw0 = clock64();
 #endif
           // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
-          // (row 0's right quad is the diagonal tile -- warp 0's)
-          int r = 0, q = warp;
-          for (;;) {
-            while (r < nrt && q >= nlq + r / 4 + 1) { q -= nlq + r / 4 + 1; ++r; }
-            if (r >= nrt) break;
-            const int R = JT + 1 + r;
-            if (q < nlq) {
-              quad(R, 4 * q, min(4, JT - 4 * q));
-            } else {
-              const int c0 = 4 * (q - nlq), cnt = min(4, r + 1 - c0);
-              if (r > 0 || c0 > 0) quad(R, JT + 1 + c0, cnt);
+          // (row 0's right quad is the diagonal tile -- the D warp's).  Row r's items go to the
+          // kWarps - 1 T warps round robin, starting at warp (5 r) mod (kWarps - 1).
+          constexpr int kT = kWarps - 1;
+          for (int r = 0, w0 = 0; r < nrt; ++r, w0 = (w0 + 5) % kT) {
+            const int R = JT + 1 + r, len = nlq + (r >> 2) + (r > 0 ? 1 : 0);
+            for (int q = (warp - w0 + kT) % kT; q < len; q += kT) {
+              if (q < nlq) {
+                quad(R, 4 * q, min(4, JT - 4 * q));
+              } else {
+                const int c0 = 4 * (q - nlq);
+                quad(R, JT + 1 + c0, min(4, r + 1 - c0));
+              }
             }
-            q += kWarps - 1;
           }
 #ifdef GPBO_FIT_TIMING
           if (blockIdx.x == 0 && threadIdx.x == 0) fit_tw += clock64() - tw0;
@@ -446,24 +474,66 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     rs = fmax(rs, a3);
   }
   __syncthreads();
-  // alpha = L^-T w  (warp per k, lanes over i >= k)
+  // alpha = L^-T w (thread per column k, down its tile column; two partial sums)
   double l1 = 0.0, amx = 0.0;
-  for (int kk = warp; kk < m.n_pad; kk += kWarps) {
-    double a2 = 0.0;
-    if (kk < n)
-      for (int i = kk + lane; i < n; i += 32) a2 += W[at(i, kk)] * w[i];
-    a2 = warp_sum(a2);
-    if (lane == 0) { alpha64[m.a_off + kk] = a2; l1 += fabs(a2); amx = fmax(amx, fabs(a2)); }
+  for (int kk = tid; kk < m.n_pad; kk += kFitThreads) {
+    double a2 = 0.0, a3 = 0.0;
+    if (kk < n) {
+      const int C = kk >> 3, c = kk & 7;
+      for (int R = C; R < nt; ++R) {
+        const double *col = W + tb(R, C) + c;
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          const int i = 8 * R + r;
+          if (i >= kk && i < n) a2 = fma(col[8 * r], w[i], a2);
+          if (i + 1 >= kk && i + 1 < n) a3 = fma(col[8 * r + 8], w[i + 1], a3);
+        }
+      }
+    }
+    a2 += a3;
+    alpha64[m.a_off + kk] = a2;
+    l1 += fabs(a2);
+    amx = fmax(amx, fabs(a2));
   }
-  // L^-1, lower part, col-major (the refine phase and the tcgen05 image read only i >= j)
-  for (int j = warp; j < n; j += kWarps) {
-    double *Ic = Linv64 + m.mat_off + (size_t)j * n;
-    for (int i = j + lane; i < n; i += 32) Ic[i] = W[at(i, j)];
+  // L^-1, lower part, col-major (the refine phase and the tcgen05 image read only i >= j):
+  // warp per tile, lane -> column c = lane / 4, rows 2 (lane % 4) + {0, 1}
+  for (int e = warp; e < ntiles; e += kWarps) {
+    int R, C;
+    tile_rc(e, R, C);
+    const int c = lane >> 2, r0 = 2 * (lane & 3), j = 8 * C + c;
+    const double *src = W + tb(R, C) + 8 * r0 + c;
+    double *dst = Linv64 + m.mat_off + (size_t)j * n + 8 * R + r0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 8 * R + r0 + h;
+      if (i < n && j <= i) dst[h] = src[8 * h];
+    }
   }
-  l1 = block_reduce(l1, red, AddOp(), 0.0);
-  amx = block_reduce(amx, red, MaxOp(), 0.0);
-  rs = block_reduce(rs, red, MaxOp(), 0.0);
-  lam = block_reduce(lam, red, MaxOp(), 0.0);
+  // the four statistics in one block reduction
+  {
+    double v[4] = {l1, amx, rs, lam};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, v[q], o);
+        v[q] = q == 0 ? v[q] + t : fmax(v[q], t);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[4 * warp + q] = v[q];
+    __syncthreads();
+    if (tid < 4) {
+      double t = red[tid];
+      for (int w2 = 1; w2 < kWarps; ++w2) t = tid == 0 ? t + red[4 * w2] : fmax(t, red[4 * w2 + tid]);
+      red[4 * kWarps + tid] = t;
+    }
+    __syncthreads();
+    l1 = red[4 * kWarps];
+    amx = red[4 * kWarps + 1];
+    rs = red[4 * kWarps + 2];
+    lam = red[4 * kWarps + 3];
+  }
   FIT_T(5);
 #ifdef GPBO_FIT_TIMING
   if (blockIdx.x == 0 && tid == 0)
@@ -483,18 +553,14 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
 }
 
 __global__ void __launch_bounds__(kFitThreads, 1)
-fit_kernel(const SearchMeta *__restrict__ meta_in, const float *__restrict__ X32,
-           const float *__restrict__ ls32, const double *__restrict__ y64, double *L64,
-           double *Linv64, double *Xs64, double *alpha64, double *Wscr64,
+fit_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
            SearchMeta *__restrict__ meta_out) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[33];
+  __shared__ double red[4 * kWarps + 4];
   if (meta_in[blockIdx.x].use_smem)
-    fit_body<true>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs64, alpha64, Wscr64,
-                   meta_out);
+    fit_body<true>(sm, red, meta_in, io, meta_out);
   else
-    fit_body<false>(sm, red, meta_in, X32, ls32, y64, L64, Linv64, Xs64, alpha64, Wscr64,
-                    meta_out);
+    fit_body<false>(sm, red, meta_in, io, meta_out);
 }
 
 // CUDA-core scoring operands, built on first use of that path (score_simt.cu): X / l in float32
@@ -522,15 +588,16 @@ simt_operands_kernel(const SearchMeta *__restrict__ meta, const float *__restric
 
 }  // namespace
 
-cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
-                       const float *ls32, const double *y64, double *L64, double *Linv64,
-                       double *Xs64, double *alpha64, double *Wscr64, SearchMeta *meta_out,
-                       cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes);
-  if (e != cudaSuccess) return e;
-  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, X32, ls32, y64, L64, Linv64, Xs64,
-                                                     alpha64, Wscr64, meta_out);
+cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
+                       SearchMeta *meta_out, cudaStream_t stream) {
+  static int smem_set = -1;  // the attribute call costs microseconds: only when it grows
+  if (smem_bytes > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(fit_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (e != cudaSuccess) return e;
+    smem_set = smem_bytes;
+  }
+  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, io, meta_out);
   return cudaGetLastError();
 }
 

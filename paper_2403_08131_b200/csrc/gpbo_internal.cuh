@@ -8,7 +8,7 @@
 
 namespace gpbo {
 
-constexpr int kFitThreads = 512;
+constexpr int kFitThreads = 384;
 constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
 // Panel width of the fit's blocked factorisation (fit.cu) and its shared-memory plan:
 // y~, w (n-vectors), spare/flags, the block maps M, N, R, 8 panel rows G of stride gs, and -- for
@@ -16,6 +16,7 @@ constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring ke
 // (27 * 28 / 2 tiles * 512 B = 189 KB at n = 216).
 constexpr int kFitB = 8;
 constexpr int kFitSmemMaxN = 216;
+constexpr int kFitSmemBudget = 227 * 1024 - 512;  // dynamic shared memory of the fit kernel
 __host__ __device__ constexpr int fit_nr8(int n) { return (n + 7) & ~7; }
 // G row stride: = 8 (mod 16) doubles, so DMMA fragment loads of 4 rows hit distinct banks
 __host__ __device__ constexpr int fit_gstride(int n) { return ((n + 15) & ~15) + 8; }
@@ -61,7 +62,7 @@ struct SearchMeta {
   int32_t jitter_k;
   int32_t status;       // gpbo_status of this search
   int32_t use_smem;     // fit keeps its working matrix in shared memory
-  int32_t pad_;
+  int32_t xs_smem;      // fit stages x / l (n x d float64) in shared memory for the Gram
   int64_t scr_off;      // else: its tile-packed working matrix (fit_tile_doubles) in model.Wscr64
 };
 
@@ -130,10 +131,16 @@ struct RefineLaunch {
 
 // Kernel launchers (defined in the .cu files).
 namespace gpbo {
-cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const float *X32,
-                       const float *ls32, const double *y64, double *L64, double *Linv64,
-                       double *Xs64, double *alpha64, double *Wscr64, SearchMeta *meta_out,
-                       cudaStream_t stream);
+// Fit kernel inputs (the caller's arrays, host-staged or device) and the model arrays it fills.
+struct FitIO {
+  const float *X_src, *ls_src;   // [sum n_s d_s], [sum d_s]
+  const double *y_src;           // [sum n_s]
+  const float *sf2_src, *sn2_src;  // [S] (device); null: taken from the meta records
+  float *X32, *ls32;             // model copies (skipped when equal to the sources)
+  double *y64, *L64, *Linv64, *Xs64, *alpha64, *Wscr64;
+};
+cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
+                       SearchMeta *meta_out, cudaStream_t stream);
 cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
                                  const float *ls32, const double *Linv64, float *Xs32,
                                  float *LT32, cudaStream_t stream);
