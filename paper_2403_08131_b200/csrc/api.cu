@@ -654,8 +654,9 @@ gpbo_status gp_model_export(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, d
     CK(cudaMemcpyAsync(buf.data(), srcs[w] + q.mat_off, buf.size() * 8, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    for (int j = 0; j < n; ++j)  // col-major device (lower part) -> row-major caller
-      for (int i = 0; i < n; ++i) outs[w][(size_t)i * n + j] = i >= j ? buf[(size_t)j * n + i] : 0.0;
+    for (int j = 0; j < n; ++j)  // device lower part (L col-major, L^-1 row-major) -> row-major
+      for (int i = 0; i < n; ++i)
+        outs[w][(size_t)i * n + j] = i < j ? 0.0 : w == 0 ? buf[(size_t)j * n + i] : buf[(size_t)i * n + j];
   }
   if (alpha) {
     CK(cudaMemcpyAsync(alpha, model->alpha64 + q.a_off, n * 8, cudaMemcpyDeviceToHost,

@@ -495,18 +495,18 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     l1 += fabs(a2);
     amx = fmax(amx, fabs(a2));
   }
-  // L^-1, lower part, col-major (the refine phase and the tcgen05 image read only i >= j):
-  // warp per tile, lane -> column c = lane / 4, rows 2 (lane % 4) + {0, 1}
+  // L^-1, lower part, ROW-major (element (i, k) at i n + k; the refine phase, the tcgen05 image
+  // and the CUDA-core operands read only k <= i): warp per tile, lane -> row r = lane / 4,
+  // columns 2 (lane % 4) + {0, 1}
   for (int e = warp; e < ntiles; e += kWarps) {
     int R, C;
     tile_rc(e, R, C);
-    const int c = lane >> 2, r0 = 2 * (lane & 3), j = 8 * C + c;
-    const double *src = W + tb(R, C) + 8 * r0 + c;
-    double *dst = Linv64 + m.mat_off + (size_t)j * n + 8 * R + r0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = 8 * R + r0 + h;
-      if (i < n && j <= i) dst[h] = src[8 * h];
+    const int i = 8 * R + gid, c0 = 8 * C + 2 * tig;
+    if (i < n) {
+      const double2 v = *reinterpret_cast<const double2 *>(W + tb(R, C) + 2 * lane);
+      double *dst = Linv64 + m.mat_off + (size_t)i * n + c0;
+      if (c0 <= i) dst[0] = v.x;
+      if (c0 + 1 <= i) dst[1] = v.y;
     }
   }
   // the four statistics in one block reduction
@@ -582,7 +582,7 @@ simt_operands_kernel(const SearchMeta *__restrict__ meta, const float *__restric
   for (int k = threadIdx.x >> 5; k < m.n_pad; k += blockDim.x >> 5) {
     float *row = LT32 + m.lt_off + (size_t)k * m.n_pad;
     for (int j = threadIdx.x & 31; j < m.n_pad; j += 32)
-      row[j] = (k < n && j < n && j >= k) ? (float)Li[(size_t)k * n + j] : 0.f;
+      row[j] = (k < n && j < n && j >= k) ? (float)Li[(size_t)j * n + k] : 0.f;
   }
 }
 

@@ -36,7 +36,7 @@ struct SearchMeta {
   int64_t x_off;        // raw X  (float32, n x d)            into model.X32
   int64_t ls_off;       // lengthscales (float32, d)          into model.ls32
   int64_t y_off;        // y (float64, n)                     into model.y64
-  int64_t mat_off;      // n x n float64 col-major            into model.L64 / model.Linv64
+  int64_t mat_off;      // n x n float64: L col-major, L^-1 row-major  into model.L64 / .Linv64
   int64_t xs_off;       // X/l (float32, n_pad x d_pad)       into model.Xs32
   int64_t lt_off;       // (L^-1)^T float32 n_pad x n_pad      into model.LT32
   int64_t a_off;        // alpha (n_pad)                      into model.alpha64
@@ -116,7 +116,7 @@ struct RefineLaunch {
   const double *Xs64;          // X / l in float64, n x d per search (indexed by x_off)
   const float *ls32;
   const double *alpha64;
-  const double *Linv64;        // L^-1, n x n column-major per search (mat_off)
+  const double *Linv64;        // L^-1, n x n row-major per search (mat_off), lower part
   unsigned long long *keys;
   const unsigned int *thr;
   const RefineEntry *list;     // argmax mode: entries; posterior mode: NULL (dense rows)

@@ -92,22 +92,28 @@ refine_kernel(const RefineLaunch p) {
       mu += k * alpha[j];
     }
     mu = block_sum2(mu, red);  // includes the barrier that publishes ksh
-    // v = L^-1 k*: thread owns rows j; Linv64 is column-major (column k contiguous over j)
+    // v = L^-1 k*: warp per row j (Linv64 is row-major: lanes read consecutive k), two rows at a
+    // time for more loads in flight
     const double *Li = p.Linv64 + m.mat_off;
+    const int lane = tid & 31, wp = tid >> 5;
+    constexpr int kW = kRefineThreads / 32;
     double vv = 0.0;
-    for (int j = tid; j < n; j += kRefineThreads) {
-      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-      int k = 0;
-      for (; k + 3 <= j; k += 4) {
-        v0 = fma(Li[(size_t)k * n + j], ksh[k], v0);
-        v1 = fma(Li[(size_t)(k + 1) * n + j], ksh[k + 1], v1);
-        v2 = fma(Li[(size_t)(k + 2) * n + j], ksh[k + 2], v2);
-        v3 = fma(Li[(size_t)(k + 3) * n + j], ksh[k + 3], v3);
+    for (int j = wp; j < n; j += 2 * kW) {
+      const int j2 = j + kW;
+      const double *r1 = Li + (size_t)j * n, *r2 = Li + (size_t)min(j2, n - 1) * n;
+      double a = 0.0, b = 0.0;
+      for (int k = lane; k <= j; k += 32) a = fma(r1[k], ksh[k], a);
+      if (j2 < n)
+        for (int k = lane; k <= j2; k += 32) b = fma(r2[k], ksh[k], b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
       }
-      for (; k <= j; ++k) v0 = fma(Li[(size_t)k * n + j], ksh[k], v0);
-      const double v = (v0 + v1) + (v2 + v3);
-      vv = fma(v, v, vv);
+      vv = fma(a, a, vv);
+      if (j2 < n) vv = fma(b, b, vv);
     }
+    if (lane != 0) vv = 0.0;
     vv = block_sum2(vv, red);
     if (tid == 0) {
       const double var64 = fmax((double)m.sf2 - vv, 0.0);

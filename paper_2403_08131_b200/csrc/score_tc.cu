@@ -413,7 +413,37 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         const uint32_t va = tl_addr;
         int c = half * hc;
         const int ce = c + hc;
-        for (; c + 16 <= ce; c += 16) {  // (x32 batching spills at the 168-register cap)
+        // two x16 loads in flight per wait (x32+ batching spills at the 168-register cap)
+        for (; c + 64 <= ce; c += 64) {
+          uint32_t r0[16], r1[16], r2[16], r3[16];
+          tc::tmem_ld16(va + (uint32_t)c, r0);
+          tc::tmem_ld16(va + (uint32_t)(c + 16), r1);
+          tc::tmem_ld16(va + (uint32_t)(c + 32), r2);
+          tc::tmem_ld16(va + (uint32_t)(c + 48), r3);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float v0 = __uint_as_float(r0[q]), v1 = __uint_as_float(r1[q]);
+            const float v2 = __uint_as_float(r2[q]), v3 = __uint_as_float(r3[q]);
+            vv = fmaf(v0, v0, vv);
+            vv = fmaf(v1, v1, vv);
+            vv = fmaf(v2, v2, vv);
+            vv = fmaf(v3, v3, vv);
+          }
+        }
+        for (; c + 32 <= ce; c += 32) {
+          uint32_t r0[16], r1[16];
+          tc::tmem_ld16(va + (uint32_t)c, r0);
+          tc::tmem_ld16(va + (uint32_t)(c + 16), r1);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float v0 = __uint_as_float(r0[q]), v1 = __uint_as_float(r1[q]);
+            vv = fmaf(v0, v0, vv);
+            vv = fmaf(v1, v1, vv);
+          }
+        }
+        if (c + 16 <= ce) {
           uint32_t r16[16];
           tc::tmem_ld16(va + (uint32_t)c, r16);
           tc::tmem_wait_ld();
@@ -422,6 +452,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             const float v = __uint_as_float(r16[q]);
             vv = fmaf(v, v, vv);
           }
+          c += 16;
         }
         if (c < ce) {
           uint32_t r8[8];
@@ -660,7 +691,7 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
     for (int idx = t0; idx < R * 32; idx += tstep) {
       const int r = idx >> 5, k = idx & 31;
       const int j = 32 * pp + r, kk = 32 * pp + k;
-      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)kk * n + j], uL) : 0.0;
+      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
       put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
     }
   }
