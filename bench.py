@@ -207,13 +207,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step_device():
-        m = ctx.fit(n, d, Xd, yd, lsd, sf2d, sn2d, kernel=w.kernel)
+        m = ctx.fit(n, d, Xd, yd, lsd, sf2d, sn2d, kernel=w.kernel, wait=False)
         idx, ei = ctx.score_argmax(m, Xsd, m_off, base)
         m.free()
         return idx, ei
 
     def step_host():
-        m = ctx.fit(n, d, Xh, yh, lsh, sf2h, sn2h, kernel=w.kernel)
+        m = ctx.fit(n, d, Xh, yh, lsh, sf2h, sn2h, kernel=w.kernel, wait=False)
         idx, ei = ctx.score_argmax(m, Xs_pin, m_off, base)
         m.free()
         return idx, ei

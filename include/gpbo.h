@@ -112,6 +112,17 @@ typedef struct {
 
 gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *args, gpbo_model **out,
                    int32_t *status, int32_t *jitter_k);
+
+/* Asynchronous gp_fit: enqueues the fit on ctx's stream and returns without waiting (GPBO_OK,
+ * or GPBO_EINVAL / GPBO_ENOMEM for argument errors detectable on the host).  The per-search
+ * statuses stay on the device: scoring calls skip a failed search there (it returns idx -1), and
+ * the host copy is refreshed by the next synchronising call (ei_score_argmax, bo_suggest_batch,
+ * gp_posterior, gp_model_stats/export) or explicitly by gp_model_sync, which writes status[S] /
+ * jitter_k[S] (may be NULL) and returns what gp_fit would have returned (GPBO_EINVAL if an input
+ * was non-finite; the model then scores nothing and must still be freed). */
+gpbo_status gp_fit_async(gpbo_ctx *ctx, const gpbo_fit_args *args, gpbo_model **out);
+gpbo_status gp_model_sync(gpbo_ctx *ctx, const gpbo_model *model, int32_t *status,
+                          int32_t *jitter_k);
 void gp_model_free(gpbo_model *model);
 
 /* Fitted per-search statistics (host copies, any may be NULL): y mean and std (raw units),

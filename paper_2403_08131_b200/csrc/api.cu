@@ -34,6 +34,8 @@ struct gpbo_ctx {
   void *aux_h = nullptr;    // pinned mirror
   void *meta_h = nullptr;   // pinned staging of the fit's meta records
   size_t meta_cap = 0;
+  cudaEvent_t meta_ev = nullptr;  // recorded after the upload that reads meta_h
+  cudaEvent_t aux_ev = nullptr;   // recorded after the upload that reads aux_h
   size_t aux_cap = 0;
   int64_t launches = 0;
   // optional per-kernel CUDA-event timing (gpbo_set_profiling): kinds fit / fast / refine / pack
@@ -64,6 +66,7 @@ struct gpbo_model {
   unsigned char *img = nullptr;  // tcgen05 operand images
   int64_t img_bytes = 0;
   mutable bool simt_ready = false;  // Xs32 / LT32 built (on first CUDA-core scoring call)
+  mutable bool meta_pending = false;  // gp_fit_async: host meta not yet refreshed from the device
 };
 
 namespace {
@@ -170,6 +173,19 @@ gpbo_status ensure_meta_h(gpbo_ctx *ctx, size_t bytes) {
   return GPBO_OK;
 }
 
+// Host copy of the fit results of an asynchronously fitted model (blocking; not on the hot path
+// of the scoring call, which refreshes it in its own final synchronisation).
+gpbo_status refresh_meta(const gpbo_model *model) {
+  if (!model->meta_pending) return GPBO_OK;
+  gpbo_model *m = const_cast<gpbo_model *>(model);
+  if (cudaMemcpyAsync(m->meta.data(), m->meta_d, sizeof(SearchMeta) * m->S,
+                      cudaMemcpyDeviceToHost, m->stream) != cudaSuccess ||
+      cudaStreamSynchronize(m->stream) != cudaSuccess)
+    return GPBO_ECUDA;
+  m->meta_pending = false;
+  return GPBO_OK;
+}
+
 gpbo_status ensure_keys(gpbo_ctx *ctx, int S) {
   if (S <= ctx->keys_cap) return GPBO_OK;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -210,7 +226,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   if (st) return st;
   st = ensure_keys(ctx, S);
   if (st) return st;
-  CK(cudaStreamSynchronize(ctx->stream));  // aux_h may still feed an earlier copy
+  if (ctx->aux_ev) CK(cudaEventSynchronize(ctx->aux_ev));  // aux_h may feed an earlier copy
   char *h = (char *)ctx->aux_h;
   int64_t *h_off = (int64_t *)h;
   int64_t *h_base = h_off + (S + 1);
@@ -247,7 +263,9 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     if (Ms < 0 || h_base[i] < 0 || h_base[i] + Ms >= 0xFFFFFFFFll)
       return fail(ctx, GPBO_EINVAL, "candidate offsets out of range (M_s must be < 2^32-1)");
     const int st_i = model->meta[s_first + i].status;
-    const bool fitted = st_i == GPBO_OK || st_i == GPBO_WDEGENERATE;
+    // an asynchronous fit's status is not known here: its tiles run and the kernels skip a
+    // failed search on the device
+    const bool fitted = model->meta_pending || st_i == GPBO_OK || st_i == GPBO_WDEGENERATE;
     const int64_t t = fitted ? (Ms + tile - 1) / tile : 0;  // failed fits score nothing
     if ((int64_t)h_tiles[i] + t > (1ll << 30))
       return fail(ctx, GPBO_EINVAL, "too many candidates in one call");
@@ -260,6 +278,8 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     if (st) return st;
   }
   CK(cudaMemcpyAsync(ctx->aux_d, ctx->aux_h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->aux_ev) CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->aux_ev, ctx->stream));
   unsigned int *thr_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap);
   unsigned int *count_d = thr_d + ctx->keys_cap;
   CK(cudaMemsetAsync(ctx->keys_d, 0, ctx->keys_cap * (sizeof(unsigned long long) + 4) + 4,
@@ -345,7 +365,11 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
   unsigned int *count_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap) + ctx->keys_cap;
   CK(cudaMemcpyAsync(ctx->keys_h + ctx->keys_cap, count_d, 4, cudaMemcpyDeviceToHost,
                      ctx->stream));
+  if (model->meta_pending)  // the fit results ride along with the keys
+    CK(cudaMemcpyAsync(const_cast<gpbo_model *>(model)->meta.data(), model->meta_d,
+                       sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  model->meta_pending = false;
   CK(cudaGetLastError());
   harvest_events(ctx);
   ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
@@ -428,6 +452,8 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->aux_d) cudaFree(ctx->aux_d);
   if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
   if (ctx->meta_h) cudaFreeHost(ctx->meta_h);
+  if (ctx->meta_ev) cudaEventDestroy(ctx->meta_ev);
+  if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
   if (ctx->keys_d) cudaFree(ctx->keys_d);
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
   if (ctx->list_d) cudaFree(ctx->list_d);
@@ -482,8 +508,9 @@ void gp_model_free(gpbo_model *model) {
   delete model;
 }
 
-gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int32_t *status,
-                   int32_t *jitter_k) {
+namespace {
+gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bool wait,
+                     int32_t *status, int32_t *jitter_k) {
   if (!ctx) return GPBO_EINVAL;
   if (!a || !out) return fail(ctx, GPBO_EINVAL, "null args/out");
   *out = nullptr;
@@ -589,9 +616,12 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   }
   gpbo_status pst = ensure_meta_h(ctx, sizeof(SearchMeta) * S);
   if (pst) { gp_model_free(m); return pst; }
+  if (ctx->meta_ev) CKM(cudaEventSynchronize(ctx->meta_ev));  // previous upload read meta_h
   std::memcpy(ctx->meta_h, m->meta.data(), sizeof(SearchMeta) * S);
   CKM(cudaMemcpyAsync(meta_in, ctx->meta_h, sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
                       ctx->stream));
+  if (!ctx->meta_ev) CKM(cudaEventCreateWithFlags(&ctx->meta_ev, cudaEventDisableTiming));
+  CKM(cudaEventRecord(ctx->meta_ev, ctx->stream));
   {
     KernTimer t(ctx, kKernFit);
     CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream));
@@ -602,6 +632,11 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
     CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs64, m->alpha64, m->ls32, m->img,
                              ctx->stream));
     ctx->launches += 1;
+  }
+  if (!wait) {  // gp_fit_async: results stay on the device until gp_model_sync / scoring
+    m->meta_pending = true;
+    *out = m;
+    return GPBO_OK;
   }
   CKM(cudaMemcpyAsync(ctx->meta_h, m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
                       ctx->stream));
@@ -627,10 +662,38 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int3
   if (worst == GPBO_ENOTPD) ctx->err = "Cholesky failed at the largest jitter for some search";
   return worst;
 }
+}  // namespace
+
+gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int32_t *status,
+                   int32_t *jitter_k) {
+  return fit_impl(ctx, a, out, true, status, jitter_k);
+}
+
+gpbo_status gp_fit_async(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out) {
+  return fit_impl(ctx, a, out, false, nullptr, nullptr);
+}
+
+gpbo_status gp_model_sync(gpbo_ctx *ctx, const gpbo_model *model, int32_t *status,
+                          int32_t *jitter_k) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!model) return fail(ctx, GPBO_EINVAL, "null model");
+  if (refresh_meta(model)) return fail(ctx, GPBO_ECUDA, "meta download failed");
+  gpbo_status worst = GPBO_OK;
+  for (int s = 0; s < model->S; ++s) {
+    const SearchMeta &q = model->meta[s];
+    if (status) status[s] = q.status;
+    if (jitter_k) jitter_k[s] = q.jitter_k;
+    if (q.status == GPBO_EINVAL) worst = GPBO_EINVAL;
+    else if (q.status == GPBO_ENOTPD && worst != GPBO_EINVAL) worst = GPBO_ENOTPD;
+    else if (q.status == GPBO_WDEGENERATE && worst == GPBO_OK) worst = GPBO_WDEGENERATE;
+  }
+  return worst;
+}
 
 gpbo_status gp_model_stats(const gpbo_model *model, int32_t s, double *mean, double *std,
                            double *best, double *alpha_l1) {
   if (!model || s < 0 || s >= model->S) return GPBO_EINVAL;
+  if (refresh_meta(model)) return GPBO_ECUDA;
   const SearchMeta &q = model->meta[s];
   if (mean) *mean = q.mean;
   if (std) *std = q.std;
@@ -642,6 +705,7 @@ gpbo_status gp_model_stats(const gpbo_model *model, int32_t s, double *mean, dou
 gpbo_status gp_model_export(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, double *L,
                             double *Linv, double *alpha) {
   if (!ctx) return GPBO_EINVAL;
+  if (model && refresh_meta(model)) return fail(ctx, GPBO_ECUDA, "meta download failed");
   if (!model || s < 0 || s >= model->S) return fail(ctx, GPBO_EINVAL, "bad model/search");
   CK(cudaSetDevice(ctx->device));
   const SearchMeta &q = model->meta[s];
@@ -673,6 +737,7 @@ gpbo_status gp_posterior(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, cons
     return fail(ctx, GPBO_EINVAL, "bad model/search/candidates");
   if (mem != GPBO_HOST && mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
   CK(cudaSetDevice(ctx->device));
+  if (refresh_meta(model)) return fail(ctx, GPBO_ECUDA, "meta download failed");
   const SearchMeta &q = model->meta[s];
   if (q.status != GPBO_OK && q.status != GPBO_WDEGENERATE)
     return fail(ctx, GPBO_ENOTPD, "search has no valid fit");
@@ -693,7 +758,7 @@ gpbo_status gp_posterior(gpbo_ctx *ctx, const gpbo_model *model, int32_t s, cons
   o.var = (mem == GPBO_DEVICE && var) ? var : (float *)(b + xb + ob);
   o.ei = (mem == GPBO_DEVICE && ei) ? ei : (float *)(b + xb + 2 * ob);
   const int64_t off[2] = {0, M};
-  const double best = q.best;
+  const double best = NAN;  // the fitted incumbent (resolved on the device)
   st = run_score(ctx, model, s, 1, xd, off, nullptr, &best, gpbo::kModePosterior, o);
   if (st) return st;
   if (mem == GPBO_HOST) {
@@ -718,7 +783,8 @@ gpbo_status gpbo_debug_fast_phase(gpbo_ctx *ctx, const gpbo_model *model, int32_
   float *d[6] = {mu, dmu, var, dvar, ei_lo, ei_hi};
   for (int i = 0; i < 6; ++i) o.dbg[i] = d[i];
   const int64_t off[2] = {0, M};
-  const double best = model->meta[s].best;
+  if (refresh_meta(model)) return fail(ctx, GPBO_ECUDA, "meta download failed");
+  const double best = NAN;  // the fitted incumbent (resolved on the device)
   gpbo_status st = run_score(ctx, model, s, 1, Xstar_dev, off, nullptr, &best,
                              gpbo::kModeDebug, o);
   if (st) return st;
@@ -739,7 +805,7 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
   int64_t rows = 0, floats = 0;
   for (int s = 0; s < S; ++s) {
     const SearchMeta &q = model->meta[s];
-    best_std[s] = best ? (best[s] - q.mean) / q.std : q.best;
+    best_std[s] = best ? best[s] : NAN;  // raw units (standardised on the device) / fitted best
     const int64_t Ms = m_off[s + 1] - m_off[s];
     if (Ms < 0) return fail(ctx, GPBO_EINVAL, "m_off must be non-decreasing");
     rows += Ms;
@@ -801,7 +867,7 @@ gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
     base[s] = a;
     off[s + 1] = off[s] + (b - a);
     xoff[s + 1] = xoff[s] + (b - a) * model->meta[s].d;
-    best_std[s] = model->meta[s].best;
+    best_std[s] = NAN;  // the fitted incumbent (resolved on the device)
   }
   gpbo_status st = ensure_stage(ctx, (size_t)xoff[S] * 4 + 16);
   if (st) return st;

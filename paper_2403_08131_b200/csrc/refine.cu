@@ -118,7 +118,7 @@ refine_kernel(const RefineLaunch p) {
     if (tid == 0) {
       const double var64 = fmax((double)m.sf2 - vv, 0.0);
       const double sig = sqrt(var64);
-      const double imp = p.best[s] - mu;
+      const double imp = resolve_best(p.best[s], m) - mu;
       const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
       if (p.list) {
         const unsigned long long key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));

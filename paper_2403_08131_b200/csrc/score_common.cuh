@@ -59,6 +59,12 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k)
   return k;
 }
 
+// The incumbent in standardised units: the caller's raw-unit value (standardised with the fit's
+// mean / std, which live on the device for an asynchronous fit), or NaN = the fitted best.
+__device__ __forceinline__ double resolve_best(double best_in, const SearchMeta &m) {
+  return isnan(best_in) ? m.best : (best_in - m.mean) / m.std;
+}
+
 // Epilogue of the fast phase for one candidate (every thread of the block calls it; the block
 // belongs to one search).  mu: standardised fast mean (float32 K*), dmu: its error bound,
 // var: standardised latent variance, dvar: its error bound.
@@ -79,8 +85,11 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
                                             uint32_t bar_id = 0, uint32_t nthreads = 0,
                                             int gw0 = 0) {
   if (nthreads == 0) nthreads = blockDim.x;
+  const SearchMeta &mm = p.meta[s];
+  const bool fitted = mm.status == GPBO_OK || mm.status == GPBO_WDEGENERATE;
+  valid = valid && fitted;  // a failed asynchronous fit scores nothing
   const bool ok = valid && (force_refine || (isfinite(mu) && isfinite(var)));
-  const double best = p.best[s];
+  const double best = resolve_best(p.best[s], mm);
   float ei_lo = 0.f, ei_hi = 0.f;
   if (ok && p.mode != kModePosterior) {
     if (force_refine) {

@@ -62,6 +62,8 @@ def load():
         "gpbo_last_error": (C.c_char_p, [vp]),
         "gpbo_version": (C.c_char_p, []),
         "gp_fit": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(vp), vp, vp]),
+        "gp_fit_async": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(vp)]),
+        "gp_model_sync": (C.c_int, [vp, vp, vp, vp]),
         "gp_model_free": (None, [vp]),
         "gp_model_stats": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "gp_model_export": (C.c_int, [vp, vp, i32, vp, vp, vp]),
@@ -95,7 +97,7 @@ def load():
 def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
-            "gpbo_version", "gp_fit", "gp_model_free", "gp_model_stats", "gp_model_export",
+            "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
@@ -134,7 +136,24 @@ class Model:
     def __init__(self, ctx, handle, S, n, d, status, jitter_k):
         self.ctx, self.handle, self.S = ctx, handle, S
         self.n, self.d = list(n), list(d)
-        self.status, self.jitter_k = status, jitter_k
+        self._status, self._jitter_k = status, jitter_k
+
+    def sync(self):
+        """gp_model_sync: fetch the per-search statuses of an asynchronous fit."""
+        if self._status is None:
+            st = np.zeros(self.S, np.int32)
+            jk = np.zeros(self.S, np.int32)
+            load().gp_model_sync(self.ctx.handle, self.handle, st.ctypes.data, jk.ctypes.data)
+            self._status, self._jitter_k = st, jk
+        return self
+
+    @property
+    def status(self):
+        return self.sync()._status
+
+    @property
+    def jitter_k(self):
+        return self.sync()._jitter_k
 
     def stats(self, s):
         lib = load()
@@ -241,8 +260,9 @@ class Context:
         """0 auto, 1 CUDA-core, 2 tcgen05 (see include/gpbo.h)."""
         _check(self, load().gpbo_set_score_impl(self.handle, int(impl)))
 
-    def fit(self, n, d, X, y, lengthscale, signal_var, noise_var, kernel=MATERN52):
-        """gp_fit over a ragged batch; returns a Model (status per search in model.status)."""
+    def fit(self, n, d, X, y, lengthscale, signal_var, noise_var, kernel=MATERN52, wait=True):
+        """gp_fit over a ragged batch; returns a Model (status per search in model.status).
+        wait=False: gp_fit_async (statuses fetched on first access of model.status)."""
         lib = load()
         S = len(n)
         n_a = np.ascontiguousarray(n, dtype=np.int32)
@@ -253,6 +273,9 @@ class Context:
         args = FitArgs(S, n_a.ctypes.data, d_a.ctypes.data, ptrs[0][0], ptrs[1][0], ptrs[2][0],
                        ptrs[3][0], ptrs[4][0], int(kernel), mem)
         h = C.c_void_p()
+        if not wait:
+            _check(self, lib.gp_fit_async(self.handle, C.byref(args), C.byref(h)))
+            return Model(self, h, S, n_a, d_a, None, None)
         status = np.zeros(S, np.int32)
         jk = np.zeros(S, np.int32)
         st = lib.gp_fit(self.handle, C.byref(args), C.byref(h), status.ctypes.data,

@@ -262,3 +262,56 @@ def test_fast_phase_brackets_contain_oracle(G, name, make, impl):
             json.dump(stats, f)
     finally:
         ctx.set_score_impl(0)
+
+
+# ------------------------------------------------------------------ asynchronous fit
+def test_async_fit_matches_sync(G):
+    """gp_fit_async + ei_score_argmax == gp_fit + ei_score_argmax bit for bit (incl. a raw-unit
+    incumbent standardised on the device), and gp_model_sync reports the fit's statuses."""
+    gpbo, ctx = G
+    w = gen.make(3, M=4096)
+    Xs = np.ascontiguousarray(np.concatenate(w.Xstar), np.float32)
+    off = np.zeros(w.S + 1, np.int64)
+    off[1:] = np.cumsum([x.shape[0] for x in w.Xstar])
+    ms = ctx.fit(*H.pack(w), kernel=w.kernel)
+    ma = ctx.fit(*H.pack(w), kernel=w.kernel, wait=False)
+    i0, e0 = ctx.score_argmax(ms, Xs, off)
+    i1, e1 = ctx.score_argmax(ma, Xs, off)
+    assert np.array_equal(i0, i1) and np.array_equal(e0.view(np.uint32), e1.view(np.uint32))
+    best = np.array([s.y.min() - 0.1 for s in w.searches])
+    ma2 = ctx.fit(*H.pack(w), kernel=w.kernel, wait=False)
+    i2, e2 = ctx.score_argmax(ma2, Xs, off, best=best)
+    i3, e3 = ctx.score_argmax(ms, Xs, off, best=best)
+    assert np.array_equal(i2, i3) and np.array_equal(e2.view(np.uint32), e3.view(np.uint32))
+    assert np.array_equal(ma.status, ms.status) and np.array_equal(ma.jitter_k, ms.jitter_k)
+    for s in range(w.S):
+        assert ma.stats(s) == ms.stats(s)
+    for m in (ms, ma, ma2):
+        m.free()
+
+
+def test_async_fit_failed_search_scores_nothing(G):
+    """A non-finite input in one search: the asynchronous fit is enqueued (no host error), that
+    search returns idx -1 on the device path, the other searches are unaffected, and
+    gp_model_sync reports EINVAL."""
+    gpbo, ctx = G
+    w = gen.make(3, M=2048)
+    n, d, X, y, ls, sf2, sn2 = H.pack(w)
+    y = y.copy()
+    y[n[0] + 3] = np.nan  # search 1
+    Xs = np.ascontiguousarray(np.concatenate(w.Xstar), np.float32)
+    off = np.zeros(w.S + 1, np.int64)
+    off[1:] = np.cumsum([x.shape[0] for x in w.Xstar])
+    ma = ctx.fit(n, d, X, y, ls, sf2, sn2, kernel=w.kernel, wait=False)
+    idx, ei = ctx.score_argmax(ma, Xs, off)
+    assert idx[1] == -1 and ei[1] == 0.0
+    y_ok = H.pack(w)[3]
+    ms = ctx.fit(n, d, X, y_ok, ls, sf2, sn2, kernel=w.kernel)
+    i0, _ = ctx.score_argmax(ms, Xs, off)
+    keep = [s for s in range(w.S) if s != 1]
+    assert np.array_equal(idx[keep], i0[keep])
+    st = np.zeros(w.S, np.int32)
+    rc = gpbo.load().gp_model_sync(ctx.handle, ma.handle, st.ctypes.data, None)
+    assert rc == gpbo.EINVAL and st[1] == gpbo.EINVAL
+    ma.free()
+    ms.free()
