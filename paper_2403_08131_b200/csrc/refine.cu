@@ -82,36 +82,54 @@ refine_kernel(const RefineLaunch p) {
     const double *alpha = p.alpha64 + m.a_off;
     double mu = 0.0;
     for (int j = tid; j < n; j += kRefineThreads) {
-      double r2 = 0.0;
-      for (int c = 0; c < d; ++c) {
-        const double diff = xsh[c] - Xj[(size_t)c * n + j];  // column-major x/l
-        r2 += diff * diff;
+      double r2 = 0.0, r2b = 0.0;
+      int c = 0;
+      for (; c + 2 <= d; c += 2) {  // two independent loads per step
+        const double d0 = xsh[c] - Xj[(size_t)c * n + j];  // column-major x/l
+        const double d1 = xsh[c + 1] - Xj[(size_t)(c + 1) * n + j];
+        r2 += d0 * d0;
+        r2b += d1 * d1;
       }
+      if (c < d) {
+        const double d0 = xsh[c] - Xj[(size_t)c * n + j];
+        r2 += d0 * d0;
+      }
+      r2 += r2b;
       const double k = kernel64(r2, (double)m.sf2, m.kernel);
       ksh[j] = k;
       mu += k * alpha[j];
     }
     mu = block_sum2(mu, red);  // includes the barrier that publishes ksh
-    // v = L^-1 k*: warp per row j (Linv64 is row-major: lanes read consecutive k), two rows at a
-    // time for more loads in flight
+    // v = L^-1 k*: warp per row j (Linv64 is row-major: lanes read consecutive k); four rows per
+    // pass and the k loop unrolled by two, so up to 8 loads per lane are in flight (the rows come
+    // from L2 / HBM: a pass is one memory round trip)
     const double *Li = p.Linv64 + m.mat_off;
     const int lane = tid & 31, wp = tid >> 5;
     constexpr int kW = kRefineThreads / 32;
     double vv = 0.0;
-    for (int j = wp; j < n; j += 2 * kW) {
-      const int j2 = j + kW;
-      const double *r1 = Li + (size_t)j * n, *r2 = Li + (size_t)min(j2, n - 1) * n;
-      double a = 0.0, b = 0.0;
-      for (int k = lane; k <= j; k += 32) a = fma(r1[k], ksh[k], a);
-      if (j2 < n)
-        for (int k = lane; k <= j2; k += 32) b = fma(r2[k], ksh[k], b);
+    for (int j0 = wp; j0 < n; j0 += 4 * kW) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double *row[4];
+      int jr[4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
+      for (int r = 0; r < 4; ++r) {
+        jr[r] = j0 + r * kW < n ? j0 + r * kW : -1;  // -1: no such row
+        row[r] = Li + (size_t)min(j0 + r * kW, n - 1) * n;
       }
-      vv = fma(a, a, vv);
-      if (j2 < n) vv = fma(b, b, vv);
+      const int jmax = min(j0 + 3 * kW, n - 1);
+      for (int k = lane; k <= jmax; k += 32) {  // the 4 rows' loads issue together
+        const double kv = ksh[k];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (k <= jr[r]) acc[r] = fma(row[r][k], kv, acc[r]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (j0 + r * kW < n) vv = fma(acc[r], acc[r], vv);
     }
     if (lane != 0) vv = 0.0;
     vv = block_sum2(vv, red);
