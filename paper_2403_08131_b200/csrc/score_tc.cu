@@ -63,6 +63,7 @@ enum {
   B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
   B_SF0, B_SF1,                             // raw candidate rows landed in staging (TMA)
   B_PF0, B_PF1, B_PE0, B_PE1,               // per-tile partial sums (mu, |mu| bound) K* -> drain
+  B_VB0, B_VB1, B_VB2, B_VB3, B_VB4, B_VB5, B_VB6, B_VB7,  // V column block p final (per panel)
   B_IMG, B_COUNT
 };
 
@@ -189,6 +190,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
       tc::mbar_init(bar(B_KF0 + i), 8);
       tc::mbar_init(bar(B_KE0 + i), 1);
     }
+    for (int i = 0; i < 8; ++i) tc::mbar_init(bar(B_VB0 + i), 1);
     tc::mbar_init(bar(B_IMG), 1);
     tc::fence_mbar_init();
   }
@@ -295,10 +297,13 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             }
           }
           tc::mma_commit_warp(bar(B_KE0 + ks));
+          // V columns [32 p, 32 p + 32) receive no later contribution: the drain may read them
+          tc::mma_commit_warp(bar(B_VB0 + v_pp));
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
           if (++v_pp == npan) {
-            tc::mma_commit_warp(bar(B_VF0));
+            // the unused block barriers complete too: every B_VB completes once per tile
+            for (int q = npan; q < 8; ++q) tc::mma_commit_warp(bar(B_VB0 + q));
             v_pp = 0;
             ++v_tl;
           }
@@ -401,30 +406,33 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
       const uint32_t va = tbase + ((uint32_t)(32 * lq) << 16);
       for (int tl = 0; tl < T; ++tl) {
         const uint32_t ti = gi + tl;
-        tc::mbar_wait(bar(B_VF0), ti & 1u);
-        tc::tc_fence_after();
+        // progressive drain: column block p of V is final once panel p's MMAs complete (each
+        // B_VB barrier completes once per tile, and the next tile cannot start before B_VE)
         float vv = 0.f;
-        int c = 0;
-        for (; c + 32 <= n16; c += 32) {
-          uint32_t r0[16], r1[16];
-          tc::tmem_ld16(va + (uint32_t)c, r0);
-          tc::tmem_ld16(va + (uint32_t)(c + 16), r1);
-          tc::tmem_wait_ld();
+        for (int pb = 0; pb < npan; ++pb) {
+          tc::mbar_wait(bar(B_VB0 + pb), ti & 1u);
+          tc::tc_fence_after();
+          const int c = 32 * pb;
+          if (c + 32 <= n16) {
+            uint32_t r0[16], r1[16];
+            tc::tmem_ld16(va + (uint32_t)c, r0);
+            tc::tmem_ld16(va + (uint32_t)(c + 16), r1);
+            tc::tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float v0 = __uint_as_float(r0[q]), v1 = __uint_as_float(r1[q]);
-            vv = fmaf(v0, v0, vv);
-            vv = fmaf(v1, v1, vv);
-          }
-        }
-        if (c < n16) {  // n16 is a multiple of 16
-          uint32_t r16[16];
-          tc::tmem_ld16(va + (uint32_t)c, r16);
-          tc::tmem_wait_ld();
+            for (int q = 0; q < 16; ++q) {
+              const float v0 = __uint_as_float(r0[q]), v1 = __uint_as_float(r1[q]);
+              vv = fmaf(v0, v0, vv);
+              vv = fmaf(v1, v1, vv);
+            }
+          } else {  // n16 - c = 16
+            uint32_t r16[16];
+            tc::tmem_ld16(va + (uint32_t)c, r16);
+            tc::tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float v = __uint_as_float(r16[q]);
-            vv = fmaf(v, v, vv);
+            for (int q = 0; q < 16; ++q) {
+              const float v = __uint_as_float(r16[q]);
+              vv = fmaf(v, v, vv);
+            }
           }
         }
         tc::tc_fence_before();
