@@ -529,6 +529,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   m->stream = ctx->stream;
   m->meta.resize(S);
   int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0, nscr = 0;
+  int64_t nkt = 0;
   int smem_max = 0;
   for (int s = 0; s < S; ++s) {
     const int n = a->n[s], d = a->d[s];
@@ -554,9 +555,9 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     gpbo::tc_fill_geometry(q);
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
-    int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
-    q.xs_smem = smem + n * d * 8 <= gpbo::kFitSmemBudget;
-    if (q.xs_smem) smem += n * d * 8;
+    q.kt_off = nkt; nkt += gpbo::fit_tile_doubles(n);
+    const int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
+    q.xs_smem = 0;
     smem_max = std::max(smem_max, smem);
     m->nmax = std::max(m->nmax, n);
     m->dmax = std::max(m->dmax, q.d_pad);
@@ -571,7 +572,8 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   const size_t o_x = take(nx * 4), o_ls = take(nls * 4), o_xs = take(nxs * 4);
   const size_t o_lt = take(nlt * 4), o_y = take(ny * 8), o_L = take(nmat * 8);
   const size_t o_Li = take(nmat * 8), o_a = take(na * 8), o_img = take(nimg);
-  const size_t o_x64 = take(nx * 8), o_scr = take(nscr * 8);
+  const size_t o_x64 = take(nx * 8), o_scr = take(nscr * 8), o_kt = take(nkt * 8);
+  const size_t o_pm = take((size_t)S * 16 * 8);
   cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
   if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
   m->meta_d = (SearchMeta *)(m->block + o_meta);
@@ -587,6 +589,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   m->img = (unsigned char *)(m->block + o_img);
   m->Xs64 = (double *)(m->block + o_x64);
   double *Wscr64 = (double *)(m->block + o_scr);
+  double *Kt64 = (double *)(m->block + o_kt);
   m->img_bytes = nimg;
   const cudaMemcpyKind kind = a->mem == GPBO_HOST ? cudaMemcpyHostToDevice
                                                   : cudaMemcpyDeviceToDevice;
@@ -605,6 +608,8 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   io.X32 = m->X32; io.ls32 = m->ls32; io.y64 = m->y64;
   io.L64 = m->L64; io.Linv64 = m->Linv64; io.Xs64 = m->Xs64; io.alpha64 = m->alpha64;
   io.Wscr64 = Wscr64;
+  io.Kt64 = Kt64;
+  io.pm_part = (double *)(m->block + o_pm);
   if (a->mem == GPBO_HOST) {  // stage into the model's arrays
     CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
     CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));
@@ -624,8 +629,10 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   CKM(cudaEventRecord(ctx->meta_ev, ctx->stream));
   {
     KernTimer t(ctx, kKernFit);
+    CKM(gpbo::launch_gram(meta_in, S, m->nmax, m->dmax, io, ctx->stream));
     CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream));
   }
+  ctx->launches += 2;
   ctx->launches += 1;
   if (nimg > 0) {
     KernTimer t(ctx, kKernPack);

@@ -25,6 +25,7 @@
 //   T  the rest: W(i, k) -= sum_u G[u][i] G[u][k] over rows below the block x (columns left of
 //      it and the trailing triangle), 8 x 8 DMMA tiles dealt to the warps.  Warp 0 updates the
 //      next diagonal block first and runs its D while the other warps finish T (look-ahead).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -189,21 +190,9 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   }
   const double best = block_reduce(bmin, red, MinOp(), INFINITY);
 
-  // ---- x / l in float64, column-major (d x n), for the Gram, the refine phase and the
-  // tcgen05 image; pmax = max_j |x_j / l|^2
-  double *xsm = sm + fit_smem_doubles(n, kSmem);  // x / l in shared memory when m.xs_smem
-  double pm = 0.0;
-  for (int i = tid; i < n; i += kFitThreads) {
-    double q = 0.0;
-    for (int c = 0; c < d; ++c) {
-      const double v = (double)X[i * d + c] / (double)ls[c];
-      Xs64[m.x_off + (size_t)c * n + i] = v;
-      if (m.xs_smem) xsm[c * n + i] = v;
-      q += v * v;
-    }
-    pm = fmax(pm, q);
-  }
-  const double pmax = block_reduce(pm, red, MaxOp(), 0.0);
+  // ---- pmax = max_j |x_j / l|^2 (the pre-pass's per-CTA maxima)
+  double pmax = 0.0;
+  for (int b = 0; b * 128 < n; ++b) pmax = fmax(pmax, io.pm_part[16 * s + b]);
 
   // ---- H2 + H3 + H4 along the jitter ladder j_k = 1e-8 10^k sf2
   const double sf2 = m.sf2, sn2 = m.sn2;
@@ -299,32 +288,24 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   for (int k = 0; k < 7 && jk < 0; ++k, p10 *= 10.0) {
     jit = 1e-8 * p10 * sf2;
     __syncthreads();
-    // H2: one 8 x 8 tile per warp item, two entries per lane (its accumulator-fragment slots):
-    // squared distances of x / l by direct differences (reading R1), the kernel, + sn2 + jitter
-    // on the diagonal; entries outside the matrix are stored as 0
-    auto gram = [&](const double *xs) {
-      for (int e = warp; e < ntiles; e += kWarps) {
-        int R, C;
-        tile_rc(e, R, C);
-        const int i = 8 * R + gid, kc = 8 * C + 2 * tig;
-        const int ia = min(i, n - 1), k0 = min(kc, n - 1), k1 = min(kc + 1, n - 1);
-        double r0 = 0.0, r1 = 0.0;
-#pragma unroll 4
-        for (int c = 0; c < d; ++c) {
-          const double *col = xs + c * n;
-          const double xi = col[ia];
-          const double d0 = xi - col[k0], d1 = xi - col[k1];
-          r0 = fma(d0, d0, r0);
-          r1 = fma(d1, d1, r1);
-        }
-        double v0 = 0.0, v1 = 0.0;
-        if (i < n && kc <= i) v0 = kernel_value(r0, sf2, m.kernel) + (kc == i ? sn2 + jit : 0.0);
-        if (i < n && kc + 1 <= i)
-          v1 = kernel_value(r1, sf2, m.kernel) + (kc + 1 == i ? sn2 + jit : 0.0);
-        *reinterpret_cast<double2 *>(W + tb(R, C) + 2 * lane) = make_double2(v0, v1);
+    // H2: the pre-pass's kernel tiles (L2) into W, 4 x 16 B in flight per thread, then + sn2 +
+    // jitter on the diagonal
+    {
+      const double2 *src = reinterpret_cast<const double2 *>(io.Kt64 + m.kt_off);
+      double2 *dst = reinterpret_cast<double2 *>(W);
+      const int n2 = ntiles * 32;
+      for (int e0 = tid; e0 < n2; e0 += 4 * kFitThreads) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * kFitThreads < n2) v[u] = src[e0 + u * kFitThreads];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * kFitThreads < n2) dst[e0 + u * kFitThreads] = v[u];
       }
-    };
-    if (m.xs_smem) gram(xsm); else gram(xc);
+      __syncthreads();
+      for (int i = tid; i < n; i += kFitThreads) W[at(i, i)] += sn2 + jit;
+    }
     __syncthreads();
     FIT_T(1);
     if (warp == kWarps - 1) diag_block(0);
@@ -552,6 +533,66 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   }
 }
 
+// ---- Gram pre-pass (H2), spread over many CTAs so the single-CTA factorisation starts from a
+// ready kernel matrix.  One launch, CTA (x, s) of 128 threads:
+//   x < ceil(n / 128): x / l in float64 (the oracle's A / l) for points 128 x .. into Xs64
+//      (column-major d x n), and the CTA's max |x / l|^2 into pm_part[16 s + x];
+//   warp w: tile e = 4 x + w of the tile-packed lower triangle -- its 16 points' x / l staged in
+//      shared memory, squared distances by direct differences (reading R1), the kernel (no noise,
+//      no jitter: the fit adds them per jitter-ladder step); entries outside the matrix are 0.
+__global__ void __launch_bounds__(128)
+gram_kernel(const SearchMeta *__restrict__ meta, const FitIO io) {
+  __shared__ double xw[4][16][GPBO_MAX_D + 1];
+  __shared__ double red[4];
+  const int s = blockIdx.y;
+  const SearchMeta m = meta[s];
+  const int n = m.n, d = m.d, nt = (n + 7) / 8;
+  const float *X = io.X_src + m.x_off;
+  const float *ls = io.ls_src + m.ls_off;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if ((int)blockIdx.x * 128 < n) {
+    const int i = blockIdx.x * 128 + threadIdx.x;
+    double q = 0.0;
+    if (i < n)
+      for (int c = 0; c < d; ++c) {
+        const double v = (double)X[i * d + c] / (double)ls[c];
+        io.Xs64[m.x_off + (size_t)c * n + i] = v;
+        q += v * v;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q = fmax(q, __shfl_xor_sync(0xffffffffu, q, o));
+    if (lane == 0) red[w] = q;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      io.pm_part[16 * s + blockIdx.x] = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  }
+  const int e = blockIdx.x * 4 + w;
+  if (e >= nt * (nt + 1) / 2) return;
+  const int gid = lane >> 2, tig = lane & 3;
+  int R, C;
+  tile_rc(e, R, C);
+  // stage x / l of rows 8R.. (slots 0-7) and columns 8C.. (slots 8-15), clamped to n - 1
+  for (int t = lane; t < 16 * d; t += 32) {
+    const int slot = t / d, c = t - slot * d;
+    const int pt = min((slot < 8 ? 8 * R + slot : 8 * C + slot - 8), n - 1);
+    xw[w][slot][c] = (double)X[pt * d + c] / (double)ls[c];
+  }
+  __syncwarp();
+  const int i = 8 * R + gid, kc = 8 * C + 2 * tig;
+  const double *xi = xw[w][gid], *xk0 = xw[w][8 + 2 * tig], *xk1 = xw[w][9 + 2 * tig];
+  double r0 = 0.0, r1 = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double d0 = xi[c] - xk0[c], d1 = xi[c] - xk1[c];
+    r0 = fma(d0, d0, r0);
+    r1 = fma(d1, d1, r1);
+  }
+  const double sf2 = io.sf2_src ? (double)io.sf2_src[s] : (double)m.sf2;
+  double v0 = 0.0, v1 = 0.0;
+  if (i < n && kc <= i) v0 = kernel_value(r0, sf2, m.kernel);
+  if (i < n && kc + 1 <= i) v1 = kernel_value(r1, sf2, m.kernel);
+  reinterpret_cast<double2 *>(io.Kt64 + m.kt_off + tb(R, C))[lane] = make_double2(v0, v1);
+}
+
 __global__ void __launch_bounds__(kFitThreads, 1)
 fit_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
            SearchMeta *__restrict__ meta_out) {
@@ -598,6 +639,15 @@ cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const Fi
     smem_set = smem_bytes;
   }
   fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, io, meta_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, const FitIO &io,
+                        cudaStream_t stream) {
+  (void)dmax;
+  const int nt = (nmax + 7) / 8;
+  const int gx = std::max((nt * (nt + 1) / 2 + 3) / 4, (nmax + 127) / 128);
+  gram_kernel<<<dim3(gx, S), 128, 0, stream>>>(meta_d, io);
   return cudaGetLastError();
 }
 

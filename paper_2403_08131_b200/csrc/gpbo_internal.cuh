@@ -64,6 +64,7 @@ struct SearchMeta {
   int32_t use_smem;     // fit keeps its working matrix in shared memory
   int32_t xs_smem;      // fit stages x / l (n x d float64) in shared memory for the Gram
   int64_t scr_off;      // else: its tile-packed working matrix (fit_tile_doubles) in model.Wscr64
+  int64_t kt_off;       // kernel matrix k(X, X) without noise / jitter, tile-packed, in model.Kt64
 };
 
 // Candidate flagged by the fast phase for the float64 refine phase.
@@ -138,7 +139,12 @@ struct FitIO {
   const float *sf2_src, *sn2_src;  // [S] (device); null: taken from the meta records
   float *X32, *ls32;             // model copies (skipped when equal to the sources)
   double *y64, *L64, *Linv64, *Xs64, *alpha64, *Wscr64;
+  double *Kt64;                  // the Gram pre-pass output (tile-packed, no noise / jitter)
+  double *pm_part;               // [16 S] per-CTA max |x / l|^2 of the pre-pass
 };
+// Gram pre-pass on many CTAs (fit.cu): x / l (Xs64) then the kernel matrix tiles (Kt64).
+cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, const FitIO &io,
+                        cudaStream_t stream);
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
                        SearchMeta *meta_out, cudaStream_t stream);
 cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
