@@ -248,7 +248,7 @@ gpbo_status gpbo_tc_selftest(const void *A, const void *B, float *D, int N, int 
 gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int N, int K, int row_bytes,
                           int b_row_off, int reps, long long *cycles);
 
-/* Test hook: if dev_buf (device, >= 65536 uint64) is non-NULL, the tcgen05 kernel of later
+/* Test hook: if dev_buf (device, >= 98304 uint64) is non-NULL, the tcgen05 kernel of later
  * scoring calls records clock64 pipeline events of CTA 0 into it (entry 0 = count, then
  * (tag << 56 | role << 48 | panel) / clock pairs).  NULL disables. */
 gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf);

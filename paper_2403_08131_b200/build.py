@@ -33,9 +33,12 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, defines=(), out=None):
+    """defines/out: A/B experiment builds (extra -D flags, separate object dir and library)."""
     inc, lib = _nccl_dirs()
-    os.makedirs(BUILD, exist_ok=True)
+    OUT_ = out or OUT
+    BUILD_ = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(defines))
+    os.makedirs(BUILD_, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     hdr_t = max(os.path.getmtime(h) for h in headers)
@@ -47,18 +50,19 @@ def build(verbose=False, force=False):
     if os.environ.get("GPBO_TC_TRACE"):  # clock64 pipeline trace hooks (tools/trace_tc.py)
         common += ["-DGPBO_TC_TRACE"]
         force = True
+    common += ["-D" + d for d in defines]
     jobs = []
     for s in srcs:
-        o = os.path.join(BUILD, os.path.basename(s) + ".o")
+        o = os.path.join(BUILD_, os.path.basename(s) + ".o")
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_t):
             jobs.append(([NVCC] + common + ["-c", s, "-o", o], s))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         for (cmd, s), log in zip(jobs, ex.map(lambda j: _run(j[0]), jobs)):
             logs.append((s, log))
-    objs = [os.path.join(BUILD, os.path.basename(s) + ".o") for s in srcs]
-    if jobs or not os.path.exists(OUT):
-        _run([NVCC] + ARCH + ["-shared", "-o", OUT] + objs +
+    objs = [os.path.join(BUILD_, os.path.basename(s) + ".o") for s in srcs]
+    if jobs or not os.path.exists(OUT_):
+        _run([NVCC] + ARCH + ["-shared", "-o", OUT_] + objs +
              ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib, "-lcudart"])
     with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
         for s, log in logs:
@@ -66,7 +70,7 @@ def build(verbose=False, force=False):
     if verbose:
         for s, log in logs:
             print(f"==== {os.path.basename(s)}\n{log}")
-    return OUT
+    return OUT_
 
 
 if __name__ == "__main__":

@@ -79,41 +79,67 @@ __device__ __forceinline__ double resolve_best(double best_in, const SearchMeta 
 // The group of `nthreads` threads (warps gw0.. of the block, one candidate each) synchronises
 // with named barrier `bar_id` (0 = the whole block).  force_refine: the fast phase could not
 // evaluate this candidate safely (e.g. float16 range) -> EI_hi = +inf.
-__device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool valid,
-                                            int64_t row0, int64_t row, double mu, float dmu,
-                                            float var, float dvar, bool force_refine = false,
-                                            uint32_t bar_id = 0, uint32_t nthreads = 0,
-                                            int gw0 = 0) {
-  if (nthreads == 0) nthreads = blockDim.x;
+// Per-search values of the epilogue, loaded once per search segment by the persistent kernel
+// (each is a dependent global round trip; the tcgen05 drain warps hoist them out of the tile
+// loop).  thr: the search's running threshold as read by the caller for this tile.
+struct FinishSeg {
+  double best;      // incumbent, standardised
+  int64_t m_base;   // global index of the search's first local candidate
+  bool fitted;      // the (possibly asynchronous) fit succeeded
+};
+
+__device__ __forceinline__ FinishSeg finish_seg(const ScoreLaunch &p, int s) {
   const SearchMeta &mm = p.meta[s];
-  const bool fitted = mm.status == GPBO_OK || mm.status == GPBO_WDEGENERATE;
+  FinishSeg f;
+  f.fitted = mm.status == GPBO_OK || mm.status == GPBO_WDEGENERATE;
+  f.best = resolve_best(p.best[s], mm);
+  f.m_base = p.m_base[s];
+  return f;
+}
+
+__device__ __forceinline__ float read_thr(const ScoreLaunch &p, int s) {
+  return __uint_as_float(*(volatile const unsigned int *)(p.thr + s));
+}
+
+__device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, const FinishSeg &fs,
+                                            float thr, bool valid, int64_t row0, int64_t row,
+                                            double mu, float dmu, float var, float dvar,
+                                            bool force_refine, uint32_t bar_id, uint32_t nthreads,
+                                            int gw0) {
+  const bool fitted = fs.fitted;
   valid = valid && fitted;  // a failed asynchronous fit scores nothing
   const bool ok = valid && (force_refine || (isfinite(mu) && isfinite(var)));
-  const double best = resolve_best(p.best[s], mm);
+  const double best = fs.best;
   float ei_lo = 0.f, ei_hi = 0.f;
   if (ok && p.mode != kModePosterior) {
     if (force_refine) {
       ei_hi = INFINITY;
       ei_lo = 0.f;
     } else {
-      // Cheap screen (argmax mode): for z = (best - mu_lo)/s_hi < 0, Gordon's inequality
-      // Phi(-x) >= x phi(x)/(1 + x^2) gives EI <= s_hi phi(z)/(1 + z^2) -- one exp instead of
-      // the two erfc-based bracket ends.  A candidate whose screen is below the running
-      // threshold cannot be the argmax: EI_hi := screen, EI_lo := 0 (both still valid bounds).
+      // Cheap screens (argmax mode), against the running threshold thr (a lower bound of the
+      // search's final max EI_lo).  With s_hi = sqrt(var + dvar), z = (best - mu_lo)/s_hi:
+      //   z < 0:  Gordon's inequality Phi(-x) >= x phi(x)/(1 + x^2) gives
+      //           EI <= s_hi phi(z)/(1 + z^2)                       (one exp);
+      //   z >= 0: Phi <= 1 gives EI <= s_hi phi(z) + (best - mu_lo)  (one exp).
+      // A candidate whose screen is below thr cannot be the argmax: EI_hi := screen, EI_lo := 0
+      // (both still valid bounds).  Otherwise EI_hi is evaluated exactly; EI_lo is needed only
+      // when EI_hi >= thr (else it could neither raise the threshold nor be flagged).
       bool screened = false;
       if (p.mode == kModeArgmax) {
-        const float thr = __uint_as_float(*(volatile const unsigned int *)(p.thr + s));
         const float s_hi = sqrtf(var + dvar);
-        const float z = (float)(best - (mu - (double)dmu)) / s_hi;
-        if (s_hi > 0.f && z < 0.f) {
-          const float ub = s_hi * 0.398942280401432678f * __expf(-0.5f * z * z) /
-                           fmaf(z, z, 1.f) * 1.001f;
+        const float imp = (float)(best - (mu - (double)dmu));
+        const float z = imp / s_hi;
+        if (s_hi > 0.f) {
+          const float ph = s_hi * 0.398942280401432678f * __expf(-0.5f * z * z);
+          const float ub = (z < 0.f ? ph / fmaf(z, z, 1.f) : ph + imp) * 1.001f;
           if (ub < thr) { ei_hi = ub; ei_lo = 0.f; screened = true; }
         }
       }
       if (!screened) {
         ei_hi = ei_f32(mu - (double)dmu, var + dvar, best) * (1.f + 2e-4f);
-        ei_lo = ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f);
+        ei_lo = (p.mode != kModeArgmax || !(ei_hi < thr))
+                    ? ei_f32(mu + (double)dmu, fmaxf(var - dvar, 0.f), best) * (1.f - 2e-4f)
+                    : 0.f;
       }
     }
   }
@@ -131,8 +157,8 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
   }
   __shared__ unsigned int s_thr[32];
   __shared__ unsigned long long s_zk[32];
-  const unsigned int thr_entry = *(volatile const unsigned int *)(p.thr + s);
-  const uint64_t gidx = (uint64_t)(p.m_base[s] + row);
+  const unsigned int thr_entry = __float_as_uint(thr);
+  const uint64_t gidx = (uint64_t)(fs.m_base + row);
   unsigned int lo_bits = ok ? __float_as_uint(fmaxf(ei_lo, 0.f)) : 0u;
   unsigned long long zkey = (ok && !(ei_hi > 0.f)) ? make_key(0.f, gidx) : 0ull;
 #pragma unroll
@@ -162,8 +188,8 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
     }
   }
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
-  const float thr = __uint_as_float(s_thr[0]);
-  const bool flag = ok && ei_hi > 0.f && ei_hi >= thr;
+  const float thr_fin = __uint_as_float(s_thr[0]);
+  const bool flag = ok && ei_hi > 0.f && ei_hi >= thr_fin;
   const unsigned int mask = __ballot_sync(0xffffffffu, flag);
   if (mask) {
     const int leader = __ffs(mask) - 1;
@@ -175,6 +201,20 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool va
       if (pos < p.list_cap) p.list[pos] = RefineEntry{s, (uint32_t)row, var, ei_hi};
     }
   }
+}
+
+// Convenience form for kernels without a per-segment hoist (CUDA-core kernel): loads the
+// search's values and the threshold itself.
+__device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, bool valid,
+                                            int64_t row0, int64_t row, double mu, float dmu,
+                                            float var, float dvar, bool force_refine = false,
+                                            uint32_t bar_id = 0, uint32_t nthreads = 0,
+                                            int gw0 = 0) {
+  if (nthreads == 0) nthreads = blockDim.x;
+  const FinishSeg fs = finish_seg(p, s);
+  const float thr = p.mode == kModeArgmax ? read_thr(p, s) : 0.f;
+  finish_fast(p, s, fs, thr, valid, row0, row, mu, dmu, var, dvar, force_refine, bar_id, nthreads,
+              gw0);
 }
 
 }  // namespace gpbo

@@ -101,7 +101,7 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   s.k = s.a + 2 * kb_max * 8192;
   s.stage = s.k;
   s.rowinfo = s.stage + 2 * ((128 * d_max * 4 + 127) & ~127);
-  s.part_mu = s.rowinfo + 4 * 128 * 8;
+  s.part_mu = s.rowinfo + 8 * 128 * 8;
   s.part_a1 = s.part_mu + 4 * 128 * 8;
   s.bars = s.part_a1 + 4 * 128 * 4;
   s.total = s.bars + B_COUNT * 8 + 16 + 1024;  // + tmem slot, + alignment slack
@@ -143,7 +143,7 @@ __device__ __forceinline__ void trace_ev(unsigned long long *tr, uint32_t tag, u
 #endif
   if (tr == nullptr || blockIdx.x != 0) return;
   const unsigned long long c = clock64();
-  const uint32_t slice = role == 11 ? 0u : role == 8 ? 1u : role == 0 ? 2u : 3u;
+  const uint32_t slice = role == 11 ? 0u : role == 8 ? 1u : role == 0 ? 2u : role == 9 ? 4u : 3u;
   if (2 * cnt + 2 < 16384) {
     unsigned long long *b = tr + slice * 16384;
     b[2 * cnt] = ((unsigned long long)tag << 56) | ((unsigned long long)role << 48) | idx;
@@ -205,6 +205,9 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
   uint32_t gi = 0, gc_seg = 0, gk_seg = 0;
   uint32_t trc = 0;  // trace event count of this thread
   uint32_t img_phase = 0;
+  // completions of B_VE0 / B_VE1 (V buffer freed) and of the block-barrier groups B_VB0..3 /
+  // B_VB4..7 so far: the single- and double-buffered modes can alternate between segments
+  uint32_t ve0 = 0, ve1 = 0, vb0c = 0, vb1c = 0;
 
   for (int ta = t0; ta < t1;) {
     // ---------------- segment [ta, tb): consecutive tiles of one search
@@ -219,6 +222,11 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
     tc::mbar_wait(bar(B_IMG), img_phase);
     img_phase ^= 1u;
     const int n16 = m.n16, npan = m.npan, kb = m.kb;
+    // n16 <= 128: two V accumulators [0, 128) and [128, 256) alternate between tiles, so the
+    // next tile's variance MMAs never wait for the previous tile's drain; block barriers
+    // B_VB0..3 / B_VB4..7 per buffer.  Otherwise one accumulator and 8 block barriers.
+    const bool dbl = n16 <= 128;
+    const uint32_t vbq = dbl ? 4u : 8u;
     const int T = tb - ta;
     const int P = T * npan;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
@@ -276,8 +284,10 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           tc::mbar_wait(bar(B_KF0 + ks), (gk / kKStages) & 1u);
           if (lane == 0) trace_ev(p.trace, 2, 11, gk, trc);
           tc::tc_fence_after();
+          const uint32_t vti = gi + (uint32_t)v_tl;
+          const uint32_t vb = dbl ? (vti & 1u) : 0u;  // V buffer of this tile
           if (v_pp == 0) {
-            tc::mbar_wait(bar(B_VE0), ((gi + v_tl) & 1u) ^ 1u);
+            tc::mbar_wait(bar(B_VE0 + vb), ((vb ? ve1 : ve0) & 1u) ^ 1u);
             tc::tc_fence_after();
           }
           const uint32_t kt = tbase + kKstar0 + 32u * ks;  // K* stage in TMEM
@@ -288,7 +298,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
             const int j0 = 32 * v_pp + 16 * h;
             if (j0 < n16) {
               const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
-              const uint32_t dt = tbase + (uint32_t)j0;
+              const uint32_t dt = tbase + 128u * vb + (uint32_t)j0;
               const uint32_t ka = kt + 8u * h;         // k step h: hi at +8h, lo at +16 + 8h
               const uint32_t lb = lp + 66u * h;        // +1024 B rows, +32 B k-advance
               tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | h) ? 1u : 0u);
@@ -298,14 +308,15 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           }
           tc::mma_commit_warp(bar(B_KE0 + ks));
           // V columns [32 p, 32 p + 32) receive no later contribution: the drain may read them
-          tc::mma_commit_warp(bar(B_VB0 + v_pp));
+          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
           if (++v_pp == npan) {
             // the unused block barriers complete too: every B_VB completes once per tile
-            for (int q = npan; q < 8; ++q) tc::mma_commit_warp(bar(B_VB0 + q));
+            for (int q = npan; q < (int)vbq; ++q) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
             v_pp = 0;
             ++v_tl;
+            if (vb) ++ve1; else ++ve0;
           }
         }
       }
@@ -389,7 +400,7 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           }
           const uint32_t flags =
               (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
-          rowinfo[(ti & 3u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
+          rowinfo[(ti & 7u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
         }
         tc::fence_proxy_async();
         tc::named_bar_sync(3, 64);  // staging buffer sb free, A tile complete
@@ -403,14 +414,26 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
       // bracket, threshold, refine list) -- while the K* warps already work on the next tile.
       const int lq = warp & 3;
       const int row = 32 * lq + lane;
-      const uint32_t va = tbase + ((uint32_t)(32 * lq) << 16);
+      const uint32_t va0 = tbase + ((uint32_t)(32 * lq) << 16);
+      const FinishSeg fs = finish_seg(p, s);  // per-search values, once per segment
+      const int64_t row0s = p.m_off[s];
+      const float vun2 = m.vunscale2, sf2 = m.sf2, pmaxh = m.pmax_h, lrs = m.linv_rowsum;
+      const int nn = m.n;
       for (int tl = 0; tl < T; ++tl) {
         const uint32_t ti = gi + tl;
+        const uint32_t vb = dbl ? (ti & 1u) : 0u;
+        const uint32_t va = va0 + 128u * vb;
         // progressive drain: column block p of V is final once panel p's MMAs complete (each
-        // B_VB barrier completes once per tile, and the next tile cannot start before B_VE)
+        // barrier of the buffer's block group completes once per tile on that buffer, and the
+        // buffer's next tile cannot start before B_VE)
+        const bool trd = warp == 8 && lane == 0;
+        // the threshold read is issued before the V drain so its latency is hidden
+        const float thr = p.mode == kModeArgmax ? read_thr(p, s) : 0.f;
+        if (trd) trace_ev(p.trace, 16, 9, ti, trc);
         float vv = 0.f;
         for (int pb = 0; pb < npan; ++pb) {
-          tc::mbar_wait(bar(B_VB0 + pb), ti & 1u);
+          const uint32_t blk = vbq * vb + (uint32_t)pb;
+          tc::mbar_wait(bar(B_VB0 + blk), ((blk >= 4u) ? vb1c : vb0c) & 1u);
           tc::tc_fence_after();
           const int c = 32 * pb;
           if (c + 32 <= n16) {
@@ -437,27 +460,31 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_VE0));
+        if (lane == 0) tc::mbar_arrive(bar(B_VE0 + vb));
+        if (trd) trace_ev(p.trace, 17, 9, ti, trc);
+        if (!dbl || vb == 0) ++vb0c;
+        if (!dbl || vb == 1) ++vb1c;
         const uint32_t par = ti & 1u;
         tc::mbar_wait(bar(B_PF0 + par), (ti >> 1) & 1u);
         const double mu_t = part_mu[par * 128 + row] + part_mu[(2 + par) * 128 + row];
         const float a1_t = part_a1[par * 128 + row] + part_a1[(2 + par) * 128 + row];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_PE0 + par));
-        const float2 ri = rowinfo[(ti & 3u) * 128 + row];
+        if (trd) trace_ev(p.trace, 18, 9, ti, trc);
+        const float2 ri = rowinfo[(ti & 7u) * 128 + row];
         const uint32_t flags = __float_as_uint(ri.y);
         const int64_t rloc = (int64_t)(tile0 + tl) * 128 + row;
         const bool valid = (rloc < Ms) && !(flags & kFlagInvalid);
         const float u = 5.9604645e-8f;
-        const float s2 = vv * m.vunscale2;
-        const float sf2 = m.sf2;
+        const float s2 = vv * vun2;
         const float var = fmaxf(sf2 - s2, 0.f);
         // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for
         // the float16x3 augmented GEMM; margin x4
-        const float dmu = u * a1_t * (32.f * (ri.x + m.pmax_h) + 128.f);
-        const float dvar = 4.f * var_bound(u, sf2, s2, m.n, m.linv_rowsum);
-        finish_fast(p, s, valid, p.m_off[s], rloc, mu_t, dmu, var, dvar,
+        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f);
+        const float dvar = 4.f * var_bound(u, sf2, s2, nn, lrs);
+        finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
                     (flags & kFlagUnsafe) != 0u, 2, 128, 8);
+        if (trd) trace_ev(p.trace, 19, 9, ti, trc);
       }
     } else if (warp < 8) {
       // ===================================================== K* warps (0-7)
@@ -496,15 +523,32 @@ score_tc_kernel(const ScoreLaunch p, int total_tiles, int img_max, int kb_max, i
           if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
           ++ec;
         }
+        const uint32_t ks = gk % kKStages;
+#ifdef GPBO_KS_REORDER
+        // the K* stage is known free before the prefetch is issued, so the fence after the wait
+        // has no outstanding TMEM load of this thread to order against
+        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
+        tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
+#ifndef GPBO_KS_NOFENCE_KE
+        tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
+#endif
+        if (trw) trace_ev(p.trace, 7, warp, gk, trc);
+        if (g + 1 < P) {  // prefetch panel g+1
+          const int np = pp + 1 == npan ? 0 : pp + 1;
+          load_dist(np, ec, nx);
+        }
+#else
         if (g + 1 < P) {  // prefetch panel g+1
           const int np = pp + 1 == npan ? 0 : pp + 1;
           load_dist(np, ec, nx);
         }
         if (trw) trace_ev(p.trace, 6, warp, gk, trc);
-        const uint32_t ks = gk % kKStages;
         tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
+#ifndef GPBO_KS_NOFENCE_KE
         tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
+#endif
         if (trw) trace_ev(p.trace, 7, warp, gk, trc);
+#endif
         float muf = 0.f, a1f = 0.f;
         if (active) {
           float kv[16];
