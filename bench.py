@@ -267,10 +267,10 @@ def main():
     idx, ei = step_device()
     if rank == 0:
         peaks = load_peaks()
-        impl_used = "tcgen05" if ctx.last_impl == 2 else "cuda-core"
+        impl_used = {2: "tcgen05", 3: "tcgen05-stream"}.get(ctx.last_impl, "cuda-core")
         Fc = sum(flops_per_candidate(nn, dd) * x.shape[0] for nn, dd, x in zip(n, d, w.Xstar))
         achieved = Fc / (fast_ms / fast_n / 1e3) / 1e12  # TFLOP/s of the fast-phase kernel
-        if impl_used == "tcgen05":
+        if impl_used.startswith("tcgen05"):
             peak = peaks["bf16_sus"]
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": None,
@@ -292,7 +292,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": T_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f16x3+f32+f64" if impl_used == "tcgen05" else "f32+f64",
+            "dtype": "f16x3+f32+f64" if impl_used.startswith("tcgen05") else "f32+f64",
             "data": "synthetic",
             "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
                        "M_per_gpu": per_gpu, "M_global": M_total,

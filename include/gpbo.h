@@ -227,7 +227,8 @@ int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 /* Candidates the last ei_score_argmax call on ctx re-scored in the float64 refine phase
  * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
-/* Fast-phase implementation of the last scoring call: 1 = CUDA-core, 2 = tcgen05. */
+/* Fast-phase implementation of the last scoring call: 1 = CUDA-core, 2 = tcgen05 with the
+ * shared-memory-resident operand image, 3 = tcgen05 with streamed operands. */
 int gpbo_last_score_impl(const gpbo_ctx *ctx);
 
 /* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel
@@ -253,9 +254,12 @@ gpbo_status gpbo_tc_bench(const void *A, const void *B, float *D, int N, int K, 
  * (tag << 56 | role << 48 | panel) / clock pairs).  NULL disables. */
 gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf);
 
-/* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernel wherever its envelope
+/* Scoring implementation for this ctx: 0 = auto (the tcgen05 kernels wherever their envelope
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,
- * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP).  Diagnostic/testing. */
+ * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP), 3 = as 2, and models
+ * fitted while it is set use the streamed operand layout (the kernel for n > 256 / large d,
+ * forced on small searches for testing).  Models whose resident shared-memory image would not
+ * fit (n rounded to 16 > 256, or a large d) always use the streamed layout.  Diagnostic/testing. */
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl);
 
 /* Test hook: run only the fast phase of the scoring path on M device-resident candidates of

@@ -48,7 +48,8 @@ struct gpbo_ctx {
   int last_impl = 0;
   unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
-  int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05
+  int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05,
+                            // 3 = tcgen05 with the streamed image layout forced at fit time
 };
 
 struct gpbo_model {
@@ -235,13 +236,16 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   int32_t *h_tiles = (int32_t *)(h_best + S);
   // pick the implementation: tcgen05 when every search fits its envelope
   bool use_tc = ctx->score_impl != 1;
+  bool use_tcs = use_tc;  // the streamed tcgen05 kernel
   int nmax = 0, dmax = 0;
   for (int i = 0; i < S; ++i) {
     const SearchMeta &m = model->meta[s_first + i];
     nmax = std::max(nmax, m.n);
     dmax = std::max(dmax, m.d_pad);
     if (!gpbo::tc_supported(m)) use_tc = false;
+    if (!gpbo::tcs_supported(m)) use_tcs = false;
   }
+  if (use_tcs) use_tc = true;
   if (ctx->score_impl == 2 && !use_tc)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
   const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;
@@ -310,11 +314,14 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
   p.trace = ctx->trace;
   const int tiles = h_tiles[S];
-  ctx->last_impl = use_tc ? 2 : 1;
+  ctx->last_impl = use_tcs ? 3 : use_tc ? 2 : 1;
   if (tiles == 0) return GPBO_OK;
   {
     KernTimer t(ctx, kKernFast);
-    if (use_tc)
+    if (use_tcs)
+      CK(gpbo::launch_score_tcs(p, model->meta.data() + s_first, S, tiles, ctx->num_sms,
+                                ctx->stream));
+    else if (use_tc)
       CK(gpbo::launch_score_tc(p, model->meta.data() + s_first, S, tiles, ctx->num_sms,
                                ctx->stream));
     else
@@ -496,7 +503,7 @@ gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms
 }
 
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl) {
-  if (!ctx || impl < 0 || impl > 2) return GPBO_EINVAL;
+  if (!ctx || impl < 0 || impl > 3) return GPBO_EINVAL;
   ctx->score_impl = impl;
   return GPBO_OK;
 }
@@ -531,6 +538,13 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0, nscr = 0;
   int64_t nkt = 0;
   int smem_max = 0;
+  // tcgen05 image layout, uniform over the model: streamed (score_tcs.cu) when any search's
+  // resident image would not fit in shared memory, or when the ctx forces it (impl 3)
+  bool stream_layout = ctx->score_impl == 3;
+  for (int s = 0; s < S; ++s)
+    if (a->n[s] >= 1 && a->n[s] <= GPBO_MAX_N && a->d[s] >= 1 && a->d[s] <= GPBO_MAX_D &&
+        gpbo::tc_needs_stream(a->n[s], a->d[s]))
+      stream_layout = true;
   for (int s = 0; s < S; ++s) {
     const int n = a->n[s], d = a->d[s];
     if (n < 1 || n > GPBO_MAX_N || d < 1 || d > GPBO_MAX_D) {
@@ -551,8 +565,9 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     q.xs_off = nxs; nxs += (int64_t)q.n_pad * q.d_pad;
     q.lt_off = nlt; nlt += (int64_t)q.n_pad * q.n_pad;
     q.a_off = na; na += q.n_pad;
-    q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
+    q.tc_stream = stream_layout ? 1 : 0;
     gpbo::tc_fill_geometry(q);
+    q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
     q.kt_off = nkt; nkt += gpbo::fit_tile_doubles(n);

@@ -49,6 +49,7 @@ struct SearchMeta {
   double linv_absmax;   // max |(L^-1)_jk| (operand scaling of the tcgen05 image)
   // ---- tcgen05 fast phase (score_tc.cu); valid when tc_ok
   int32_t tc_ok;
+  int32_t tc_stream;    // streamed image layout (score_tcs.cu) instead of the resident one
   int32_t n16;          // n rounded up to 16 (V accumulator columns)
   int32_t kb;           // 16-wide K blocks of the augmented distance operand [x, |x|^2, 1]
   int32_t npan;         // 32-wide training-point panels

@@ -39,6 +39,7 @@
 #include "score_common.cuh"
 #include "score_tc.cuh"
 #include "tc_prims.cuh"
+#include "score_tc_helpers.cuh"
 
 namespace gpbo {
 
@@ -106,50 +107,6 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   s.bars = s.part_a1 + 4 * 128 * 4;
   s.total = s.bars + B_COUNT * 8 + 16 + 1024;  // + tmem slot, + alignment slack
   return s;
-}
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                       uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d)
-               : "memory");
-}
-
-__device__ __forceinline__ int search_of(const int32_t *tile_first, int S, int t) {
-  int lo = 0, hi = S;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (tile_first[mid] <= t) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-// optional event trace of CTA 0 (gpbo_debug_trace): each recording thread owns a slice of
-// 16384 entries (fire-and-forget stores, no atomics): slot = role slice + 2 * local count
-__device__ __forceinline__ void trace_ev(unsigned long long *tr, uint32_t tag, uint32_t role,
-                                         uint32_t idx, uint32_t &cnt) {
-#ifndef GPBO_TC_TRACE
-  return;  // compiled out unless built with -DGPBO_TC_TRACE (tools/trace_tc.py)
-#endif
-  if (tr == nullptr || blockIdx.x != 0) return;
-  const unsigned long long c = clock64();
-  const uint32_t slice = role == 11 ? 0u : role == 8 ? 1u : role == 0 ? 2u : role == 9 ? 4u : 3u;
-  if (2 * cnt + 2 < 16384) {
-    unsigned long long *b = tr + slice * 16384;
-    b[2 * cnt] = ((unsigned long long)tag << 56) | ((unsigned long long)role << 48) | idx;
-    b[2 * cnt + 1] = c;
-  }
-  ++cnt;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -646,6 +603,8 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
   if (!m.tc_ok || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
   const int n = m.n, d = m.d;
   const TcGeom g = tc_geom(n, d);
+  const TcsGeom gs = tcs_geom(n, d);
+  const bool stream = m.tc_stream != 0;
   unsigned char *img = img_all + m.img_off;
   const double *Li = Linv64 + m.mat_off;
   const double *X = Xs64 + m.x_off;
@@ -704,8 +663,40 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
       }
     }
     const int kblk = k >> 4;
-    unsigned char *hi = img + kblk * 2 * g.n16 * 32;
-    put(hi, hi + g.n16 * 32, tc::sw_offset(j, (k & 15) * 2, 32), v);
+    if (stream) {  // chunk-major: chunk q, K block, hi / lo blocks of 64 rows x 32 B
+      unsigned char *hi = img + (((j >> 6) * g.kb + kblk) * 2) * 2048;
+      put(hi, hi + 2048, tc::sw_offset(j & 63, (k & 15) * 2, 32), v);
+    } else {
+      unsigned char *hi = img + kblk * 2 * g.n16 * 32;
+      put(hi, hi + g.n16 * 32, tc::sw_offset(j, (k & 15) * 2, 32), v);
+    }
+  }
+  if (stream) {
+    // L^-1 slabs in the streamed kernel's consumption order (score_tc.cuh)
+    int off = gs.off_l;
+    for (int w = 0; w < gs.nw; ++w) {
+      for (int pp = 0; pp < tcs_window_panels(gs.n16, w); ++pp) {
+        const int R = tcs_slab_rows(gs.n16, w, pp);
+        const int r0 = tcs_window_end(gs.n16, w) - R;
+        unsigned char *hi = img + off;
+        for (int idx = t0; idx < R * 32; idx += tstep) {
+          const int r = idx >> 5, k = idx & 31;
+          const int j = r0 + r, kk = 32 * pp + k;
+          const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
+          put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
+        }
+        off += R * 128;
+      }
+    }
+    float2 *ap = reinterpret_cast<float2 *>(img + gs.off_a);
+    for (int j = t0; j < gs.n16; j += tstep) {
+      const double a = j < n ? alpha64[m.a_off + j] : 0.0;
+      ap[j] = make_float2((float)ldexp(a, -tK), (float)ldexp(fabs(a), -tK));
+    }
+    float *wp = reinterpret_cast<float *>(img + gs.off_w);
+    for (int c = t0; c < GPBO_MAX_D; c += tstep)
+      wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
+    return;
   }
   // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32)
   for (int pp = 0; pp < g.npan; ++pp) {
@@ -731,30 +722,53 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
 
 }  // namespace
 
-bool tc_supported(const SearchMeta &m) {
-  if (m.n16 > 256 || m.d + 2 > 64 || !m.tc_ok) return false;
-  const TcGeom g = tc_geom(m.n, m.d);
-  return tc_smem(g.img, g.kb, m.d).total <= kMaxSmem;
+static bool resident_fits(int n, int d) {
+  const TcGeom g = tc_geom(n, d);
+  if (g.n16 > 256 || d + 2 > 64) return false;
+  return tc_smem(g.img, g.kb, d).total <= kMaxSmem;
 }
+
+static bool stream_fits(int n, int d) {
+  const TcsGeom g = tcs_geom(n, d);
+  if (g.n16 > kTcsMaxN16 || d + 2 > 64) return false;
+  return tcs_smem_bytes(g.kb, d) <= kMaxSmem;
+}
+
+bool tc_supported(const SearchMeta &m) { return m.tc_ok && !m.tc_stream; }
+bool tcs_supported(const SearchMeta &m) { return m.tc_ok && m.tc_stream; }
 
 int64_t tc_image_bytes(const SearchMeta &m) {
-  const TcGeom g = tc_geom(m.n, m.d);
-  if (g.n16 > 256 || m.d + 2 > 64) return 0;
-  if (tc_smem(g.img, g.kb, m.d).total > kMaxSmem) return 0;
-  return g.img;
+  if (m.tc_stream) return stream_fits(m.n, m.d) ? tcs_geom(m.n, m.d).img : 0;
+  return resident_fits(m.n, m.d) ? tc_geom(m.n, m.d).img : 0;
 }
 
+// m.tc_stream on entry: 1 = streamed layout requested; it is also chosen when the resident
+// image does not fit.  (The caller makes the choice uniform over a model.)
 void tc_fill_geometry(SearchMeta &m) {
-  const TcGeom g = tc_geom(m.n, m.d);
-  m.n16 = g.n16;
-  m.kb = g.kb;
-  m.npan = g.npan;
-  m.img_bytes = g.img;
-  m.off_l = g.off_l;
-  m.off_a = g.off_a;
-  m.off_w = g.off_w;
+  if (!resident_fits(m.n, m.d)) m.tc_stream = 1;
+  if (m.tc_stream) {
+    const TcsGeom g = tcs_geom(m.n, m.d);
+    m.n16 = g.n16;
+    m.kb = g.kb;
+    m.npan = g.npan;
+    m.img_bytes = g.img;
+    m.off_l = g.off_l;
+    m.off_a = g.off_a;
+    m.off_w = g.off_w;
+  } else {
+    const TcGeom g = tc_geom(m.n, m.d);
+    m.n16 = g.n16;
+    m.kb = g.kb;
+    m.npan = g.npan;
+    m.img_bytes = g.img;
+    m.off_l = g.off_l;
+    m.off_a = g.off_a;
+    m.off_w = g.off_w;
+  }
   m.tc_ok = tc_image_bytes(m) > 0;
 }
+
+bool tc_needs_stream(int n, int d) { return !resident_fits(n, d); }
 
 cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64,
                            const double *Xs64, const double *alpha64, const float *ls32,

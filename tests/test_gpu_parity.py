@@ -28,7 +28,7 @@ def _fit(G, w):
     return ctx.fit(*H.pack(w), kernel=w.kernel)
 
 
-IMPLS = [0, 1]  # auto (tcgen05 where supported), CUDA-core
+IMPLS = [0, 1, 3]  # auto (tcgen05 where supported), CUDA-core, tcgen05 with streamed operands
 
 
 # ------------------------------------------------------------------ fit (H1-H4)
@@ -120,6 +120,15 @@ def test_posterior_matches_oracle(G, name, make, impl):
             res = gp.score(oms[s], w.Xstar[s])
             mu, var, ei = ctx.posterior(m, s, w.Xstar[s])
             H.check_T1(oms[s], res, mu, var, ei, f"{name}[{s}]")
+            # the implementation that ran: forced stream, or auto -> streamed tcgen05 whenever
+            # the resident image cannot hold the search (n16 > 256 or large d); d + 2 > 64 is
+            # outside both tcgen05 envelopes (CUDA-core kernel)
+            n, d = w.searches[s].X.shape
+            n16 = (n + 15) // 16 * 16
+            if d + 2 <= 64 and (impl == 3 or (impl == 0 and n16 > 256)):
+                assert ctx.last_impl == 3, (name, ctx.last_impl)
+            elif impl == 1:
+                assert ctx.last_impl == 1
     finally:
         ctx.set_score_impl(0)
 
