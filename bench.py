@@ -261,7 +261,8 @@ def main():
     T_dev, T_e2e = vmax(T_dev), vmax(T_e2e)
     fast_n, fast_ms = kt["fast"]
     fast_ms = vmax(fast_ms)
-    total_cands = M_total * args.steps
+    # every rank scores its local shard of every search (weak scaling): all candidates, all ranks
+    total_cands = local_cands * world * args.steps
     value = total_cands / (T_dev / 1e3)
     e2e_value = total_cands / (T_e2e / 1e3)
     idx, ei = step_device()
@@ -296,6 +297,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
                        "M_per_gpu": per_gpu, "M_global": M_total,
+                       "candidates_per_step": local_cands * world,
                        "kernel": "matern52" if w.kernel == 1 else "rbf",
                        "layout": args.layout, "l2": "flushed between steps (256 MiB write)",
                        "scoring": impl_used},

@@ -435,61 +435,68 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     }
     return;
   }
-  // ---- W now holds L^-1 (lower).  w = L^-1 y~, row abs sums and abs max (thread per row)
+  // ---- W now holds L^-1 (lower).  w = L^-1 y~ with the row abs sums and the abs max: warp
+  // per tile row, lane -> row gid of the tile, columns 2 tig + {0, 1} (one 16-byte load per lane
+  // and tile); the tiles go to the row-major L^-1 on the way (the refine phase, the tcgen05
+  // image and the CUDA-core operands read only k <= i).
   double rs = 0.0, lam = 0.0;
-  for (int i = tid; i < n; i += kFitThreads) {
+  for (int R = warp; R < nt; R += kWarps) {
+    const int i = 8 * R + gid;
     double a2 = 0.0, a3 = 0.0;
-    const int R = i >> 3;
+    double *dst = Linv64 + m.mat_off + (size_t)min(i, n - 1) * n;
     for (int C = 0; C <= R; ++C) {
-      const double *row = W + tb(R, C) + 8 * (i & 7);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int kk = 8 * C + q;
-        const double v = kk <= i ? row[q] : 0.0;
-        a2 = fma(v, yt[min(kk, n - 1)], a2);
-        a3 += fabs(v);
-        lam = fmax(lam, fabs(v));
-      }
+      const double2 v = *reinterpret_cast<const double2 *>(W + tb(R, C) + 2 * lane);
+      const int c0 = 8 * C + 2 * tig;
+      const bool in0 = i < n && c0 <= i, in1 = i < n && c0 + 1 <= i;
+      const double v0 = in0 ? v.x : 0.0, v1 = in1 ? v.y : 0.0;
+      a2 = fma(v0, yt[min(c0, n - 1)], a2);
+      a2 = fma(v1, yt[min(c0 + 1, n - 1)], a2);
+      a3 += fabs(v0) + fabs(v1);
+      lam = fmax(lam, fmax(fabs(v0), fabs(v1)));
+      if (in0) dst[c0] = v.x;
+      if (in1) dst[c0 + 1] = v.y;
     }
-    w[i] = a2;
+    a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, 1);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, 2);
+    if (tig == 0 && i < n) w[i] = a2;
     rs = fmax(rs, a3);
   }
   __syncthreads();
-  // alpha = L^-T w (thread per column k, down its tile column; two partial sums)
+  // alpha = L^-T w: warp per tile column, lane -> column pair 2 tig, rows gid of the tiles below
   double l1 = 0.0, amx = 0.0;
-  for (int kk = tid; kk < m.n_pad; kk += kFitThreads) {
-    double a2 = 0.0, a3 = 0.0;
-    if (kk < n) {
-      const int C = kk >> 3, c = kk & 7;
-      for (int R = C; R < nt; ++R) {
-        const double *col = W + tb(R, C) + c;
-#pragma unroll
-        for (int r = 0; r < 8; r += 2) {
-          const int i = 8 * R + r;
-          if (i >= kk && i < n) a2 = fma(col[8 * r], w[i], a2);
-          if (i + 1 >= kk && i + 1 < n) a3 = fma(col[8 * r + 8], w[i + 1], a3);
-        }
+  for (int C = warp; C < nt; C += kWarps) {
+    const int c0 = 8 * C + 2 * tig;
+    double s0 = 0.0, s1 = 0.0;
+    for (int R = C; R < nt; ++R) {
+      const int i = 8 * R + gid;
+      if (i < n) {
+        const double2 v = *reinterpret_cast<const double2 *>(W + tb(R, C) + 2 * lane);
+        const double wi = w[i];
+        if (c0 <= i) s0 = fma(v.x, wi, s0);
+        if (c0 + 1 <= i) s1 = fma(v.y, wi, s1);
       }
     }
-    a2 += a3;
-    alpha64[m.a_off + kk] = a2;
-    l1 += fabs(a2);
-    amx = fmax(amx, fabs(a2));
-  }
-  // L^-1, lower part, ROW-major (element (i, k) at i n + k; the refine phase, the tcgen05 image
-  // and the CUDA-core operands read only k <= i): warp per tile, lane -> row r = lane / 4,
-  // columns 2 (lane % 4) + {0, 1}
-  for (int e = warp; e < ntiles; e += kWarps) {
-    int R, C;
-    tile_rc(e, R, C);
-    const int i = 8 * R + gid, c0 = 8 * C + 2 * tig;
-    if (i < n) {
-      const double2 v = *reinterpret_cast<const double2 *>(W + tb(R, C) + 2 * lane);
-      double *dst = Linv64 + m.mat_off + (size_t)i * n + c0;
-      if (c0 <= i) dst[0] = v.x;
-      if (c0 + 1 <= i) dst[1] = v.y;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (gid == 0) {
+      if (c0 < n) {
+        alpha64[m.a_off + c0] = s0;
+        l1 += fabs(s0);
+        amx = fmax(amx, fabs(s0));
+      }
+      if (c0 + 1 < n) {
+        alpha64[m.a_off + c0 + 1] = s1;
+        l1 += fabs(s1);
+        amx = fmax(amx, fabs(s1));
+      }
     }
   }
+  for (int kk = n + tid; kk < m.n_pad; kk += kFitThreads) alpha64[m.a_off + kk] = 0.0;
   // the four statistics in one block reduction
   {
     double v[4] = {l1, amx, rs, lam};
