@@ -140,8 +140,8 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   double *Mm = piv + 24;               // the block maps M, N, R (8 x 8 each, row-major)
   double *Nm = Mm + 64;
   double *Rm = Nm + 64;
-  double *G = Rm + 64;                 // G[u][.], 8 rows of gs
-  double *W = kSmem ? G + 8 * gs : Wscr64 + m.scr_off;
+  double *G = Rm + 64;                 // G[u][.], 2 x 8 rows of gs (a pair of panels)
+  double *W = kSmem ? G + 16 * gs : Wscr64 + m.scr_off;
   // element (i, k), i >= k
   auto at = [&](int i, int k) -> int { return tb(i >> 3, k >> 3) + 8 * (i & 7) + (k & 7); };
   double *Lg = L64 + m.mat_off;        // L, col-major (lower part; export zeroes the rest)
@@ -312,87 +312,160 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     __syncthreads();
     FIT_T(2);
     bool ok = piv[16] == 0.0;
-    for (int J = 0; J < n && ok; J += kFitB) {
-      const int Jb = min(J + kFitB, n), bb = Jb - J, JT = J >> 3;
-      // -- C: rows below the block (tile rows R > JT: [x N | x M]) and columns left of it (tile
-      // columns C < JT: R w), on DMMA
-      {
-        const int nrt = nt - JT - 1;
-        for (int it = warp; it < nrt + JT; it += kWarps) {
-          double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-          if (it < nrt) {
-            const int R = JT + 1 + it, i = 8 * R + gid;
-            double *Wt = W + tb(R, JT);
+    // Global working matrix: panels are processed in pairs (blocks JT, JT + 1) so the bulk of the
+    // trailing update is ONE
+    // pass over W with K = 16 (both panels' G), halving the W tile traffic (the T phase is
+    // shared-memory bound):
+    //   C(JT)  -> G1;  partial T: G1 into tile column JT + 1 (rows below it) and tile row JT + 1
+    //   (columns left of JT) -- exactly what D(JT + 1) and C(JT + 1) read; the D warp updates the
+    //   diagonal tile JT + 1 and runs D(JT + 1) meanwhile;
+    //   C(JT + 1) -> G2;  combined T over rows R > JT + 1: columns C < JT and JT + 1 < C <= R get
+    //   G1 and G2, column JT gets G2 only (G1 skips its own block column), column JT + 1 nothing
+    //   more (G1 was applied, G2 skips it); the D warp updates diagonal tile JT + 2 and runs D.
+    // A ragged single last block has no trailing update.
+    double *G1 = G, *G2 = G + 8 * gs;
+    // -- C: rows below block JT (tile rows R > JT: [x N | x M]) and columns left of it (tile
+    // columns C < JT: R w), on DMMA; the block's G rows go to Gc
+    auto cphase = [&](int JT, double *Gc) {
+      const int J = 8 * JT, bb = min(kFitB, n - J);
+      const int nrt = nt - JT - 1;
+      for (int it = warp; it < nrt + JT; it += kWarps) {
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+        if (it < nrt) {
+          const int R = JT + 1 + it, i = 8 * R + gid;
+          double *Wt = W + tb(R, JT);
 #pragma unroll
-            for (int kk = 0; kk < 8; kk += 4) {
-              const double a = Wt[8 * gid + kk + tig];
-              dmma(d0, d1, a, Nm[(kk + tig) * 8 + gid]);
-              dmma(e0, e1, a, Mm[(kk + tig) * 8 + gid]);
-            }
-            const int u = 2 * tig;
-            G[u * gs + i] = d0;
-            G[(u + 1) * gs + i] = d1;
-            if (i < n) {
-              Lg[(size_t)(J + u) * n + i] = d0;
-              Lg[(size_t)(J + u + 1) * n + i] = d1;
-            }
-            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
-          } else {
-            const int C = it - nrt;
-            double *Wt = W + tb(JT, C);
+          for (int kk = 0; kk < 8; kk += 4) {
+            const double a = Wt[8 * gid + kk + tig];
+            dmma(d0, d1, a, Nm[(kk + tig) * 8 + gid]);
+            dmma(e0, e1, a, Mm[(kk + tig) * 8 + gid]);
+          }
+          const int u = 2 * tig;
+          Gc[u * gs + i] = d0;
+          Gc[(u + 1) * gs + i] = d1;
+          if (i < n) {
+            Lg[(size_t)(J + u) * n + i] = d0;
+            Lg[(size_t)(J + u + 1) * n + i] = d1;
+          }
+          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
+        } else {
+          const int C = it - nrt;
+          double *Wt = W + tb(JT, C);
 #pragma unroll
-            for (int kk = 0; kk < 8; kk += 4) {
-              const int mrow = kk + tig;
-              const double b = mrow < bb ? Wt[8 * mrow + gid] : 0.0;
-              dmma(d0, d1, Rm[gid * 8 + mrow], b);
+          for (int kk = 0; kk < 8; kk += 4) {
+            const int mrow = kk + tig;
+            const double b = mrow < bb ? Wt[8 * mrow + gid] : 0.0;
+            dmma(d0, d1, Rm[gid * 8 + mrow], b);
+          }
+          const int kc = 8 * C + 2 * tig;
+          Gc[gid * gs + kc] = d0;
+          Gc[gid * gs + kc + 1] = d1;
+          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
+        }
+      }
+    };
+    // W(R, C0 + q) -= sum over the given G buffers of G[u][i] G[u][k], q < cnt (<= 4 tiles of
+    // one tile row sharing the A fragments); nb = 1 (Ga) or 2 (Ga and Gb, K = 16)
+    auto quad = [&](const double *Ga, const double *Gb, int R, int C0, int cnt) {
+      const int i = 8 * R + gid;
+      double *Wt = W + tb(R, C0) + 2 * lane;
+      double2 c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < cnt) c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double *Gh = h == 0 ? Ga : Gb;
+        if (Gh == nullptr) continue;
+        const double a0 = -Gh[tig * gs + i], a1 = -Gh[(4 + tig) * gs + i];
+        const double *g0 = Gh + tig * gs + 8 * C0 + gid, *g1 = g0 + 4 * gs;
+        double b0[4], b1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < cnt) { b0[q] = g0[8 * q]; b1[q] = g1[8 * q]; }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < cnt) dmma(c[q].x, c[q].y, a0, b0[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < cnt) dmma(c[q].x, c[q].y, a1, b1[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
+    };
+    constexpr int kT = kWarps - 1;  // T warps (the highest warp is the D warp)
+    // The working matrix in shared memory: one panel per step, the trailing update overlapping
+    // the next block's D (D's latency is hidden behind a full T pass; measured faster than
+    // pairs at n = 200).  In global memory (n > kFitSmemMaxN, L2 traffic bound): pairs.
+    for (int JT = 0; kSmem && JT < nt && ok; ++JT) {
+      cphase(JT, G1);
+      __syncthreads();
+      FIT_T(3);
+      if (JT + 1 == nt) break;
+      const int nrt = nt - JT - 1, nlq = (JT + 3) / 4;
+      if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D
+        quad(G1, nullptr, JT + 1, JT + 1, 1);
+        __syncwarp();
+        diag_block(8 * (JT + 1));
+      } else {
+        // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
+        // (row 0's right quad is the diagonal tile -- the D warp's), round robin, rotated
+        for (int r = 0, w0 = 0; r < nrt; ++r, w0 = (w0 + 5) % kT) {
+          const int R = JT + 1 + r, len = nlq + (r >> 2) + (r > 0 ? 1 : 0);
+          for (int q = (warp - w0 + kT) % kT; q < len; q += kT) {
+            if (q < nlq) {
+              quad(G1, nullptr, R, 4 * q, min(4, JT - 4 * q));
+            } else {
+              const int c0 = 4 * (q - nlq);
+              quad(G1, nullptr, R, JT + 1 + c0, min(4, r + 1 - c0));
             }
-            const int kc = 8 * C + 2 * tig;
-            G[gid * gs + kc] = d0;
-            G[gid * gs + kc + 1] = d1;
-            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
           }
         }
       }
       __syncthreads();
+      FIT_T(4);
+      ok = piv[16] == 0.0;  // the next block's D (uniform)
+    }
+    for (int JT = 0; !kSmem && JT < nt && ok;) {
+      const bool pair = JT + 1 < nt;
+      cphase(JT, G1);
+      __syncthreads();
       FIT_T(3);
-      // -- T: W(i, k) -= sum_u G[u][i] G[u][k]: tile rows R > JT, tile columns C < JT and
-      // JT < C <= R; items of up to 4 consecutive tiles of one tile row share the A fragments
-      if (Jb < n) {
-        auto quad = [&](int R, int C0, int cnt) {
-          const int i = 8 * R + gid;
-          const double a0 = -G[tig * gs + i], a1 = -G[(4 + tig) * gs + i];
-          double *Wt = W + tb(R, C0) + 2 * lane;
-          const double *g0 = G + tig * gs + 8 * C0 + gid, *g1 = g0 + 4 * gs;
-          // all operands first (the stores below would otherwise fence the next tile's loads)
-          double2 c[4];
-          double b0[4], b1[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < cnt) {
-              c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
-              b0[q] = g0[8 * q];
-              b1[q] = g1[8 * q];
-            }
+      if (!pair) { ++JT; break; }
+      // -- partial T(JT) with G1: tile column JT + 1 below its diagonal, tile row JT + 1 left of
+      // JT; the D warp: the diagonal tile JT + 1, then D(JT + 1)
+      {
+        const int nlq = (JT + 3) / 4, ncol = nt - JT - 2;
+        if (warp == kWarps - 1) {
+          quad(G1, nullptr, JT + 1, JT + 1, 1);
+          __syncwarp();
+          diag_block(8 * (JT + 1));
+        } else {
+          for (int q = warp; q < ncol + nlq; q += kT) {
+            if (q < ncol) quad(G1, nullptr, JT + 2 + q, JT + 1, 1);
+            else quad(G1, nullptr, JT + 1, 4 * (q - ncol), min(4, JT - 4 * (q - ncol)));
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < cnt) dmma(c[q].x, c[q].y, a0, b0[q]);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < cnt) dmma(c[q].x, c[q].y, a1, b1[q]);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
-        };
-        const int nrt = nt - JT - 1, nlq = (JT + 3) / 4;
-        if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D (the
-          // highest warp id: the schedulers favour it while the other warps run T)
-          quad(JT + 1, JT + 1, 1);
+        }
+      }
+      __syncthreads();
+      FIT_T(4);
+      ok = piv[16] == 0.0;
+      if (!ok) break;
+      cphase(JT + 1, G2);
+      __syncthreads();
+      FIT_T(3);
+      // -- combined T over tile rows R > JT + 1
+      const int R0 = JT + 2;
+      if (R0 < nt) {
+        const int nrt = nt - R0, nlq = (JT + 3) / 4;
+        if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D
+          quad(G1, G2, R0, R0, 1);
           __syncwarp();
 #ifdef GPBO_FIT_TIMING
           const long long td0 = clock64();
 #endif
-          diag_block(Jb);
+          diag_block(8 * R0);
 #ifdef GPBO_FIT_TIMING
           if (blockIdx.x == 0 && lane == 0) fit_tD += clock64() - td0;
 #endif
@@ -400,18 +473,19 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
 #ifdef GPBO_FIT_TIMING
           const long long tw0 = clock64();
 #endif
-          // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
-          // (row 0's right quad is the diagonal tile -- the D warp's).  Row r's items go to the
-          // kWarps - 1 T warps round robin, starting at warp (5 r) mod (kWarps - 1).
-          constexpr int kT = kWarps - 1;
+          // items of tile row r (R = R0 + r): nlq left quads (G1 + G2), the column-JT tile
+          // (G2 only), then r / 4 + 1 right quads from column R0 (row 0's is the diagonal tile:
+          // the D warp's).  Round robin over the T warps, rotated per row.
           for (int r = 0, w0 = 0; r < nrt; ++r, w0 = (w0 + 5) % kT) {
-            const int R = JT + 1 + r, len = nlq + (r >> 2) + (r > 0 ? 1 : 0);
+            const int R = R0 + r, len = nlq + 1 + (r >> 2) + (r > 0 ? 1 : 0);
             for (int q = (warp - w0 + kT) % kT; q < len; q += kT) {
               if (q < nlq) {
-                quad(R, 4 * q, min(4, JT - 4 * q));
+                quad(G1, G2, R, 4 * q, min(4, JT - 4 * q));
+              } else if (q == nlq) {
+                quad(G2, nullptr, R, JT, 1);
               } else {
-                const int c0 = 4 * (q - nlq);
-                quad(R, JT + 1 + c0, min(4, r + 1 - c0));
+                const int c0 = 4 * (q - nlq - 1);
+                quad(G1, G2, R, R0 + c0, min(4, r + 1 - c0));
               }
             }
           }
@@ -419,10 +493,11 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
           if (blockIdx.x == 0 && threadIdx.x == 0) fit_tw += clock64() - tw0;
 #endif
         }
+        __syncthreads();
+        FIT_T(4);
+        ok = piv[16] == 0.0;  // the next block's D (uniform)
       }
-      __syncthreads();
-      FIT_T(4);
-      ok = piv[16] == 0.0;  // the next block's D (uniform)
+      JT += 2;
     }
     if (ok) jk = k;
   }

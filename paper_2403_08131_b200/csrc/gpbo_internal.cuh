@@ -11,7 +11,8 @@ namespace gpbo {
 constexpr int kFitThreads = 384;
 constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
 // Panel width of the fit's blocked factorisation (fit.cu) and its shared-memory plan:
-// y~, w (n-vectors), spare/flags, the block maps M, N, R, 8 panel rows G of stride gs, and -- for
+// y~, w (n-vectors), spare/flags, the block maps M, N, R, 2 x 8 panel rows G of stride gs (a
+// pair of panels), and -- for
 // n <= kFitSmemMaxN -- the working matrix as the lower triangle of 8 x 8 tiles, each row-major
 // (27 * 28 / 2 tiles * 512 B = 189 KB at n = 216).
 constexpr int kFitB = 8;
@@ -24,7 +25,7 @@ __host__ __device__ constexpr int fit_tile_doubles(int n) {
   return ((n + 7) / 8) * ((n + 7) / 8 + 1) / 2 * 64;
 }
 __host__ __device__ constexpr int fit_smem_doubles(int n, bool in_smem) {
-  return 2 * fit_nr8(n) + 24 + 3 * 64 + 8 * fit_gstride(n) + (in_smem ? fit_tile_doubles(n) : 0);
+  return 2 * fit_nr8(n) + 24 + 3 * 64 + 16 * fit_gstride(n) + (in_smem ? fit_tile_doubles(n) : 0);
 }
 
 // Per-search state of a fitted model (device copy in gpbo_model::meta_d, host copy in meta_h).
