@@ -38,6 +38,29 @@ def flops_per_candidate(n, d):
     return 2 * n * d + n * (n + 1) + 4 * n
 
 
+def profiled_traffic(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes per launch) of `kernel` from the latest
+    committed ncu --set full summary under profiles/ taken on the same bench config, else None."""
+    import glob
+    want = "--config 4" if config == 4 else ""
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{kernel}_summary.txt"))):
+        lines = open(f).read().splitlines()
+        if not lines or ("--config" in lines[0]) != bool(want) or (want and want not in lines[0]):
+            continue
+        if config not in (2, 4):
+            continue
+        vals = {}
+        for ln in lines:
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if ln.startswith(key + ":"):
+                    vals[key] = float(ln.split(":")[1])
+        if len(vals) == 2:  # ncu reports MB
+            best = ((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) * 1e6,
+                    os.path.relpath(f, ROOT))
+    return best
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -273,8 +296,12 @@ def main():
         achieved = Fc / (fast_ms / fast_n / 1e3) / 1e12  # TFLOP/s of the fast-phase kernel
         if impl_used.startswith("tcgen05"):
             peak = peaks["bf16_sus"]
+            tr = profiled_traffic("score_tcs" if impl_used == "tcgen05-stream" else "score_tc",
+                                  args.config)
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
+                    "frac": achieved / peak, "traffic": tr[0] if tr else None,
+                    "traffic_src": tr[1] if tr else None,
+                    "algorithmic_bytes": int(sum(4 * dd * x.shape[0] for dd, x in zip(d, w.Xstar))),
                     "peak_src": f"{peaks['src']} bf16 dense sustained (fp16 same rate)"}
         else:
             peak = 148 * 128 * 2 * peaks["sm_mhz"] * 1e6 / 1e12
