@@ -48,6 +48,10 @@ struct gpbo_ctx {
   int last_impl = 0;
   unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
+  // chunked host feed of ei_score_argmax (mem = GPBO_HOST): candidate chunks are copied on
+  // copy_stream while the tcgen05 kernel scores the previous chunk on `stream`
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t feed_ev[8] = {};
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05,
                             // 3 = tcgen05 with the streamed image layout forced at fit time
 };
@@ -218,9 +222,13 @@ struct Outputs {
 
 // Shared scoring launch used by gp_posterior and ei_score_argmax: the fast phase (tcgen05 or
 // CUDA-core kernel) followed by the float64 refine phase.
+// host_src (optional): the caller's host copy of the candidates; Xstar_dev is then the device
+// staging buffer they are copied into, here -- in chunks overlapped with the scoring of the
+// previous chunk when the tcgen05 kernels run, else in one copy.
 gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S,
                       const float *Xstar_dev, const int64_t *m_off, const int64_t *m_base,
-                      const double *best_std, int mode, const Outputs &out) {
+                      const double *best_std, int mode, const Outputs &out,
+                      const float *host_src = nullptr) {
   // aux layout: m_off[S+1] i64 | m_base[S] i64 | x_off[S] i64 | best[S] f64 | tile_first[S+1] i32
   const size_t bytes = (size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4;
   gpbo_status st = ensure_aux(ctx, bytes + 64);
@@ -315,19 +323,48 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.trace = ctx->trace;
   const int tiles = h_tiles[S];
   ctx->last_impl = use_tcs ? 3 : use_tc ? 2 : 1;
+  const int64_t floats_all = xo;
+  // element offset in X* of the first row of tile t (tile indices of this call)
+  auto tile_elem = [&](int t) -> int64_t {
+    if (t >= tiles) return floats_all;
+    int i = (int)(std::upper_bound(h_tiles, h_tiles + S + 1, t) - h_tiles) - 1;
+    return h_xoff[i] + (int64_t)(t - h_tiles[i]) * tile * model->meta[s_first + i].d;
+  };
+  const int nchunk = (host_src && use_tc) ? std::max(1, std::min(8, tiles / 1024)) : 1;
+  if (host_src && nchunk <= 1 && floats_all > 0)
+    CK(cudaMemcpyAsync(const_cast<float *>(Xstar_dev), host_src, (size_t)floats_all * 4,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  if (nchunk > 1 && !ctx->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto &e : ctx->feed_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   if (tiles == 0) return GPBO_OK;
-  {
+  for (int c = 0; c < nchunk; ++c) {
+    const int ta = (int)((int64_t)tiles * c / nchunk), tb = (int)((int64_t)tiles * (c + 1) / nchunk);
+    if (nchunk > 1) {
+      // chunk c's rows: from its first tile's row to the next chunk's (the last chunk: to the end)
+      const int64_t e0 = c == 0 ? 0 : tile_elem(ta), e1 = tile_elem(tb);
+      if (c == 0) {  // the copies may only start once earlier work on the stream is done
+        CK(cudaEventRecord(ctx->feed_ev[0], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->feed_ev[0], 0));
+      }
+      if (e1 > e0)
+        CK(cudaMemcpyAsync(const_cast<float *>(Xstar_dev) + e0, host_src + e0,
+                           (size_t)(e1 - e0) * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+      CK(cudaEventRecord(ctx->feed_ev[c], ctx->copy_stream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->feed_ev[c], 0));
+    }
     KernTimer t(ctx, kKernFast);
     if (use_tcs)
-      CK(gpbo::launch_score_tcs(p, model->meta.data() + s_first, S, tiles, ctx->num_sms,
+      CK(gpbo::launch_score_tcs(p, model->meta.data() + s_first, S, ta, tb - ta, ctx->num_sms,
                                 ctx->stream));
     else if (use_tc)
-      CK(gpbo::launch_score_tc(p, model->meta.data() + s_first, S, tiles, ctx->num_sms,
+      CK(gpbo::launch_score_tc(p, model->meta.data() + s_first, S, ta, tb - ta, ctx->num_sms,
                                ctx->stream));
     else
       CK(gpbo::launch_score_simt(p, tiles, dmax, nmax, ctx->stream));
+    ctx->launches += 1;
   }
-  ctx->launches += 1;
   if (mode == gpbo::kModeDebug) return GPBO_OK;
   gpbo::RefineLaunch r{};
   r.meta = p.meta;
@@ -360,10 +397,10 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
 // Fast phase + refine + cross-rank max + decode (shared by ei_score_argmax / bo_suggest_batch).
 gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
                         const int64_t *m_off, const int64_t *m_base, const double *best_std,
-                        int64_t *idx, float *ei) {
+                        int64_t *idx, float *ei, const float *host_src = nullptr) {
   const int S = model->S;
   gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_base, best_std, gpbo::kModeArgmax,
-                             Outputs());
+                             Outputs(), host_src);
   if (st) return st;
   if (ctx->nranks > 1)
     NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
@@ -455,6 +492,12 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (auto &e : ctx->feed_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->stage_d) cudaFree(ctx->stage_d);
   if (ctx->aux_d) cudaFree(ctx->aux_d);
   if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
@@ -835,15 +878,16 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
   }
   if (rows > 0 && !Xstar) return fail(ctx, GPBO_EINVAL, "null Xstar");
   // rows of search s start at element sum_{t<s} (m_off[t+1] - m_off[t]) d_t of Xstar
-  const float *xd = Xstar;
+  // host candidates: copied into the staging buffer by run_score (chunked, overlapped with the
+  // scoring of the previous chunk)
+  const float *xd = Xstar, *host_src = nullptr;
   if (mem == GPBO_HOST && floats > 0) {
     gpbo_status st = ensure_stage(ctx, (size_t)floats * 4);
     if (st) return st;
-    CK(cudaMemcpyAsync(ctx->stage_d, xd, (size_t)floats * 4, cudaMemcpyHostToDevice,
-                       ctx->stream));
+    host_src = Xstar;
     xd = (const float *)ctx->stage_d;
   }
-  return argmax_tail(ctx, model, xd, m_off, m_global_base, best_std.data(), idx, ei);
+  return argmax_tail(ctx, model, xd, m_off, m_global_base, best_std.data(), idx, ei, host_src);
 }
 
 gpbo_status gpbo_space_sample(gpbo_ctx *ctx, const gpbo_space *space, uint64_t seed,

@@ -69,9 +69,10 @@ int64_t tc_image_bytes(const SearchMeta &m);
 cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64,
                            const double *Xs64, const double *alpha64, const float *ls32,
                            unsigned char *img, cudaStream_t stream);
-cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int S,
+// Tiles [tile_lo, tile_lo + total_tiles) of the call (tile indices as in p.tile_first).
+cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int S, int tile_lo,
                             int total_tiles, int num_sms, cudaStream_t stream);
-cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int S,
+cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int S, int tile_lo,
                              int total_tiles, int num_sms, cudaStream_t stream);
 int tcs_smem_bytes(int kb_max, int d_max);
 // true when the resident image of an (n, d) search does not fit in shared memory

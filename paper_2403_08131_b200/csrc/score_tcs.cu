@@ -80,7 +80,7 @@ __host__ __device__ inline TcsSmem tcs_smem(int kb_max, int d_max) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-score_tcs_kernel(const ScoreLaunch p, int total_tiles, int kb_max, int d_max) {
+score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, int d_max) {
   extern __shared__ unsigned char sm_raw[];
   unsigned char *sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
   const TcsSmem L = tcs_smem(kb_max, d_max);
@@ -97,8 +97,9 @@ score_tcs_kernel(const ScoreLaunch p, int total_tiles, int kb_max, int d_max) {
   auto bar = [&](int i) { return tc::smem_u32(bars + i); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = (int)((long long)total_tiles * blockIdx.x / gridDim.x);
-  const int t1 = (int)((long long)total_tiles * (blockIdx.x + 1) / gridDim.x);
+  // this launch covers tiles [tile_lo, tile_lo + total_tiles) of the call (chunked host feeds)
+  const int t0 = tile_lo + (int)((long long)total_tiles * blockIdx.x / gridDim.x);
+  const int t1 = tile_lo + (int)((long long)total_tiles * (blockIdx.x + 1) / gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -547,7 +548,8 @@ score_tcs_kernel(const ScoreLaunch p, int total_tiles, int kb_max, int d_max) {
 int tcs_smem_bytes(int kb_max, int d_max) { return tcs_smem(kb_max, d_max).total; }
 
 cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int S,
-                             int total_tiles, int num_sms, cudaStream_t stream) {
+                             int tile_lo, int total_tiles, int num_sms,
+                            cudaStream_t stream) {
   int kb_max = 1, d_max = 1;
   for (int i = 0; i < S; ++i) {
     kb_max = std::max(kb_max, meta_h[i].kb);
@@ -559,7 +561,7 @@ cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int grid = std::min(num_sms, total_tiles);
-  score_tcs_kernel<<<grid, kThreads, smem, stream>>>(p, total_tiles, kb_max, d_max);
+  score_tcs_kernel<<<grid, kThreads, smem, stream>>>(p, tile_lo, total_tiles, kb_max, d_max);
   return cudaGetLastError();
 }
 

@@ -210,6 +210,30 @@ def test_device_and_host_memory_agree(G):
     assert np.array_equal(mu_h, mu_d.cpu().numpy()) and np.array_equal(ei_h, ei_d.cpu().numpy())
 
 
+@pytest.mark.parametrize("case", ["cfg2", "cfg3", "cfg4"])
+def test_chunked_host_feed_matches_device(G, case):
+    """Host candidates large enough for the chunked feed (>= 2048 tiles: copies of chunk c + 1
+    overlap the scoring of chunk c, one launch per chunk) give bit-identical keys to the
+    device-resident single launch -- including chunk boundaries inside a search and between
+    searches of a ragged batch, and the streamed kernel (cfg4)."""
+    import torch
+    gpbo, ctx = G
+    w = {"cfg2": lambda: gen.make(2, M=1 << 19),
+         "cfg3": lambda: gen.random_case(31, [100, 60, 100, 37], [5, 5, 7, 5],
+                                         [70001, 1, 131072, 99999]),
+         "cfg4": lambda: gen.make(4, M=300000)}[case]()
+    n, d, X, y, ls, sf2, sn2 = H.pack(w)
+    m = ctx.fit(n, d, X, y, ls, sf2, sn2, kernel=w.kernel)
+    Xs, off = H.pack_candidates(w)
+    Xp = torch.from_numpy(Xs).pin_memory()
+    ih, eh = ctx.score_argmax(m, Xp, off)
+    impl_h = ctx.last_impl
+    idv, edv = ctx.score_argmax(m, torch.from_numpy(Xs).cuda(), off)
+    assert impl_h == ctx.last_impl and impl_h in (2, 3)
+    assert np.array_equal(ih, idv) and np.array_equal(eh, edv), (ih, idv, eh, edv)
+    m.free()
+
+
 def test_nan_candidate_is_never_chosen(G):
     gpbo, ctx = G
     w = gen.random_case(12, 20, 3, 256)
