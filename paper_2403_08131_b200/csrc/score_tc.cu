@@ -50,10 +50,14 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
 constexpr int kDepth = 2;           // 64-column distance scratch stages (TMEM), issued ahead
-constexpr int kKStages = 4;         // K* operand stages (TMEM)
+constexpr int kKStages = 2;         // K* operand stages (TMEM), one 64-wide panel each
 // TMEM columns: V accumulator [0, n16 <= 256), distance scratch 2 x 64 [256, 384), K* operand
-// stages 4 x 32 [384, 512) (per stage: hi k-steps 0/1 at +0/+8, lo at +16/+24; lane = row, one
-// column packs the fp16 pair k = 2c, 2c+1).
+// stages 2 x 64 [384, 512) (per stage: hi k-steps 0..3 at +0/+8/+16/+24, lo at +32..+56;
+// lane = row, one column packs the fp16 pair k = 2c, 2c+1).  A K* panel is 64 training points
+// wide (= one distance chunk): every TMEM round trip of the K* warps (distance load, K* store,
+// their waits and barrier handoffs) is paid once per 64 points -- those latencies, not the
+// MUFU or tensor pipes, bound the kernel (timing experiments without MUFU work / without 2/3
+// of the MMAs: -7 % / -4 %).
 constexpr uint32_t kScratch0 = 256;
 constexpr uint32_t kKstar0 = 384;
 
@@ -186,7 +190,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     const bool dbl = n16 <= 128;
     const uint32_t vbq = dbl ? 4u : 8u;
     const int T = tb - ta;
-    const int P = T * npan;
+    const int P64 = (n16 + 63) / 64;  // 64-wide K* panels per tile
+    const int P = T * P64;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
     const int tile0 = ta - p.tile_first[s];  // local index of the segment's first tile
 
@@ -248,28 +253,32 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
             tc::mbar_wait(bar(B_VE0 + vb), ((vb ? ve1 : ve0) & 1u) ^ 1u);
             tc::tc_fence_after();
           }
-          const uint32_t kt = tbase + kKstar0 + 32u * ks;  // K* stage in TMEM
-          const uint32_t R16 = (uint32_t)(n16 - 32 * v_pp) * 4u;  // R * 64 B >> 4: hi -> lo
-          const uint32_t lp = l0 + (uint32_t)(v_pp * n16 - 16 * v_pp * (v_pp - 1)) * 8u;
+          const uint32_t kt = tbase + kKstar0 + 64u * ks;  // K* stage in TMEM
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j0 = 32 * v_pp + 16 * h;
+          for (int sk = 0; sk < 4; ++sk) {  // 16-wide k steps of the 64-wide panel
+            const int j0 = 64 * v_pp + 16 * sk;
             if (j0 < n16) {
+              const int pp = 2 * v_pp + (sk >> 1), h = sk & 1;  // 32-wide L^-1 panel, its k step
+              const uint32_t R16 = (uint32_t)(n16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
+              const uint32_t lp = l0 + (uint32_t)(pp * n16 - 16 * pp * (pp - 1)) * 8u;
               const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
               const uint32_t dt = tbase + 128u * vb + (uint32_t)j0;
-              const uint32_t ka = kt + 8u * h;         // k step h: hi at +8h, lo at +16 + 8h
-              const uint32_t lb = lp + 66u * h;        // +1024 B rows, +32 B k-advance
-              tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | h) ? 1u : 0u);
+              const uint32_t ka = kt + 8u * sk;       // k step sk: hi at +8 sk, lo at +32 + 8 sk
+              const uint32_t lb = lp + 66u * h;       // +1024 B rows, +32 B k-advance
+              tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | sk) ? 1u : 0u);
+#ifndef GPBO_EXP_NOVMMA
               tc::mma_f16_ts(dt, ka, lb + R16, H64, idn, 1u);
-              tc::mma_f16_ts(dt, ka + 16u, lb, H64, idn, 1u);
+              tc::mma_f16_ts(dt, ka + 32u, lb, H64, idn, 1u);
+#endif
             }
           }
           tc::mma_commit_warp(bar(B_KE0 + ks));
-          // V columns [32 p, 32 p + 32) receive no later contribution: the drain may read them
-          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
+          // V columns [64 q, 64 q + 64) receive no later contribution: the drain may read them
+          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + 2 * v_pp));
+          if (2 * v_pp + 1 < npan) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + 2 * v_pp + 1));
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
-          if (++v_pp == npan) {
+          if (++v_pp == P64) {
             // the unused block barriers complete too: every B_VB completes once per tile
             for (int q = npan; q < (int)vbq; ++q) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
             v_pp = 0;
@@ -446,6 +455,10 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       }
     } else if (warp < 8) {
       // ===================================================== K* warps (0-7)
+      // Per 64-wide panel q (= distance chunk q): warp half `half` of lane quarter lq evaluates
+      // training points [64 q + 32 half, +32) for its 32 candidate rows: one tcgen05.ld (x32)
+      // of the squared distances, K* = k(h), the mean partials, the float16 hi/lo split, two
+      // tcgen05.st (x16) into the K* stage (k steps 2 half, 2 half + 1).
       const int lq = warp & 3, half = warp >> 2;
       const int row = 32 * lq + lane;
       const uint32_t tl_addr = tbase + ((uint32_t)(32 * lq) << 16);
@@ -453,96 +466,81 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       const int kind = m.kernel;
       const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
       uint32_t gk = gk_seg;
-      uint32_t ec = gc_seg;  // distance chunk counter
+      uint32_t ec = gc_seg;  // distance chunk counter (= panel counter)
       double mu = 0.0;
       float a1 = 0.f;
       int tl = 0, pp = 0;
-      // Software pipeline: the distances of panel g+1 are loaded from TMEM (tcgen05.ld) before
-      // panel g is computed, so the TMEM load latency overlaps the MUFU/FMA work.
-      uint32_t hbuf[2][16];
-      auto load_dist = [&](int ppn, uint32_t chunk, uint32_t (&dst)[16]) {
-        const uint32_t st = chunk % kDepth;
-        tc::mbar_wait(bar(B_DF0 + st), (chunk / kDepth) & 1u);
-        tc::tc_fence_after();
-        if (32 * ppn + 16 * half < n16)
-          tc::tmem_ld16(tl_addr + kScratch0 + 64u * st + 32u * (ppn & 1) + 16u * half, dst);
-      };
-      // two register buffers swapped by alternating calls (no dynamic register indexing)
-      auto step = [&](int g, uint32_t (&hr)[16], uint32_t (&nx)[16]) {
+      for (int g = 0; g < P; ++g) {
         const uint32_t st = ec % kDepth;
-        const int jb = 32 * pp + 16 * half;
-        const bool active = jb < n16;
+        const int jb = 64 * pp + 32 * half;
+        const int nv = min(32, n16 - jb);  // valid points of this warp (32, 16 or <= 0)
         const bool trw = (warp == 0 || warp == 7) && lane == 0;
-        tc::tmem_wait_ld();  // panel g's distances are in hr
+        tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
+        tc::tc_fence_after();
+        uint32_t hr[32];
+        if (nv > 0) {
+          tc::tmem_ld32(tl_addr + kScratch0 + 64u * st + 32u * half, hr);
+          tc::tmem_wait_ld();
+        }
         tc::tc_fence_before();
         __syncwarp();
-        const bool chunk_done = (pp & 1) || pp == npan - 1;
-        if (chunk_done) {  // both panels of the chunk loaded: free the stage
-          if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));
-          ++ec;
-        }
+        if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));  // the scratch stage is free
+        ++ec;
+        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
         const uint32_t ks = gk % kKStages;
-#ifdef GPBO_KS_REORDER
-        // the K* stage is known free before the prefetch is issued, so the fence after the wait
-        // has no outstanding TMEM load of this thread to order against
-        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
         tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
-#ifndef GPBO_KS_NOFENCE_KE
         tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
-#endif
         if (trw) trace_ev(p.trace, 7, warp, gk, trc);
-        if (g + 1 < P) {  // prefetch panel g+1
-          const int np = pp + 1 == npan ? 0 : pp + 1;
-          load_dist(np, ec, nx);
-        }
-#else
-        if (g + 1 < P) {  // prefetch panel g+1
-          const int np = pp + 1 == npan ? 0 : pp + 1;
-          load_dist(np, ec, nx);
-        }
-        if (trw) trace_ev(p.trace, 6, warp, gk, trc);
-        tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
-#ifndef GPBO_KS_NOFENCE_KE
-        tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
-#endif
-        if (trw) trace_ev(p.trace, 7, warp, gk, trc);
-#endif
         float muf = 0.f, a1f = 0.f;
-        if (active) {
-          float kv[16];
+        if (nv > 0) {
+          float kv[32];
+#ifdef GPBO_EXP_NOKSTAR  // timing experiment only: no kernel evaluation (wrong results)
+          if (true) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) kv[q] = __uint_as_float(hr[q]);
+          } else
+#endif
           if (kind == GPBO_RBF) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
+            for (int q = 0; q < 32; ++q)
               kv[q] = ex2_approx(fmaf(fmaxf(__uint_as_float(hr[q]), 0.f), c1, c0));
           } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
+            for (int q = 0; q < 32; ++q) {
               const float tq = sqrt_approx(fmaxf(__uint_as_float(hr[q]), 0.f));
               kv[q] = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
             }
           }
+          if (nv < 32) {  // points beyond n16: scratch columns the distance MMA did not write
+#pragma unroll
+            for (int q = 16; q < 32; ++q) kv[q] = 0.f;
+          }
           const float4 *ap4 = reinterpret_cast<const float4 *>(ap + jb);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 a = ap4[q];
-            muf = fmaf(kv[2 * q], a.x, muf);
-            a1f = fmaf(kv[2 * q], a.y, a1f);
-            muf = fmaf(kv[2 * q + 1], a.z, muf);
-            a1f = fmaf(kv[2 * q + 1], a.w, a1f);
+          for (int q = 0; q < 16; ++q) {
+            if (q < 8 || nv == 32) {  // alpha pairs exist for j < n16 only
+              const float4 a = ap4[q];
+              muf = fmaf(kv[2 * q], a.x, muf);
+              a1f = fmaf(kv[2 * q], a.y, a1f);
+              muf = fmaf(kv[2 * q + 1], a.z, muf);
+              a1f = fmaf(kv[2 * q + 1], a.w, a1f);
+            }
           }
-          uint32_t hw[8], lw[8];
+          uint32_t hw[16], lw[16];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < 16; ++q) {
             const float h0 = __uint_as_float(__float_as_uint(kv[2 * q]) & 0xFFFFE000u);
             const float h1 = __uint_as_float(__float_as_uint(kv[2 * q + 1]) & 0xFFFFE000u);
             hw[q] = tc::pack_f16x2(h0, h1);
             lw[q] = tc::pack_f16x2(kv[2 * q] - h0, kv[2 * q + 1] - h1);
           }
-          // this warp's 16 k values are k step `half` of the panel
-          const uint32_t kt = tl_addr + kKstar0 + 32u * ks + 8u * half;
-          tc::tmem_st8(kt, hw);
-          tc::tmem_st8(kt + 16u, lw);
+          // this warp's 32 k values are k steps 2 half, 2 half + 1 of the panel
+          const uint32_t kt = tl_addr + kKstar0 + 64u * ks + 16u * half;
+          tc::tmem_st16(kt, hw);
+          tc::tmem_st16(kt + 32u, lw);
+#ifndef GPBO_EXP_NOWAITST  // timing experiment only (races with the MMA)
           tc::tmem_wait_st();
+#endif
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -551,7 +549,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         ++gk;
         mu += (double)muf;
         a1 += a1f;
-        if (++pp == npan) {  // tile complete: hand the partial sums to the drain warps
+        if (++pp == P64) {  // tile complete: hand the partial sums to the drain warps
           const uint32_t ti = gi + tl, par = ti & 1u;
           tc::mbar_wait(bar(B_PE0 + par), ((ti >> 1) & 1u) ^ 1u);
           part_mu[(2 * half + par) * 128 + row] = mu;
@@ -563,16 +561,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           pp = 0;
           ++tl;
         }
-      };
-      if (P > 0) load_dist(0, ec, hbuf[0]);
-      for (int g = 0; g < P; g += 2) {
-        step(g, hbuf[0], hbuf[1]);
-        if (g + 1 < P) step(g + 1, hbuf[1], hbuf[0]);
       }
     }
     gi += (uint32_t)T;
     gc_seg += (uint32_t)(T * ((npan + 1) >> 1));
-    gk_seg += (uint32_t)P;
+    gk_seg += (uint32_t)P;  // (T * P64)
     ta = tb;
   }
   tc::tc_fence_before();
