@@ -291,7 +291,8 @@ def main():
     idx, ei = step_device()
     if rank == 0:
         peaks = load_peaks()
-        impl_used = {2: "tcgen05", 3: "tcgen05-stream"}.get(ctx.last_impl, "cuda-core")
+        impl_used = {2: "tcgen05", 3: "tcgen05-stream", 4: "fp64-direct"}.get(ctx.last_impl,
+                                                                             "cuda-core")
         Fc = sum(flops_per_candidate(nn, dd) * x.shape[0] for nn, dd, x in zip(n, d, w.Xstar))
         achieved = Fc / (fast_ms / fast_n / 1e3) / 1e12  # TFLOP/s of the fast-phase kernel
         if impl_used.startswith("tcgen05"):
@@ -303,6 +304,12 @@ def main():
                     "traffic_src": tr[1] if tr else None,
                     "algorithmic_bytes": int(sum(4 * dd * x.shape[0] for dd, x in zip(d, w.Xstar))),
                     "peak_src": f"{peaks['src']} bf16 dense sustained (fp16 same rate)"}
+        elif impl_used == "fp64-direct":
+            peak = 148 * 64 * 2 * peaks["sm_mhz"] * 1e6 / 1e12
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_src": "FP64 DFMA: 148 SM x 64 lanes x 2 flop x max SM clock "
+                                "(tools/micro: 58-64 DFMA/clk/SM); small problem: latency-bound"}
         else:
             peak = 148 * 128 * 2 * peaks["sm_mhz"] * 1e6 / 1e12
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -320,7 +327,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": T_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f16x3+f32+f64" if impl_used.startswith("tcgen05") else "f32+f64",
+            "dtype": ("f16x3+f32+f64" if impl_used.startswith("tcgen05") else
+                      "f64" if impl_used == "fp64-direct" else "f32+f64"),
             "data": "synthetic",
             "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
                        "M_per_gpu": per_gpu, "M_global": M_total,

@@ -228,7 +228,8 @@ int64_t gpbo_launch_count(const gpbo_ctx *ctx);
  * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
 /* Fast-phase implementation of the last scoring call: 1 = CUDA-core, 2 = tcgen05 with the
- * shared-memory-resident operand image, 3 = tcgen05 with streamed operands. */
+ * shared-memory-resident operand image, 3 = tcgen05 with streamed operands, 4 = float64 direct
+ * (small problems; no refine phase). */
 int gpbo_last_score_impl(const gpbo_ctx *ctx);
 
 /* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel
@@ -258,8 +259,10 @@ gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf);
  * covers every search of the call, else the CUDA-core kernel), 1 = CUDA-core kernel only,
  * 2 = tcgen05 only (calls outside its envelope fail with GPBO_ENOTSUP), 3 = as 2, and models
  * fitted while it is set use the streamed operand layout (the kernel for n > 256 / large d,
- * forced on small searches for testing).  Models whose resident shared-memory image would not
- * fit (n rounded to 16 > 256, or a large d) always use the streamed layout.  Diagnostic/testing. */
+ * forced on small searches for testing), 4 = the float64 direct kernel (one thread per
+ * candidate, every row scored exactly; n <= 64; auto picks it when sum over searches of
+ * rows x n16^2 <= 2^24).  Models whose resident shared-memory image would not fit (n rounded to
+ * 16 > 256, or a large d) always use the streamed layout.  Diagnostic/testing. */
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl);
 
 /* Test hook: run only the fast phase of the scoring path on M device-resident candidates of

@@ -53,7 +53,8 @@ struct gpbo_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t feed_ev[8] = {};
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05,
-                            // 3 = tcgen05 with the streamed image layout forced at fit time
+                            // 3 = tcgen05 with the streamed image layout forced at fit time,
+                            // 4 = float64 direct kernel (n <= 64)
 };
 
 struct gpbo_model {
@@ -71,6 +72,7 @@ struct gpbo_model {
   unsigned char *img = nullptr;  // tcgen05 operand images
   int64_t img_bytes = 0;
   mutable bool simt_ready = false;  // Xs32 / LT32 built (on first CUDA-core scoring call)
+  mutable bool packed = false;      // tcgen05 operand images built (on first tcgen05 call)
   mutable bool meta_pending = false;  // gp_fit_async: host meta not yet refreshed from the device
 };
 
@@ -243,21 +245,37 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   double *h_best = (double *)(h_xoff + S);
   int32_t *h_tiles = (int32_t *)(h_best + S);
   // pick the implementation: tcgen05 when every search fits its envelope
-  bool use_tc = ctx->score_impl != 1;
+  bool use_tc = ctx->score_impl != 1 && ctx->score_impl != 4;
   bool use_tcs = use_tc;  // the streamed tcgen05 kernel
   int nmax = 0, dmax = 0;
+  double work = 0.0;  // sum over searches of rows x n16^2 (the direct kernel's cost)
   for (int i = 0; i < S; ++i) {
     const SearchMeta &m = model->meta[s_first + i];
     nmax = std::max(nmax, m.n);
     dmax = std::max(dmax, m.d_pad);
     if (!gpbo::tc_supported(m)) use_tc = false;
     if (!gpbo::tcs_supported(m)) use_tcs = false;
+    const double n16 = (double)((m.n + 15) & ~15);
+    work += (double)(m_off[i + 1] - m_off[i]) * n16 * n16;
   }
   if (use_tcs) use_tc = true;
+  // small problems (config 1, the first BO iterations): one float64 kernel scores every row
+  // exactly -- no operand image, no fast phase, no refine (auto below 2^24 row x n16^2, or
+  // forced by impl 4); n <= 64 only
+  const bool direct = mode != gpbo::kModeDebug && nmax <= gpbo::kDirectMaxN &&
+                      (ctx->score_impl == 4 || (ctx->score_impl == 0 && work <= 16777216.0));
+  if (direct) use_tc = use_tcs = false;
   if (ctx->score_impl == 2 && !use_tc)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
-  const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;
-  if (!use_tc && !model->simt_ready) {
+  const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;  // (direct: any)
+  if (use_tc && !model->packed) {
+    KernTimer t(ctx, kKernPack);
+    CK(gpbo::launch_pack_tc(model->meta_d, model->S, model->Linv64, model->Xs64, model->alpha64,
+                            model->ls32, model->img, ctx->stream));
+    ctx->launches += 1;
+    model->packed = true;
+  }
+  if (!use_tc && !direct && !model->simt_ready) {
     CK(gpbo::launch_simt_operands(model->meta_d, model->S, model->X32, model->ls32,
                                   model->Linv64, model->Xs32, model->LT32, ctx->stream));
     ctx->launches += 1;
@@ -322,7 +340,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
   p.trace = ctx->trace;
   const int tiles = h_tiles[S];
-  ctx->last_impl = use_tcs ? 3 : use_tc ? 2 : 1;
+  ctx->last_impl = direct ? 4 : use_tcs ? 3 : use_tc ? 2 : 1;
   const int64_t floats_all = xo;
   // element offset in X* of the first row of tile t (tile indices of this call)
   auto tile_elem = [&](int t) -> int64_t {
@@ -339,6 +357,25 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     for (auto &e : ctx->feed_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   if (tiles == 0) return GPBO_OK;
+  if (direct) {
+    gpbo::RefineLaunch r{};
+    r.meta = p.meta;
+    r.Xstar = p.Xstar;
+    r.m_off = p.m_off; r.m_base = p.m_base; r.x_off = p.x_off;
+    r.best = p.best;
+    r.Xs64 = model->Xs64;
+    r.ls32 = model->ls32;
+    r.alpha64 = model->alpha64;
+    r.Linv64 = model->Linv64;
+    r.keys = ctx->keys_d;
+    if (mode != gpbo::kModeArgmax) { r.out_mu = out.mu; r.out_var = out.var; r.out_ei = out.ei; }
+    {
+      KernTimer t(ctx, kKernFast);
+      CK(gpbo::launch_direct(r, S, rows, ctx->stream));
+    }
+    ctx->launches += 1;
+    return GPBO_OK;
+  }
   for (int c = 0; c < nchunk; ++c) {
     const int ta = (int)((int64_t)tiles * c / nchunk), tb = (int)((int64_t)tiles * (c + 1) / nchunk);
     if (nchunk > 1) {
@@ -546,7 +583,7 @@ gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms
 }
 
 gpbo_status gpbo_set_score_impl(gpbo_ctx *ctx, int impl) {
-  if (!ctx || impl < 0 || impl > 3) return GPBO_EINVAL;
+  if (!ctx || impl < 0 || impl > 4) return GPBO_EINVAL;
   ctx->score_impl = impl;
   return GPBO_OK;
 }
@@ -692,12 +729,8 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   }
   ctx->launches += 2;
   ctx->launches += 1;
-  if (nimg > 0) {
-    KernTimer t(ctx, kKernPack);
-    CKM(gpbo::launch_pack_tc(m->meta_d, S, m->Linv64, m->Xs64, m->alpha64, m->ls32, m->img,
-                             ctx->stream));
-    ctx->launches += 1;
-  }
+  // the tcgen05 operand images are packed by the first tcgen05 scoring call (run_score): small
+  // problems scored by the float64 direct kernel never need them
   if (!wait) {  // gp_fit_async: results stay on the device until gp_model_sync / scoring
     m->meta_pending = true;
     *out = m;

@@ -156,4 +156,7 @@ cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, i
                               cudaStream_t stream);
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
                           cudaStream_t stream);
+// Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
+constexpr int kDirectMaxN = 64;
+cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream);
 }  // namespace gpbo

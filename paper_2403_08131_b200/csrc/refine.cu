@@ -150,6 +150,95 @@ refine_kernel(const RefineLaunch p) {
   }
 }
 
+// Small problems (rows x n16^2 small, n <= 64): the whole scoring in float64 -- no operand image,
+// no fast phase, no refine list; exact up to float64 rounding (the oracle's arithmetic).  One
+// warp per candidate: lane j owns training points j and j + 32 (k*_j by direct differences of
+// x / l, the kernel, alpha_j k*_j) and rows j, j + 32 of v = L^-1 k* (k*_i broadcast by shuffle);
+// warp sums give mu~ and |v|^2, lane 0 forms EI.  Keys (argmax mode; one atomic per block and
+// search) or dense raw mu / var / EI (posterior mode).
+constexpr int kDirectWarps = 8;
+
+__global__ void __launch_bounds__(32 * kDirectWarps)
+direct_kernel(const RefineLaunch p, int S, int64_t rows) {
+  __shared__ unsigned long long skey[kDirectWarps];
+  __shared__ int ss[kDirectWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * kDirectWarps + wid;  // candidate (warp-uniform)
+  const bool posterior = p.out_mu || p.out_var || p.out_ei;
+  unsigned long long key = 0ull;
+  int s = 0;
+  if (g < rows) {
+    int lo = 0, hi = S;  // search of row g: m_off[s] <= g < m_off[s + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (p.m_off[mid] <= g) lo = mid; else hi = mid;
+    }
+    s = lo;
+    while (s + 1 < S && p.m_off[s + 1] <= g) ++s;  // empty searches
+    const SearchMeta &m = p.meta[s];
+    if (m.status == GPBO_OK || m.status == GPBO_WDEGENERATE) {
+      const int n = m.n, d = m.d;
+      const int64_t row = g - p.m_off[s];
+      const float *x = p.Xstar + p.x_off[s] + row * d;
+      const float *ls = p.ls32 + m.ls_off;
+      const double *Xj = p.Xs64 + m.x_off;  // column-major x / l
+      const double *alpha = p.alpha64 + m.a_off;
+      // x*_c / l_c for c = lane, lane + 32
+      const double xa = lane < d ? (double)x[lane] / (double)ls[lane] : 0.0;
+      const double xb = lane + 32 < d ? (double)x[lane + 32] / (double)ls[lane + 32] : 0.0;
+      const int j0 = lane, j1 = lane + 32;
+      double r0 = 0.0, r1 = 0.0;
+      for (int c = 0; c < d; ++c) {
+        const double xc = __shfl_sync(0xffffffffu, c < 32 ? xa : xb, c & 31);
+        if (j0 < n) { const double t = xc - Xj[(size_t)c * n + j0]; r0 = fma(t, t, r0); }
+        if (j1 < n) { const double t = xc - Xj[(size_t)c * n + j1]; r1 = fma(t, t, r1); }
+      }
+      const double sf2 = (double)m.sf2;
+      const double k0 = j0 < n ? kernel64(r0, sf2, m.kernel) : 0.0;
+      const double k1 = j1 < n ? kernel64(r1, sf2, m.kernel) : 0.0;
+      double mu = (j0 < n ? k0 * alpha[j0] : 0.0) + (j1 < n ? k1 * alpha[j1] : 0.0);
+      const double *Li = p.Linv64 + m.mat_off;  // row-major, lower part
+      double v0 = 0.0, v1 = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double ki = __shfl_sync(0xffffffffu, i < 32 ? k0 : k1, i & 31);
+        if (i <= j0 && j0 < n) v0 = fma(Li[(size_t)j0 * n + i], ki, v0);
+        if (i <= j1 && j1 < n) v1 = fma(Li[(size_t)j1 * n + i], ki, v1);
+      }
+      double vv = v0 * v0 + v1 * v1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mu += __shfl_xor_sync(0xffffffffu, mu, o);
+        vv += __shfl_xor_sync(0xffffffffu, vv, o);
+      }
+      if (lane == 0) {
+        const double var64 = fmax(sf2 - vv, 0.0);
+        const double sig = sqrt(var64);
+        const double imp = resolve_best(p.best[s], m) - mu;
+        const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
+        if (posterior) {
+          if (p.out_mu) p.out_mu[g] = (float)(m.mean + m.std * mu);
+          if (p.out_var) p.out_var[g] = (float)(m.std * m.std * var64);
+          if (p.out_ei) p.out_ei[g] = (float)(m.std * ei);
+        } else {
+          key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));
+        }
+      }
+    }
+  }
+  if (posterior) return;
+  if (lane == 0) { skey[wid] = key; ss[wid] = s; }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // consecutive candidates: mostly one search per block
+    unsigned long long acc = 0ull;
+    const int s0 = ss[0];
+    for (int w = 0; w < kDirectWarps; ++w) {
+      if (ss[w] == s0) acc = skey[w] > acc ? skey[w] : acc;
+      else if (skey[w]) atomicMax(p.keys + ss[w], skey[w]);
+    }
+    if (acc) atomicMax(p.keys + s0, acc);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
@@ -157,6 +246,13 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
   if (max_entries <= 0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>(max_entries, (int64_t)num_sms * 4);
   refine_kernel<<<grid, kRefineThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  direct_kernel<<<(unsigned)((rows + kDirectWarps - 1) / kDirectWarps), 32 * kDirectWarps, 0,
+                  stream>>>(p, S, rows);
   return cudaGetLastError();
 }
 

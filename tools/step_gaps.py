@@ -13,7 +13,8 @@ from workloads import gen  # noqa: E402
 
 dev = torch.device("cuda", 0)
 stream = torch.cuda.current_stream(dev)
-w = gen.make(2, M=1 << 20)
+CFG = int(next((a for a in sys.argv[1:] if a.isdigit()), "2"))
+w = gen.make(CFG, M=1 << 20 if CFG == 2 else None)
 ctx = gpbo.Context(device=0, stream=stream)
 n = [s.X.shape[0] for s in w.searches]
 d = [s.X.shape[1] for s in w.searches]
