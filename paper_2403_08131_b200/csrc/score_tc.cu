@@ -789,7 +789,7 @@ bool tc_needs_stream(int n, int d) { return !resident_fits(n, d); }
 cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64,
                            const double *Xs64, const double *alpha64, const float *ls32,
                            unsigned char *img, cudaStream_t stream) {
-  pack_tc_kernel<<<dim3(S, 16), 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
+  pack_tc_kernel<<<dim3(S, 64), 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
                                                    alpha64, ls32, img);
   return cudaGetLastError();
 }
