@@ -8,7 +8,10 @@
 
 namespace gpbo {
 
-constexpr int kFitThreads = 384;
+#ifndef GPBO_FIT_THREADS
+#define GPBO_FIT_THREADS 384
+#endif
+constexpr int kFitThreads = GPBO_FIT_THREADS;
 constexpr int kSimtTile = 64;  // candidates per CTA of the CUDA-core scoring kernel
 // Panel width of the fit's blocked factorisation (fit.cu) and its shared-memory plan:
 // y~, w (n-vectors), spare/flags, the block maps M, N, R, 2 x 8 panel rows G of stride gs (a
