@@ -381,10 +381,9 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     if (nchunk > 1) {
       // chunk c's rows: from its first tile's row to the next chunk's (the last chunk: to the end)
       const int64_t e0 = c == 0 ? 0 : tile_elem(ta), e1 = tile_elem(tb);
-      if (c == 0) {  // the copies may only start once earlier work on the stream is done
-        CK(cudaEventRecord(ctx->feed_ev[0], ctx->stream));
-        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->feed_ev[0], 0));
-      }
+      // no wait before the first copy: the staging buffer's previous users were synchronous
+      // calls (finished on return), and the work queued on the stream since (an asynchronous
+      // fit) does not touch it -- the copies overlap the fit
       if (e1 > e0)
         CK(cudaMemcpyAsync(const_cast<float *>(Xstar_dev) + e0, host_src + e0,
                            (size_t)(e1 - e0) * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
