@@ -424,7 +424,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   }
   {
     KernTimer t(ctx, kKernRefine);
-    CK(gpbo::launch_refine(r, rows, ctx->num_sms, ctx->stream));
+    CK(gpbo::launch_refine(r, rows, ctx->num_sms, nmax, ctx->stream));
   }
   ctx->launches += 1;
   return GPBO_OK;

@@ -157,7 +157,7 @@ cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X
                                  float *LT32, cudaStream_t stream);
 cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, int nmax,
                               cudaStream_t stream);
-cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
+cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms, int nmax,
                           cudaStream_t stream);
 // Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
 constexpr int kDirectMaxN = 64;

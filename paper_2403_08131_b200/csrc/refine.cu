@@ -14,6 +14,8 @@
 //
 // gp_posterior runs the same code densely over all rows (posterior mode).
 // One CTA per candidate; threads stride over training points, then over rows of L^-1.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -150,6 +152,111 @@ refine_kernel(const RefineLaunch p) {
   }
 }
 
+// Argmax-mode refine with a thread-block cluster of kSplit CTAs per flagged candidate: every CTA
+// forms k* (and mu~) for all training points, then the rows of v = L^-1 k* are dealt to the
+// CTAs (row j to CTA j mod kSplit) so the L^-1 stream (n^2 / 2 float64 from L2: 160 KB at
+// n = 200, 1 MB at n = 500) is read by kSplit SMs at once; the partial |v|^2 go to CTA 0's shared
+// memory (DSMEM) and are summed there in rank order (deterministic), and CTA 0 forms EI and the
+// key.  The fast phase's final threshold is fixed while this runs, so every CTA of a cluster
+// takes the same skip decision.
+constexpr int kSplit = 8;
+
+__global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kRefineThreads)
+refine_split_kernel(const RefineLaunch p) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double xsh[GPBO_MAX_D];
+  __shared__ double ksh[GPBO_MAX_N];
+  __shared__ double red[kRefineThreads / 32];
+  __shared__ double part[kSplit];
+  const int tid = threadIdx.x;
+  const int rank = (int)cluster.block_rank();
+  const int64_t cid = blockIdx.x / kSplit, ncl = gridDim.x / kSplit;
+  double *part0 = cluster.map_shared_rank(part, 0);
+  const int64_t nent = (int64_t)*p.list_count;
+  for (int64_t e = cid; e < nent; e += ncl) {
+    const RefineEntry en = p.list[e];
+    if (en.ei_hi < __uint_as_float(p.thr[en.s])) continue;  // uniform over the cluster
+    const int s = en.s;
+    const uint32_t row = en.row;
+    const SearchMeta &m = p.meta[s];
+    const int n = m.n, d = m.d;
+    const float *x = p.Xstar + p.x_off[s] + (int64_t)row * d;
+    const float *ls = p.ls32 + m.ls_off;
+    __syncthreads();
+    for (int c = tid; c < d; c += kRefineThreads) xsh[c] = (double)x[c] / (double)ls[c];
+    __syncthreads();
+    const double *Xj = p.Xs64 + m.x_off;
+    const double *alpha = p.alpha64 + m.a_off;
+    double mu = 0.0;
+    for (int j = tid; j < n; j += kRefineThreads) {
+      double r2 = 0.0, r2b = 0.0;
+      int c = 0;
+      for (; c + 2 <= d; c += 2) {
+        const double d0 = xsh[c] - Xj[(size_t)c * n + j];
+        const double d1 = xsh[c + 1] - Xj[(size_t)(c + 1) * n + j];
+        r2 += d0 * d0;
+        r2b += d1 * d1;
+      }
+      if (c < d) {
+        const double d0 = xsh[c] - Xj[(size_t)c * n + j];
+        r2 += d0 * d0;
+      }
+      r2 += r2b;
+      const double k = kernel64(r2, (double)m.sf2, m.kernel);
+      ksh[j] = k;
+      mu += k * alpha[j];
+    }
+    mu = block_sum2(mu, red);
+    // this CTA's rows j = rank + kSplit (w + kW i): warp per row, four rows per pass
+    const double *Li = p.Linv64 + m.mat_off;
+    const int lane = tid & 31, wp = tid >> 5;
+    constexpr int kW = kRefineThreads / 32;
+    double vv = 0.0;
+    for (int jb = wp; rank + kSplit * jb < n; jb += 4 * kW) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double *rowp[4];
+      int jr[4];
+      int jmax = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int j = rank + kSplit * (jb + r * kW);
+        jr[r] = j < n ? j : -1;
+        rowp[r] = Li + (size_t)min(j, n - 1) * n;
+        if (j < n) jmax = max(jmax, j);
+      }
+      for (int k = lane; k <= jmax; k += 32) {
+        const double kv = ksh[k];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (k <= jr[r]) acc[r] = fma(rowp[r][k], kv, acc[r]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (jr[r] >= 0) vv = fma(acc[r], acc[r], vv);
+    }
+    if (lane != 0) vv = 0.0;
+    vv = block_sum2(vv, red);
+    if (tid == 0) part0[rank] = vv;
+    cluster.sync();  // the partials have landed in CTA 0
+    if (rank == 0 && tid == 0) {
+      double v2 = 0.0;
+      for (int r = 0; r < kSplit; ++r) v2 += part[r];
+      const double var64 = fmax((double)m.sf2 - v2, 0.0);
+      const double sig = sqrt(var64);
+      const double imp = resolve_best(p.best[s], m) - mu;
+      const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
+      const unsigned long long key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));
+      if (key) atomicMax(p.keys + s, key);
+    }
+    cluster.sync();  // CTA 0 has read the partials before the next entry overwrites them
+  }
+}
+
 // Small problems (rows x n16^2 small, n <= 64): the whole scoring in float64 -- no operand image,
 // no fast phase, no refine list; exact up to float64 rounding (the oracle's arithmetic).  One
 // warp per candidate: lane j owns training points j and j + 32 (k*_j by direct differences of
@@ -241,9 +348,17 @@ direct_kernel(const RefineLaunch p, int S, int64_t rows) {
 
 }  // namespace
 
-cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms,
+cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms, int nmax,
                           cudaStream_t stream) {
   if (max_entries <= 0) return cudaSuccess;
+  // argmax mode with long L^-1 rows (n > 128: configs 2, 4): clusters of kSplit CTAs per flagged
+  // candidate, 4 CTAs per SM (config 2 refine 23 -> 17 us, config 4 92 -> 41 us).  Small n with
+  // many flagged candidates (config 3: ~3.5k) keeps one CTA per candidate (56 vs 371 us).
+  if (p.list && nmax > 128) {
+    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(max_entries, num_sms * 4 / kSplit));
+    refine_split_kernel<<<(unsigned)(ncl * kSplit), kRefineThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+  }
   const int grid = (int)std::min<int64_t>(max_entries, (int64_t)num_sms * 4);
   refine_kernel<<<grid, kRefineThreads, 0, stream>>>(p);
   return cudaGetLastError();

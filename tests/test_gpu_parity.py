@@ -241,6 +241,27 @@ def test_chunked_host_feed_matches_device(G, case):
     m.free()
 
 
+@pytest.mark.parametrize("impl", IMPLS)
+def test_empty_and_single_candidate_searches(G, impl):
+    """A search with no candidates returns idx -1 (key 0 = "no candidate"); a one-candidate search
+    returns that candidate; the others are unaffected -- on every implementation."""
+    gpbo, ctx = G
+    ctx.set_score_impl(impl)
+    try:
+        w = gen.random_case(41, [30, 12, 50, 7], [4, 4, 6, 3], [500, 0, 1, 300], S=4)
+        m = _fit(G, w)
+        Xs, off = H.pack_candidates(w)
+        idx, ei = ctx.score_argmax(m, Xs, off)
+        assert int(idx[1]) == -1
+        assert int(idx[2]) == 0
+        oms = H.oracle_fits(w)
+        for s in (0, 2, 3):
+            res = gp.score(oms[s], w.Xstar[s])
+            H.check_argmax(res, int(idx[s]), f"empty[{s}]")
+    finally:
+        ctx.set_score_impl(0)
+
+
 def test_nan_candidate_is_never_chosen(G):
     gpbo, ctx = G
     w = gen.random_case(12, 20, 3, 256)
