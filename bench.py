@@ -153,7 +153,8 @@ def main():
     ap.add_argument("--layout", default="uniform", choices=["uniform", "bo"])
     ap.add_argument("--score-impl", type=int, default=0, help="0 auto, 1 CUDA-core, 2 tcgen05")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 20,
+                    help="candidates the CPU oracle scores for cpu_baseline (~10-15 s at config 2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
