@@ -26,6 +26,8 @@ struct gpbo_ctx {
   unsigned long long *keys_d = nullptr;  // [cap] keys | [cap] u32 thresholds | u32 list count
   unsigned long long *keys_h = nullptr;
   int keys_cap = 0;
+  unsigned long long *cur_keys_d = nullptr;  // this call's keys | thr | count (in aux_d)
+  size_t cur_key_bytes = 0;
   gpbo::RefineEntry *list_d = nullptr;   // refine list of the argmax path
   size_t list_cap = 0;
   void *stage_d = nullptr;  // device staging of host-resident candidates / outputs
@@ -200,7 +202,7 @@ gpbo_status ensure_keys(gpbo_ctx *ctx, int S) {
   if (ctx->keys_h) CK(cudaFreeHost(ctx->keys_h));
   int cap = std::max(S, 64);
   CK(cudaMalloc(&ctx->keys_d, cap * (sizeof(unsigned long long) + 4) + 16));
-  CK(cudaMallocHost(&ctx->keys_h, (cap + 1) * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&ctx->keys_h, (2 * cap + 2) * sizeof(unsigned long long)));
   ctx->keys_cap = cap;
   return GPBO_OK;
 }
@@ -232,7 +234,11 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
                       const double *best_std, int mode, const Outputs &out,
                       const float *host_src = nullptr) {
   // aux layout: m_off[S+1] i64 | m_base[S] i64 | x_off[S] i64 | best[S] f64 | tile_first[S+1] i32
-  const size_t bytes = (size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4;
+  // | (8-aligned) keys[S] u64 | thr[S] u32 | list count u32 -- the key / threshold / count words
+  // are zeroed by the same upload (no separate memset) and read back by one copy
+  const size_t meta_bytes = ((size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4 + 7) & ~(size_t)7;
+  const size_t key_bytes = (size_t)S * 12 + 4;
+  const size_t bytes = meta_bytes + key_bytes;
   gpbo_status st = ensure_aux(ctx, bytes + 64);
   if (st) return st;
   st = ensure_keys(ctx, S);
@@ -307,13 +313,15 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     st = ensure_list(ctx, (size_t)rows);
     if (st) return st;
   }
+  std::memset((char *)ctx->aux_h + meta_bytes, 0, key_bytes);
   CK(cudaMemcpyAsync(ctx->aux_d, ctx->aux_h, bytes, cudaMemcpyHostToDevice, ctx->stream));
   if (!ctx->aux_ev) CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(ctx->aux_ev, ctx->stream));
-  unsigned int *thr_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap);
-  unsigned int *count_d = thr_d + ctx->keys_cap;
-  CK(cudaMemsetAsync(ctx->keys_d, 0, ctx->keys_cap * (sizeof(unsigned long long) + 4) + 4,
-                     ctx->stream));
+  unsigned long long *keys_d = (unsigned long long *)((char *)ctx->aux_d + meta_bytes);
+  unsigned int *thr_d = (unsigned int *)(keys_d + S);
+  unsigned int *count_d = thr_d + S;
+  ctx->cur_keys_d = keys_d;
+  ctx->cur_key_bytes = key_bytes;
   char *dptr = (char *)ctx->aux_d;
   gpbo::ScoreLaunch p{};
   p.meta = model->meta_d + s_first;
@@ -329,7 +337,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.alpha64 = model->alpha64;
   p.ls32 = model->ls32;
   p.img = model->img;
-  p.keys = ctx->keys_d;
+  p.keys = keys_d;
   p.out_var = out.var;
   p.mode = mode;
   p.thr = thr_d;
@@ -367,7 +375,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     r.ls32 = model->ls32;
     r.alpha64 = model->alpha64;
     r.Linv64 = model->Linv64;
-    r.keys = ctx->keys_d;
+    r.keys = keys_d;
     if (mode != gpbo::kModeArgmax) { r.out_mu = out.mu; r.out_var = out.var; r.out_ei = out.ei; }
     {
       KernTimer t(ctx, kKernFast);
@@ -411,7 +419,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   r.ls32 = model->ls32;
   r.alpha64 = model->alpha64;
   r.Linv64 = model->Linv64;
-  r.keys = ctx->keys_d;
+  r.keys = keys_d;
   r.thr = thr_d;
   if (mode == gpbo::kModeArgmax) {
     r.list = ctx->list_d;
@@ -438,12 +446,11 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
   gpbo_status st = run_score(ctx, model, 0, S, xd, m_off, m_base, best_std, gpbo::kModeArgmax,
                              Outputs(), host_src);
   if (st) return st;
+  unsigned long long *keys_d = ctx->cur_keys_d;
   if (ctx->nranks > 1)
-    NK(ncclAllReduce(ctx->keys_d, ctx->keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->keys_h, ctx->keys_d, S * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  unsigned int *count_d = (unsigned int *)(ctx->keys_d + ctx->keys_cap) + ctx->keys_cap;
-  CK(cudaMemcpyAsync(ctx->keys_h + ctx->keys_cap, count_d, 4, cudaMemcpyDeviceToHost,
+    NK(ncclAllReduce(keys_d, keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+  // keys, thresholds and the refine count in one read-back
+  CK(cudaMemcpyAsync(ctx->keys_h, keys_d, ctx->cur_key_bytes, cudaMemcpyDeviceToHost,
                      ctx->stream));
   if (model->meta_pending)  // the fit results ride along with the keys
     CK(cudaMemcpyAsync(const_cast<gpbo_model *>(model)->meta.data(), model->meta_d,
@@ -452,7 +459,7 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
   model->meta_pending = false;
   CK(cudaGetLastError());
   harvest_events(ctx);
-  ctx->last_refine = (int64_t)(unsigned int)ctx->keys_h[ctx->keys_cap];
+  ctx->last_refine = (int64_t)((const unsigned int *)(ctx->keys_h + S))[S];
   for (int s = 0; s < S; ++s) {
     const unsigned long long k = ctx->keys_h[s];
     const SearchMeta &q = model->meta[s];
