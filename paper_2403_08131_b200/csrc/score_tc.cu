@@ -222,8 +222,10 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           uint32_t bq = x0 + (uint32_t)q * 128u;          // rows 64 q (2048 B)
           for (int k = 0; k < kb; ++k) {
             tc::mma_f16_split(dt, a, H32, bq, H32, idn, k > 0);
+#ifndef GPBO_EXP_NODIST  // timing experiment only: 1 of the 3 distance products
             tc::mma_f16_split(dt, a, H32, bq + xlo, H32, idn, 1u);
             tc::mma_f16_split(dt, a + 256u, H32, bq, H32, idn, 1u);  // A lo: +4096 B
+#endif
             a += 512u;
             bq += 2u * xlo;
           }
@@ -329,6 +331,18 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const uint32_t a0 = tc::smem_u32(Abuf) + ab * kb * 8192;
         for (int r = lt; r < 128; r += 64) {
           const bool valid = r < rows;
+#ifndef GPBO_LOADER_SCALAR  // (A/B switch)
+          if ((d & 3) == 0) {  // vectorised path (configs 2, 4)
+            float qh;
+            bool nan;
+            convert_row_vec4(stg, w, r, d, kb, valid, a0, qh, nan);
+            const bool unsafe = !(qh <= 30000.f);
+            const uint32_t flags =
+                (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
+            rowinfo[(ti & 7u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
+            continue;
+          }
+#endif
           float qh = 0.f;
           bool nan = false;
           if (valid)
@@ -404,7 +418,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           tc::mbar_wait(bar(B_VB0 + blk), ((blk >= 4u) ? vb1c : vb0c) & 1u);
           tc::tc_fence_after();
           const int c = 32 * pb;
+#ifdef GPBO_EXP_NODRAINLD  // timing experiment only: the drain does not read V
+          if (false) {
+#else
           if (c + 32 <= n16) {
+#endif
             uint32_t r0[16], r1[16];
             tc::tmem_ld16(va + (uint32_t)c, r0);
             tc::tmem_ld16(va + (uint32_t)(c + 16), r1);
@@ -450,8 +468,12 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         // the float16x3 augmented GEMM; margin x4
         const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f);
         const float dvar = 4.f * var_bound(u, sf2, s2, nn, lrs);
+#ifndef GPBO_EXP_NOFINISH  // timing experiment only
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
                     (flags & kFlagUnsafe) != 0u, 2, 128, 8);
+#else
+        (void)dmu; (void)dvar; (void)valid; (void)rloc;
+#endif
         if (trd) trace_ev(p.trace, 19, 9, ti, trc);
       }
     } else if (warp < 8) {

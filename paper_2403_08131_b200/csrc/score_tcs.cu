@@ -304,6 +304,18 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
         const uint32_t a0 = tc::smem_u32(Abuf) + ab * kb * 8192;
         for (int r = lane; r < 128; r += 32) {
           const bool valid = r < rows;
+#ifndef GPBO_LOADER_SCALAR  // (A/B switch)
+          if ((d & 3) == 0) {  // vectorised path (config 4)
+            float qh;
+            bool nan;
+            convert_row_vec4(stage, wsc, r, d, kb, valid, a0, qh, nan);
+            const bool unsafe = !(qh <= 30000.f);
+            const uint32_t flags =
+                (valid && !nan ? 0u : kFlagInvalid) | (unsafe ? kFlagUnsafe : 0u);
+            rowinfo[(ti & 7u) * 128 + r] = make_float2(qh * m.hscale, __uint_as_float(flags));
+            continue;
+          }
+#endif
           float qh = 0.f;
           bool nan = false;
           if (valid)
