@@ -540,14 +540,16 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
             for (int q = 0; q < 32; ++q) kv[q] = __uint_as_float(hr[q]);
           } else
 #endif
+          // |h| (a free source modifier) rather than max(h, 0): the GEMM-form h can be a few ulps
+          // negative; |h| stays within the same error bound of the true h >= 0
           if (kind == GPBO_RBF) {
 #pragma unroll
             for (int q = 0; q < 32; ++q)
-              kv[q] = ex2_approx(fmaf(fmaxf(__uint_as_float(hr[q]), 0.f), c1, c0));
+              kv[q] = ex2_approx(fmaf(fabsf(__uint_as_float(hr[q])), c1, c0));
           } else {
 #pragma unroll
             for (int q = 0; q < 32; ++q) {
-              const float tq = sqrt_approx(fmaxf(__uint_as_float(hr[q]), 0.f));
+              const float tq = sqrt_approx(fabsf(__uint_as_float(hr[q])));
               kv[q] = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
             }
           }

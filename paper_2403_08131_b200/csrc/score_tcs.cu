@@ -481,11 +481,11 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
           if (kind == GPBO_RBF) {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              kv[q] = ex2_approx(fmaf(fmaxf(__uint_as_float(hr[q]), 0.f), c1, c0));
+              kv[q] = ex2_approx(fmaf(fabsf(__uint_as_float(hr[q])), c1, c0));
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              const float tq = sqrt_approx(fmaxf(__uint_as_float(hr[q]), 0.f));
+              const float tq = sqrt_approx(fabsf(__uint_as_float(hr[q])));
               kv[q] = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
             }
           }
