@@ -126,12 +126,16 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, const F
       // when EI_hi >= thr (else it could neither raise the threshold nor be flagged).
       bool screened = false;
       if (p.mode == kModeArgmax) {
-        const float s_hi = sqrtf(var + dvar);
+        // approximate sqrt / division / exp (relative errors ~1e-6, far inside the 1.001 margin):
+        // this screen runs for every candidate on the drain warps, which share their
+        // sub-partitions with the K* warps
+        float s_hi;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s_hi) : "f"(var + dvar));
         const float imp = (float)(best - (mu - (double)dmu));
-        const float z = imp / s_hi;
+        const float z = __fdividef(imp, s_hi);
         if (s_hi > 0.f) {
           const float ph = s_hi * 0.398942280401432678f * __expf(-0.5f * z * z);
-          const float ub = (z < 0.f ? ph / fmaf(z, z, 1.f) : ph + imp) * 1.001f;
+          const float ub = (z < 0.f ? __fdividef(ph, fmaf(z, z, 1.f)) : ph + imp) * 1.001f;
           if (ub < thr) { ei_hi = ub; ei_lo = 0.f; screened = true; }
         }
       }

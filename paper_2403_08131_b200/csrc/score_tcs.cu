@@ -370,6 +370,8 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
       const int64_t row0s = p.m_off[s];
       const float vun2 = m.vunscale2, sf2 = m.sf2, pmaxh = m.pmax_h, lrs = m.linv_rowsum;
       const int nn = m.n;
+      // variance bound 4 var_bound(u, sf2, s2, n, lrs) = vbk (sf2 + s2), its factor hoisted
+      const float vbk = 4.f * 16.f * 5.9604645e-8f * sqrtf((float)nn) * (1.f + 0.01f * lrs * sqrtf(sf2));
       uint32_t cv = gv;
       for (int tl = 0; tl < T; ++tl) {
         const uint32_t ti = gi + tl;
@@ -426,7 +428,7 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
         const float var = fmaxf(sf2 - s2, 0.f);
         // error bounds as in score_tc.cu
         const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f);
-        const float dvar = 4.f * var_bound(u, sf2, s2, nn, lrs);
+        const float dvar = vbk * (sf2 + s2);
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
                     (flags & kFlagUnsafe) != 0u, 2, 128, 8);
       }
