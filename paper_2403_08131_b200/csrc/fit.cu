@@ -35,6 +35,10 @@ namespace gpbo {
 namespace {
 
 constexpr int kWarps = kFitThreads / 32;
+#ifndef GPBO_FIT_QW
+#define GPBO_FIT_QW 4
+#endif
+constexpr int kQ = GPBO_FIT_QW;  // tiles of one tile row per trailing-update work item (<= kQ)
 static_assert(kFitB == 8, "the DMMA tiling of fit.cu assumes 8-step panels");
 
 #ifdef GPBO_FIT_TIMING  // phase clocks of CTA 0 printed at exit (tools/fit_phases.py)
@@ -369,9 +373,9 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     auto quad = [&](const double *Ga, const double *Gb, int R, int C0, int cnt) {
       const int i = 8 * R + gid;
       double *Wt = W + tb(R, C0) + 2 * lane;
-      double2 c[4];
+      double2 c[kQ];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kQ; ++q)
         if (q < cnt) c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -379,19 +383,19 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
         if (Gh == nullptr) continue;
         const double a0 = -Gh[tig * gs + i], a1 = -Gh[(4 + tig) * gs + i];
         const double *g0 = Gh + tig * gs + 8 * C0 + gid, *g1 = g0 + 4 * gs;
-        double b0[4], b1[4];
+        double b0[kQ], b1[kQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kQ; ++q)
           if (q < cnt) { b0[q] = g0[8 * q]; b1[q] = g1[8 * q]; }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kQ; ++q)
           if (q < cnt) dmma(c[q].x, c[q].y, a0, b0[q]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kQ; ++q)
           if (q < cnt) dmma(c[q].x, c[q].y, a1, b1[q]);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kQ; ++q)
         if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
     };
     constexpr int kT = kWarps - 1;  // T warps (the highest warp is the D warp)
@@ -403,7 +407,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
       __syncthreads();
       FIT_T(3);
       if (JT + 1 == nt) break;
-      const int nrt = nt - JT - 1, nlq = (JT + 3) / 4;
+      const int nrt = nt - JT - 1, nlq = (JT + kQ - 1) / kQ;
       if (warp == kWarps - 1) {  // look-ahead: the next diagonal tile, then its D
         quad(G1, nullptr, JT + 1, JT + 1, 1);
         __syncwarp();
@@ -412,13 +416,13 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
         // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
         // (row 0's right quad is the diagonal tile -- the D warp's), round robin, rotated
         for (int r = 0, w0 = 0; r < nrt; ++r, w0 = (w0 + 5) % kT) {
-          const int R = JT + 1 + r, len = nlq + (r >> 2) + (r > 0 ? 1 : 0);
+          const int R = JT + 1 + r, len = nlq + (r > 0 ? r / kQ + 1 : 0);
           for (int q = (warp - w0 + kT) % kT; q < len; q += kT) {
             if (q < nlq) {
-              quad(G1, nullptr, R, 4 * q, min(4, JT - 4 * q));
+              quad(G1, nullptr, R, kQ * q, min(kQ, JT - kQ * q));
             } else {
-              const int c0 = 4 * (q - nlq);
-              quad(G1, nullptr, R, JT + 1 + c0, min(4, r + 1 - c0));
+              const int c0 = kQ * (q - nlq);
+              quad(G1, nullptr, R, JT + 1 + c0, min(kQ, r + 1 - c0));
             }
           }
         }
