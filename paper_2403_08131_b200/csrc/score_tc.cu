@@ -639,6 +639,7 @@ __global__ void __launch_bounds__(256)
 pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const double *alpha64,
                const float *ls32, unsigned char *img_all) {
   __shared__ double sc[4];
+  __shared__ double il2[GPBO_MAX_D];  // 1 / l_c^2, loaded by all threads at once
   const int s = blockIdx.x;
   const int nch = gridDim.y, ch = blockIdx.y;  // blocks of one search split every loop below
   SearchMeta m = meta[s];
@@ -653,9 +654,15 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
   const double gk = m.kernel == GPBO_RBF ? 0.70710678118654752440 : 2.2360679774997896964;
   const double lmax = m.linv_absmax;
   const int t0 = ch * blockDim.x + threadIdx.x, tstep = nch * blockDim.x;
+  // the lengthscale loads in parallel (thread 0 alone made d dependent global round trips)
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const double l = (double)ls32[m.ls_off + c];
+    il2[c] = 1.0 / (l * l);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double qbox = 0.0;
-    for (int c = 0; c < d; ++c) qbox += 1.0 / ((double)ls32[m.ls_off + c] * ls32[m.ls_off + c]);
+    for (int c = 0; c < d; ++c) qbox += il2[c];
     const double Qm = fmax(gk * gk * qbox, gk * gk * (double)m.pmax);
     const int e = (int)ceil(0.5 * log2(fmax(Qm, 1e-30) / 8192.0));
     const int tK = (int)floor(log2(8192.0 / (double)m.sf2));
