@@ -483,7 +483,8 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
 extern "C" {
 
 const char *gpbo_version(void) {
-  return "libgpbo 0.1 (sm_100a; fit fp64 1 CTA/search; score: tcgen05 fp16x3 + SIMT fallback)";
+  return "libgpbo 0.2 (sm_100a; fit fp64 1 CTA/search; score: tcgen05 fp16x3 resident / TMA-streamed, "
+         "fp64 direct for small problems, CUDA-core fallback; fp64 refine)";
 }
 
 gpbo_status gpbo_nccl_unique_id(void *out) {
