@@ -105,6 +105,8 @@ CASES = [
     ("n129_d33", lambda: gen.random_case(4, 129, 33, 1000)),
     ("n255_d64", lambda: gen.random_case(5, 255, 64, 600)),
     ("n511_d20", lambda: gen.random_case(6, 511, 20, 400)),
+    # config-5 late-iteration shape (d = 35 encoded, n ~ 200): streamed tcgen05 layout
+    ("n200_d35", lambda: gen.random_case(7, 200, 35, 1500)),
 ]
 
 
