@@ -194,6 +194,9 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   }
   const double best = block_reduce(bmin, red, MinOp(), INFINITY);
 
+  // Programmatic dependent launch: everything above reads only the caller's inputs and ran
+  // while the Gram pre-pass was still executing; from here on its outputs are read.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- pmax = max_j |x_j / l|^2 (the pre-pass's per-CTA maxima)
   double pmax = 0.0;
   for (int b = 0; b * 128 < n; ++b) pmax = fmax(pmax, io.pm_part[16 * s + b]);
@@ -630,6 +633,9 @@ __global__ void __launch_bounds__(128)
 gram_kernel(const SearchMeta *__restrict__ meta, const FitIO io) {
   __shared__ double xw[4][16][GPBO_MAX_D + 1];
   __shared__ double red[4];
+  // let the dependent fit kernel start its input validation / standardisation now; it waits
+  // (griddepcontrol.wait) for this grid's completion before reading Xs64 / Kt64 / pm_part
+  asm volatile("griddepcontrol.launch_dependents;");
   const int s = blockIdx.y;
   const SearchMeta m = meta[s];
   const int n = m.n, d = m.d, nt = (n + 7) / 8;
@@ -724,8 +730,18 @@ cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const Fi
     if (e != cudaSuccess) return e;
     smem_set = smem_bytes;
   }
-  fit_kernel<<<S, kFitThreads, smem_bytes, stream>>>(meta_d, io, meta_out);
-  return cudaGetLastError();
+  // programmatic dependent launch after the Gram pre-pass (see fit_body's griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S);
+  cfg.blockDim = dim3(kFitThreads);
+  cfg.dynamicSmemBytes = (size_t)smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fit_kernel, meta_d, io, meta_out);
 }
 
 cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, const FitIO &io,
