@@ -62,6 +62,7 @@ refine_kernel(const RefineLaunch p) {
   __shared__ double ksh[GPBO_MAX_N];
   __shared__ double red[kRefineThreads / 32];
   const int tid = threadIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast phase's outputs are complete
   const int64_t nent = p.list ? (int64_t)*p.list_count : p.dense_rows;
   for (int64_t e = blockIdx.x; e < nent; e += gridDim.x) {
     int s;
@@ -173,6 +174,7 @@ refine_split_kernel(const RefineLaunch p) {
   const int rank = (int)cluster.block_rank();
   const int64_t cid = blockIdx.x / kSplit, ncl = gridDim.x / kSplit;
   double *part0 = cluster.map_shared_rank(part, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast phase's list is complete
   const int64_t nent = (int64_t)*p.list_count;
   for (int64_t e = cid; e < nent; e += ncl) {
     const RefineEntry en = p.list[e];
@@ -356,8 +358,18 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
   // many flagged candidates (config 3: ~3.5k) keeps one CTA per candidate (56 vs 371 us).
   if (p.list && nmax > 128) {
     const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(max_entries, num_sms * 4 / kSplit));
-    refine_split_kernel<<<(unsigned)(ncl * kSplit), kRefineThreads, 0, stream>>>(p);
-    return cudaGetLastError();
+    // programmatic dependent launch after the fast phase (griddepcontrol.wait inside); the
+    // cluster shape comes from __cluster_dims__
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ncl * kSplit));
+    cfg.blockDim = dim3(kRefineThreads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, refine_split_kernel, p);
   }
   const int grid = (int)std::min<int64_t>(max_entries, (int64_t)num_sms * 4);
   refine_kernel<<<grid, kRefineThreads, 0, stream>>>(p);

@@ -162,6 +162,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // programmatic dependent launch: barrier init and TMEM allocation above overlapped the
+  // previous kernel (the operand pack); its outputs (meta constants, image) are read below.
+  // The refine kernel may be scheduled on SMs this grid frees.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
 
   // Counters are CTA-global across segments (mbarrier phases continue): tiles gi, distance
   // panels gd, K* panels gk.  Every role advances them identically.
@@ -641,6 +646,7 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
   __shared__ double sc[4];
   __shared__ double il2[GPBO_MAX_D];  // 1 / l_c^2, loaded by all threads at once
   const int s = blockIdx.x;
+  asm volatile("griddepcontrol.launch_dependents;");  // the scoring kernel may start its setup
   const int nch = gridDim.y, ch = blockIdx.y;  // blocks of one search split every loop below
   SearchMeta m = meta[s];
   if (!m.tc_ok || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
@@ -847,8 +853,17 @@ cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int grid = std::min(num_sms, total_tiles);
-  kern<<<grid, kThreads, smem, stream>>>(p, tile_lo, total_tiles, img_max, kb_max, d_max);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, tile_lo, total_tiles, img_max, kb_max, d_max);
 }
 
 }  // namespace gpbo

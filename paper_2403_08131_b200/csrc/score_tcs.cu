@@ -129,6 +129,11 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // programmatic dependent launch: barrier init and TMEM allocation above overlapped the
+  // previous kernel (the operand pack); its outputs (meta constants, image) are read below.
+  // The refine kernel may be scheduled on SMs this grid frees.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
 
   // CTA-global counters (mbarrier phases continue across segments); every role advances the
   // ones it uses identically: tiles gi, distance chunks gc, K* items gk, window uses gv,
