@@ -732,7 +732,8 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   {
     KernTimer t(ctx, kKernFit);
     CKM(gpbo::launch_gram(meta_in, S, m->nmax, m->dmax, io, ctx->stream));
-    CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream));
+    CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream,
+                         m->nmax <= gpbo::kFitSmemMaxN));
   }
   ctx->launches += 2;
   ctx->launches += 1;

@@ -722,7 +722,7 @@ simt_operands_kernel(const SearchMeta *__restrict__ meta, const float *__restric
 }  // namespace
 
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
-                       SearchMeta *meta_out, cudaStream_t stream) {
+                       SearchMeta *meta_out, cudaStream_t stream, bool pdl) {
   static int smem_set = -1;  // the attribute call costs microseconds: only when it grows
   if (smem_bytes > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(fit_kernel,
@@ -730,7 +730,9 @@ cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const Fi
     if (e != cudaSuccess) return e;
     smem_set = smem_bytes;
   }
-  // programmatic dependent launch after the Gram pre-pass (see fit_body's griddepcontrol.wait)
+  // programmatic dependent launch after the Gram pre-pass (see fit_body's griddepcontrol.wait);
+  // the caller enables it for shared-memory working matrices only (n <= 216: fit 0.145 ->
+  // 0.137 ms at n = 200; with the L2-resident matrix of n = 500 it measured 1.24 -> 1.34 ms)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S);
   cfg.blockDim = dim3(kFitThreads);
@@ -740,7 +742,7 @@ cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const Fi
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, fit_kernel, meta_d, io, meta_out);
 }
 

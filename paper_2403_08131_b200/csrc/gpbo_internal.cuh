@@ -151,7 +151,7 @@ struct FitIO {
 cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, const FitIO &io,
                         cudaStream_t stream);
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
-                       SearchMeta *meta_out, cudaStream_t stream);
+                       SearchMeta *meta_out, cudaStream_t stream, bool pdl);
 cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
                                  const float *ls32, const double *Linv64, float *Xs32,
                                  float *LT32, cudaStream_t stream);
