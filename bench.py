@@ -132,21 +132,56 @@ class ClockSampler:
                 "samples": self.n, "source": "nvml, 0.5 ms polling during the timed region"}
 
 
-def cpu_oracle_rate(cfg, M_sample, seed_rank=0):
-    """Time the float64 oracle on a bounded sample of the workload (host cores)."""
+def cpu_oracle_rate(cfg, M_sample, threads=None, layout="uniform", want_results=False):
+    """Time the float64 oracle on a bounded sample of the workload (host cores; `threads` BLAS
+    threads, default all).  want_results: also return the oracle's ScoreResult per search."""
     from threadpoolctl import threadpool_limits
     from oracle import gp
     from workloads import gen
-    cores = os.cpu_count()
-    w = gen.make(cfg, M=M_sample)
+    cores = threads or os.cpu_count()
+    w = gen.make(cfg, M=M_sample, layout=layout)
+    res = []
     with threadpool_limits(limits=cores):
         t0 = time.perf_counter()
         for s, Xs in zip(w.searches, w.Xstar):
             m = gp.fit(s.X, s.y, s.lengthscale, s.sf2, s.sn2, w.kernel)
-            gp.score(m, Xs)
+            res.append(gp.score(m, Xs))
         dt = time.perf_counter() - t0
     total = sum(x.shape[0] for x in w.Xstar)
+    if want_results:
+        return total / dt, cores, total, dt, res
     return total / dt, cores, total, dt
+
+
+def cpu_model():
+    """Host CPU model name (lscpu 'Model name', else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def spawn_ranks(ngpus):
+    """`bench.py --gpus N` without a torchrun environment: re-exec under torch.distributed.run
+    with N ranks on this node (127.0.0.1 rendezvous), as the driver launches it."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={ngpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -161,15 +196,26 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 20,
                     help="candidates the CPU oracle scores for cpu_baseline (~10-15 s at config 2)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: fixed candidates per GPU; strong: the config's M split over N")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:  # the NCCL communicator init lines (stderr) document the H10 transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     from workloads import gen
     S0, n0, d0, M0 = gen.CONFIG_SHAPES[args.config]
+    # weak scaling: configs 1-3 keep their M per GPU, config 4 its 2^19 per-GPU shard; strong
+    # scaling: the config's whole pool split over the ranks
     per_gpu = M0 if args.config != 4 else M0 // 8
+    if args.scaling == "strong":
+        per_gpu = -(-M0 // world)
 
     if args.impl == "reference":
         if rank != 0:
@@ -216,7 +262,7 @@ def main():
     ctx.set_score_impl(args.score_impl)
 
     # ---- inputs (seeded, host -> HBM once, untimed)
-    M_total = per_gpu * world
+    M_total = M0 if args.scaling == "strong" else per_gpu * world
     w = gen.make(args.config, M=M_total, rank=rank, world=world, layout=args.layout)
     S = w.S
     n = [s.X.shape[0] for s in w.searches]
@@ -247,6 +293,10 @@ def main():
         idx, ei = ctx.score_argmax(m, Xs_pin, m_off, base)
         m.free()
         return idx, ei
+
+    def step_score(m):
+        """score-only: the fitted model stays resident (SURVEY.md §8(d) primary scaling metric)"""
+        return ctx.score_argmax(m, Xsd, m_off, base)
 
     def timed(step, K, W, profile=False):
         for _ in range(W):
@@ -284,6 +334,10 @@ def main():
     _, _, kt, _ = timed(step_device, args.steps, args.warmup, profile=True)
     # ---- end-to-end through the C ABI with host buffers
     T_e2e, _, _, _ = timed(step_host, args.steps, args.warmup)
+    # ---- score-only (model resident, fit outside the timed region): H6-H10 alone
+    m_res = ctx.fit(n, d, Xd, yd, lsd, sf2d, sn2d, kernel=w.kernel)
+    T_score, _, _, _ = timed(lambda: step_score(m_res), args.steps, args.warmup)
+    m_res.free()
 
     def vmax(x):
         if world == 1:
@@ -292,13 +346,19 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
-    T_dev, T_e2e = vmax(T_dev), vmax(T_e2e)
+    T_dev, T_e2e, T_score = vmax(T_dev), vmax(T_e2e), vmax(T_score)
     fast_n, fast_ms = kt["fast"]
     fast_ms = vmax(fast_ms)
-    # every rank scores its local shard of every search (weak scaling): all candidates, all ranks
-    total_cands = local_cands * world * args.steps
+    # every rank scores its local shard of every search: the candidates of all ranks per step
+    global_cands = local_cands
+    if world > 1:
+        tt = torch.tensor([local_cands], dtype=torch.int64, device=dev)
+        dist.all_reduce(tt)
+        global_cands = int(tt.item())
+    total_cands = global_cands * args.steps
     value = total_cands / (T_dev / 1e3)
     e2e_value = total_cands / (T_e2e / 1e3)
+    score_value = total_cands / (T_score / 1e3)
     idx, ei = step_device()
     if rank == 0:
         peaks = load_peaks()
@@ -306,15 +366,22 @@ def main():
                                                                              "cuda-core")
         Fc = sum(flops_per_candidate(nn, dd) * x.shape[0] for nn, dd, x in zip(n, d, w.Xstar))
         achieved = Fc / (fast_ms / fast_n / 1e3) / 1e12  # TFLOP/s of the fast-phase kernel
+        clocks = clk.summary()
+        # the burst peak applies when the clocks stayed at max with no cap during the timed
+        # region (the kernel runs in ~0.1-3 ms bursts); else the sustained one
+        capped = bool(clocks["reasons"]) or not (clocks["sm_mhz"] and clocks["sm_max_mhz"] and
+                                                 clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
         if impl_used.startswith("tcgen05"):
-            peak = peaks["bf16_sus"]
+            peak = peaks["bf16_sus"] if capped else peaks["bf16"]
             tr = profiled_traffic("score_tcs" if impl_used == "tcgen05-stream" else "score_tc",
                                   args.config)
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": tr[0] if tr else None,
                     "traffic_src": tr[1] if tr else None,
                     "algorithmic_bytes": int(sum(4 * dd * x.shape[0] for dd, x in zip(d, w.Xstar))),
-                    "peak_src": f"{peaks['src']} bf16 dense sustained (fp16 same rate)"}
+                    "peak_src": f"{peaks['src']} bf16 dense "
+                                f"{'sustained' if capped else 'burst (clocks at max, no cap)'}"
+                                " (fp16 same rate)"}
         elif impl_used == "fp64-direct":
             peak = 148 * 64 * 2 * peaks["sm_mhz"] * 1e6 / 1e12
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -327,36 +394,66 @@ def main():
                     "frac": achieved / peak, "traffic": None,
                     "peak_src": "FP32 FFMA: 148 SM x 128 lanes x 2 flop x max SM clock"}
         cpu = None
+        oracle_check = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, cores, tot_c, dt = cpu_oracle_rate(args.config, args.cpu_sample)
+            rate, cores, tot_c, dt, ores = cpu_oracle_rate(args.config, args.cpu_sample,
+                                                           layout=args.layout, want_results=True)
+            # 1-thread figure on a smaller sample (SURVEY.md §8(d) oracle timing)
+            m1 = max(4096, args.cpu_sample // 16)
+            rate1, _, tot1, dt1 = cpu_oracle_rate(args.config, m1, threads=1, layout=args.layout)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{tot_c} candidates of {gen.CONFIG_NAMES[args.config]} "
-                             f"(fit + score + argmax, float64 numpy, {dt:.1f} s)"}
+                             f"(fit + score + argmax, float64 numpy, {dt:.1f} s)",
+                   "cpu_model": cpu_model(),
+                   "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                                  "sample": f"{tot1} candidates ({dt1:.1f} s)"}}
+            # the GPU's suggestion vs the oracle's argmax on the same candidates, where the
+            # sample is the whole timed workload (reading R11: index parity where the gap is
+            # decisive, else a pick within 1e-3 of the oracle's maximum)
+            if tot_c == local_cands:
+                ok, detail = True, []
+                for si, r in enumerate(ores):
+                    gi = int(idx[si])
+                    top = float(r.ei_all.max())
+                    exact = r.gap_rel > 1e-3 and top >= 1e-30
+                    good = (gi == r.idx) if exact else (
+                        0 <= gi < r.ei_all.size and (top < 1e-30 or r.ei_all[gi] >= top * (1 - 1e-3)))
+                    ok = ok and good
+                    if si < 4:
+                        detail.append({"gpu_idx": gi, "oracle_idx": r.idx,
+                                       "gap_rel": r.gap_rel, "decisive": exact})
+                oracle_check = {"oracle_idx_match": ok, "searches": len(ores),
+                                "first": detail}
         h2d = Xh.nbytes + yh.nbytes + lsh.nbytes + sf2h.nbytes + sn2h.nbytes + Xsh.nbytes
         d2h = 8 * S + 4 + 192 * S
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": T_dev / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": ("f16x3+f32+f64" if impl_used.startswith("tcgen05") else
                       "f64" if impl_used == "fp64-direct" else "f32+f64"),
             "data": "synthetic",
             "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
                        "M_per_gpu": per_gpu, "M_global": M_total,
-                       "candidates_per_step": local_cands * world,
+                       "candidates_per_step": global_cands,
                        "kernel": "matern52" if w.kernel == 1 else "rbf",
                        "layout": args.layout, "l2": "flushed between steps (256 MiB write)",
                        "scoring": impl_used},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
-            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "score_only": {"value": score_value, "unit": UNIT,
+                           "ms_per_step": T_score / args.steps,
+                           "what": "ei_score_argmax alone on a resident model (H6-H10)"},
+            "clocks": clocks, "gpu_launches": int(launches),
             "breakdown_ms_per_step": {k: kt[k][1] / args.steps for k in kt},
             "breakdown_src": "second timed pass of the same steps with CUDA events around each "
                              "library kernel (events perturb the step by ~6 %, so the value's "
                              "pass runs without them)",
             "refined_per_step": refined / args.steps,
             "result": {"idx": int(idx[0]), "ei": float(ei[0])},
+            "oracle_check": oracle_check,
+            "collectives": ctx.collectives,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

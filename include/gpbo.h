@@ -69,9 +69,11 @@ typedef struct gpbo_model gpbo_model;
  * gpbo_nccl_unique_id: writes a fresh NCCL unique id (GPBO_NCCL_ID_BYTES bytes) to out; call on
  *   rank 0 and broadcast it (e.g. torch.distributed.broadcast_object_list) to the other ranks.
  * gpbo_ctx_create: binds to CUDA device `device` and stream `cuda_stream` (a cudaStream_t; NULL
- *   = the legacy default stream).  nranks > 1 creates an NCCL communicator from
- *   `nccl_unique_id` (must be non-NULL then; NULL is required when nranks == 1).  All ranks
- *   must call it collectively.  On success *out owns the communicator and scratch buffers. */
+ *   = the legacy default stream).  A non-NULL `nccl_unique_id` creates an NCCL communicator of
+ *   `nranks` ranks (required when nranks > 1; with nranks == 1 it gives a 1-rank communicator,
+ *   so the H10 all-reduce path also runs on one GPU); NULL with nranks == 1 = no communicator.
+ *   All ranks must call it collectively.  On success *out owns the communicator and scratch
+ *   buffers. */
 gpbo_status gpbo_nccl_unique_id(void *out);
 gpbo_status gpbo_ctx_create(int device, void *cuda_stream, int nranks, int rank,
                             const void *nccl_unique_id, gpbo_ctx **out);
@@ -120,6 +122,13 @@ gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *args, gpbo_model **out,
  * gp_posterior, gp_model_stats/export) or explicitly by gp_model_sync, which writes status[S] /
  * jitter_k[S] (may be NULL) and returns what gp_fit would have returned (GPBO_EINVAL if an input
  * was non-finite; the model then scores nothing and must still be freed). */
+/* Lifetime: with mem = GPBO_DEVICE the fit kernels read the caller's X, y, lengthscale,
+ * signal_var and noise_var asynchronously on ctx's stream, so those device buffers must stay
+ * valid (not freed, not reused by an allocator on another stream) until ctx's stream has passed
+ * the fit -- i.e. until the next synchronising call on ctx returns.  Host inputs (GPBO_HOST) are
+ * staged by stream-ordered copies: pageable memory may be reused on return, pinned (page-locked)
+ * memory only after the stream has passed the fit.  The Python binding keeps references to the
+ * input arrays on the Model until it is freed. */
 gpbo_status gp_fit_async(gpbo_ctx *ctx, const gpbo_fit_args *args, gpbo_model **out);
 gpbo_status gp_model_sync(gpbo_ctx *ctx, const gpbo_model *model, int32_t *status,
                           int32_t *jitter_k);
@@ -223,6 +232,9 @@ gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
 
 /* Number of CUDA kernels the library launched on ctx since creation (for bench accounting). */
 int64_t gpbo_launch_count(const gpbo_ctx *ctx);
+
+/* ncclAllReduce calls (H10) ctx has issued on its communicator since creation. */
+int64_t gpbo_collective_count(const gpbo_ctx *ctx);
 
 /* Candidates the last ei_score_argmax call on ctx re-scored in the float64 refine phase
  * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */

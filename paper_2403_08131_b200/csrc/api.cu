@@ -40,6 +40,7 @@ struct gpbo_ctx {
   cudaEvent_t aux_ev = nullptr;   // recorded after the upload that reads aux_h
   size_t aux_cap = 0;
   int64_t launches = 0;
+  int64_t collectives = 0;  // ncclAllReduce calls issued on comm
   // optional per-kernel CUDA-event timing (gpbo_set_profiling): kinds fit / fast / refine / pack
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -274,19 +275,6 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   if (ctx->score_impl == 2 && !use_tc)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
   const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;  // (direct: any)
-  if (use_tc && !model->packed) {
-    KernTimer t(ctx, kKernPack);
-    CK(gpbo::launch_pack_tc(model->meta_d, model->S, model->Linv64, model->Xs64, model->alpha64,
-                            model->ls32, model->img, ctx->stream));
-    ctx->launches += 1;
-    model->packed = true;
-  }
-  if (!use_tc && !direct && !model->simt_ready) {
-    CK(gpbo::launch_simt_operands(model->meta_d, model->S, model->X32, model->ls32,
-                                  model->Linv64, model->Xs32, model->LT32, ctx->stream));
-    ctx->launches += 1;
-    model->simt_ready = true;
-  }
   h_tiles[0] = 0;
   int64_t xo = 0;
   for (int i = 0; i < S; ++i) {
@@ -317,6 +305,21 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   CK(cudaMemcpyAsync(ctx->aux_d, ctx->aux_h, bytes, cudaMemcpyHostToDevice, ctx->stream));
   if (!ctx->aux_ev) CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(ctx->aux_ev, ctx->stream));
+  // operand preparation after the upload, so the scoring kernel directly follows the pack on the
+  // stream: its programmatic dependent launch overlaps barrier init / TMEM allocation with it
+  if (use_tc && !model->packed) {
+    KernTimer t(ctx, kKernPack);
+    CK(gpbo::launch_pack_tc(model->meta_d, model->S, model->Linv64, model->Xs64, model->alpha64,
+                            model->ls32, model->img, ctx->stream));
+    ctx->launches += 1;
+    model->packed = true;
+  }
+  if (!use_tc && !direct && !model->simt_ready) {
+    CK(gpbo::launch_simt_operands(model->meta_d, model->S, model->X32, model->ls32,
+                                  model->Linv64, model->Xs32, model->LT32, ctx->stream));
+    ctx->launches += 1;
+    model->simt_ready = true;
+  }
   unsigned long long *keys_d = (unsigned long long *)((char *)ctx->aux_d + meta_bytes);
   unsigned int *thr_d = (unsigned int *)(keys_d + S);
   unsigned int *count_d = thr_d + S;
@@ -447,8 +450,10 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
                              Outputs(), host_src);
   if (st) return st;
   unsigned long long *keys_d = ctx->cur_keys_d;
-  if (ctx->nranks > 1)
+  if (ctx->comm) {  // H10: every rank ends with the same per-search keys
     NK(ncclAllReduce(keys_d, keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    ctx->collectives += 1;
+  }
   // keys, thresholds and the refine count in one read-back
   CK(cudaMemcpyAsync(ctx->keys_h, keys_d, ctx->cur_key_bytes, cudaMemcpyDeviceToHost,
                      ctx->stream));
@@ -498,7 +503,7 @@ gpbo_status gpbo_nccl_unique_id(void *out) {
 gpbo_status gpbo_ctx_create(int device, void *cuda_stream, int nranks, int rank,
                             const void *nccl_unique_id, gpbo_ctx **out) {
   if (!out || nranks < 1 || rank < 0 || rank >= nranks) return GPBO_EINVAL;
-  if ((nranks > 1) != (nccl_unique_id != nullptr)) return GPBO_EINVAL;
+  if (nranks > 1 && nccl_unique_id == nullptr) return GPBO_EINVAL;
   *out = nullptr;
   gpbo_ctx *ctx = new gpbo_ctx();
   ctx->device = device;
@@ -519,7 +524,7 @@ gpbo_status gpbo_ctx_create(int device, void *cuda_stream, int nranks, int rank,
     if (!strcmp(e, "simt")) ctx->score_impl = 1;
     if (!strcmp(e, "tc")) ctx->score_impl = 2;
   }
-  if (nranks > 1) {
+  if (nccl_unique_id != nullptr) {  // (a 1-rank communicator is allowed: same code path)
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     if (ncclCommInitRank(&ctx->comm, nranks, id, rank) != ncclSuccess) {
@@ -562,6 +567,8 @@ const char *gpbo_last_error(const gpbo_ctx *ctx) { return ctx ? ctx->err.c_str()
 int64_t gpbo_launch_count(const gpbo_ctx *ctx) { return ctx ? ctx->launches : -1; }
 
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_refine : -1; }
+
+int64_t gpbo_collective_count(const gpbo_ctx *ctx) { return ctx ? ctx->collectives : -1; }
 
 int gpbo_last_score_impl(const gpbo_ctx *ctx) { return ctx ? ctx->last_impl : -1; }
 
@@ -735,8 +742,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream,
                          m->nmax <= gpbo::kFitSmemMaxN));
   }
-  ctx->launches += 2;
-  ctx->launches += 1;
+  ctx->launches += 2;  // gram_kernel + fit_kernel
   // the tcgen05 operand images are packed by the first tcgen05 scoring call (run_score): small
   // problems scored by the float64 direct kernel never need them
   if (!wait) {  // gp_fit_async: results stay on the device until gp_model_sync / scoring

@@ -26,6 +26,7 @@
 //      it and the trailing triangle), 8 x 8 DMMA tiles dealt to the warps.  Warp 0 updates the
 //      next diagonal block first and runs its D while the other warps finish T (look-ahead).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 
@@ -721,14 +722,24 @@ simt_operands_kernel(const SearchMeta *__restrict__ meta, const float *__restric
 
 }  // namespace
 
+constexpr int kMaxDevices = 64;
+
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
                        SearchMeta *meta_out, cudaStream_t stream, bool pdl) {
-  static int smem_set = -1;  // the attribute call costs microseconds: only when it grows
-  if (smem_bytes > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(fit_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  // the attribute call costs microseconds: only when it grows.  The attribute is per device, so
+  // is the cache (one ctx per device may run in one process, on different threads)
+  static std::atomic<int> smem_set[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices || smem_bytes > smem_set[dev].load()) {
+    e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
-    smem_set = smem_bytes;
+    if (dev >= 0 && dev < kMaxDevices) {
+      int cur = smem_set[dev].load();
+      while (smem_bytes > cur && !smem_set[dev].compare_exchange_weak(cur, smem_bytes)) {
+      }
+    }
   }
   // programmatic dependent launch after the Gram pre-pass (see fit_body's griddepcontrol.wait);
   // the caller enables it for shared-memory working matrices only (n <= 216: fit 0.145 ->

@@ -137,17 +137,21 @@ refine_kernel(const RefineLaunch p) {
     if (lane != 0) vv = 0.0;
     vv = block_sum2(vv, red);
     if (tid == 0) {
+      // a non-finite candidate row (NaN / inf input, or a row masked by the generator's dedup)
+      // makes mu or |v|^2 non-finite: it is never a suggestion and its outputs are NaN (fmax
+      // would otherwise turn NaN into sig = 0, EI = 0 and a valid key)
+      const bool fin = isfinite(mu) && isfinite(vv);
       const double var64 = fmax((double)m.sf2 - vv, 0.0);
       const double sig = sqrt(var64);
       const double imp = resolve_best(p.best[s], m) - mu;
-      const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
+      const double ei = !fin ? NAN : sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
       if (p.list) {
-        const unsigned long long key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));
+        const unsigned long long key = fin ? make_key((float)ei, (uint64_t)(p.m_base[s] + row)) : 0ull;
         if (key) atomicMax(p.keys + s, key);
       } else {
-        if (p.out_mu) p.out_mu[e] = (float)(m.mean + m.std * mu);
-        if (p.out_var) p.out_var[e] = (float)(m.std * m.std * var64);
-        if (p.out_ei) p.out_ei[e] = (float)(m.std * ei);
+        if (p.out_mu) p.out_mu[e] = fin ? (float)(m.mean + m.std * mu) : NAN;
+        if (p.out_var) p.out_var[e] = fin ? (float)(m.std * m.std * var64) : NAN;
+        if (p.out_ei) p.out_ei[e] = fin ? (float)(m.std * ei) : NAN;
       }
     }
   }
@@ -248,11 +252,12 @@ refine_split_kernel(const RefineLaunch p) {
     if (rank == 0 && tid == 0) {
       double v2 = 0.0;
       for (int r = 0; r < kSplit; ++r) v2 += part[r];
+      const bool fin = isfinite(mu) && isfinite(v2);  // non-finite rows: no key (refine_kernel)
       const double var64 = fmax((double)m.sf2 - v2, 0.0);
       const double sig = sqrt(var64);
       const double imp = resolve_best(p.best[s], m) - mu;
       const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
-      const unsigned long long key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));
+      const unsigned long long key = fin ? make_key((float)ei, (uint64_t)(p.m_base[s] + row)) : 0ull;
       if (key) atomicMax(p.keys + s, key);
     }
     cluster.sync();  // CTA 0 has read the partials before the next entry overwrites them
@@ -320,15 +325,18 @@ direct_kernel(const RefineLaunch p, int S, int64_t rows) {
         vv += __shfl_xor_sync(0xffffffffu, vv, o);
       }
       if (lane == 0) {
+        // non-finite rows (NaN input, dedup-masked candidates) are invalid: no key, NaN outputs
+        // -- as the fast-phase kernels (kFlagInvalid / isfinite in finish_fast)
+        const bool fin = isfinite(mu) && isfinite(vv);
         const double var64 = fmax(sf2 - vv, 0.0);
         const double sig = sqrt(var64);
         const double imp = resolve_best(p.best[s], m) - mu;
         const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
         if (posterior) {
-          if (p.out_mu) p.out_mu[g] = (float)(m.mean + m.std * mu);
-          if (p.out_var) p.out_var[g] = (float)(m.std * m.std * var64);
-          if (p.out_ei) p.out_ei[g] = (float)(m.std * ei);
-        } else {
+          if (p.out_mu) p.out_mu[g] = fin ? (float)(m.mean + m.std * mu) : NAN;
+          if (p.out_var) p.out_var[g] = fin ? (float)(m.std * m.std * var64) : NAN;
+          if (p.out_ei) p.out_ei[g] = fin ? (float)(m.std * ei) : NAN;
+        } else if (fin) {
           key = make_key((float)ei, (uint64_t)(p.m_base[s] + row));
         }
       }

@@ -580,8 +580,19 @@ cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int grid = std::min(num_sms, total_tiles);
-  score_tcs_kernel<<<grid, kThreads, smem, stream>>>(p, tile_lo, total_tiles, kb_max, d_max);
-  return cudaGetLastError();
+  // programmatic dependent launch after the operand pack (the kernel's griddepcontrol.wait
+  // precedes every read of the image), as score_tc
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, score_tcs_kernel, p, tile_lo, total_tiles, kb_max, d_max);
 }
 
 }  // namespace gpbo

@@ -71,6 +71,7 @@ def load():
         "ei_score_argmax": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "gpbo_launch_count": (i64, [vp]),
         "gpbo_last_refine_count": (i64, [vp]),
+        "gpbo_collective_count": (i64, [vp]),
         "gpbo_last_score_impl": (C.c_int, [vp]),
         "gpbo_set_profiling": (C.c_int, [vp, C.c_int]),
         "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
@@ -98,7 +99,7 @@ def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
             "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_stats", "gp_model_export",
-            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
+            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
             "gpbo_tc_bench", "gpbo_space_create", "gpbo_space_free", "gpbo_space_dim",
@@ -137,6 +138,7 @@ class Model:
         self.ctx, self.handle, self.S = ctx, handle, S
         self.n, self.d = list(n), list(d)
         self._status, self._jitter_k = status, jitter_k
+        self._inputs = None
 
     def sync(self):
         """gp_model_sync: fetch the per-search statuses of an asynchronous fit."""
@@ -175,6 +177,7 @@ class Model:
         if self.handle:
             load().gp_model_free(self.handle)
             self.handle = None
+        self._inputs = None
 
     def __del__(self):
         try:
@@ -233,6 +236,11 @@ class Context:
         return int(load().gpbo_launch_count(self.handle))
 
     @property
+    def collectives(self):
+        """ncclAllReduce calls issued on this ctx's communicator (H10)."""
+        return int(load().gpbo_collective_count(self.handle))
+
+    @property
     def last_refine_count(self):
         return int(load().gpbo_last_refine_count(self.handle))
 
@@ -275,7 +283,10 @@ class Context:
         h = C.c_void_p()
         if not wait:
             _check(self, lib.gp_fit_async(self.handle, C.byref(args), C.byref(h)))
-            return Model(self, h, S, n_a, d_a, None, None)
+            m = Model(self, h, S, n_a, d_a, None, None)
+            # the kernels read the inputs asynchronously (include/gpbo.h, gp_fit_async lifetime)
+            m._inputs = (X, y, lengthscale, signal_var, noise_var)
+            return m
         status = np.zeros(S, np.int32)
         jk = np.zeros(S, np.int32)
         st = lib.gp_fit(self.handle, C.byref(args), C.byref(h), status.ctypes.data,
