@@ -236,6 +236,18 @@ int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 /* ncclAllReduce calls (H10) ctx has issued on its communicator since creation. */
 int64_t gpbo_collective_count(const gpbo_ctx *ctx);
 
+/* Soundness check of the last argmax call (ei_score_argmax / bo_suggest_batch): the number of
+ * refined or audited candidates whose float64 EI fell outside the fast phase's EI bracket.  A
+ * search with any violation was re-scored exactly (every row in float64) before its result was
+ * decoded, so a failed error bound costs time, never a wrong suggestion.  Expected: 0. */
+int64_t gpbo_last_bracket_violations(const gpbo_ctx *ctx);
+
+/* Test hook: multiply the fast phase's error bounds (dmu, dvar) by `scale` (default 1; 0 makes
+ * the EI bracket nearly zero-width).  A negative scale keeps the bounds but halves every EI
+ * bracket -- deliberately unsound, so the violation path above is exercised.  GPBO_EINVAL for a
+ * non-finite scale. */
+gpbo_status gpbo_debug_bound_scale(gpbo_ctx *ctx, float scale);
+
 /* Candidates the last ei_score_argmax call on ctx re-scored in the float64 refine phase
  * (those whose fast-phase EI upper bound reached the running per-search maximum lower bound). */
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);

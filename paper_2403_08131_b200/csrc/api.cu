@@ -26,8 +26,11 @@ struct gpbo_ctx {
   unsigned long long *keys_d = nullptr;  // [cap] keys | [cap] u32 thresholds | u32 list count
   unsigned long long *keys_h = nullptr;
   int keys_cap = 0;
-  unsigned long long *cur_keys_d = nullptr;  // this call's keys | thr | count (in aux_d)
+  unsigned long long *cur_keys_d = nullptr;  // this call's keys | viol | thr | count (in aux_d)
   size_t cur_key_bytes = 0;
+  const int64_t *cur_p_off = nullptr;  // this call's device m_off | m_base | x_off | best (aux_d)
+  int64_t last_violations = 0;  // bracket violations found by the last argmax call
+  float bound_scale = 1.f;      // error-bound multiplier of the fast phase (test hook)
   gpbo::RefineEntry *list_d = nullptr;   // refine list of the argmax path
   size_t list_cap = 0;
   void *stage_d = nullptr;  // device staging of host-resident candidates / outputs
@@ -203,7 +206,7 @@ gpbo_status ensure_keys(gpbo_ctx *ctx, int S) {
   if (ctx->keys_h) CK(cudaFreeHost(ctx->keys_h));
   int cap = std::max(S, 64);
   CK(cudaMalloc(&ctx->keys_d, cap * (sizeof(unsigned long long) + 4) + 16));
-  CK(cudaMallocHost(&ctx->keys_h, (2 * cap + 2) * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&ctx->keys_h, (3 * cap + 2) * sizeof(unsigned long long)));
   ctx->keys_cap = cap;
   return GPBO_OK;
 }
@@ -235,10 +238,11 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
                       const double *best_std, int mode, const Outputs &out,
                       const float *host_src = nullptr) {
   // aux layout: m_off[S+1] i64 | m_base[S] i64 | x_off[S] i64 | best[S] f64 | tile_first[S+1] i32
-  // | (8-aligned) keys[S] u64 | thr[S] u32 | list count u32 -- the key / threshold / count words
-  // are zeroed by the same upload (no separate memset) and read back by one copy
+  // | (8-aligned) keys[S] u64 | viol[S] u64 | thr[S] u32 | list count u32 -- the key /
+  // violation / threshold / count words are zeroed by the same upload (no separate memset) and
+  // read back by one copy; keys and viol are adjacent so one all-reduce(max) covers both
   const size_t meta_bytes = ((size_t)(S + 1) * 8 + (size_t)S * 24 + (size_t)(S + 1) * 4 + 7) & ~(size_t)7;
-  const size_t key_bytes = (size_t)S * 12 + 4;
+  const size_t key_bytes = (size_t)S * 20 + 4;
   const size_t bytes = meta_bytes + key_bytes;
   gpbo_status st = ensure_aux(ctx, bytes + 64);
   if (st) return st;
@@ -321,10 +325,12 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     model->simt_ready = true;
   }
   unsigned long long *keys_d = (unsigned long long *)((char *)ctx->aux_d + meta_bytes);
-  unsigned int *thr_d = (unsigned int *)(keys_d + S);
+  unsigned long long *viol_d = keys_d + S;
+  unsigned int *thr_d = (unsigned int *)(keys_d + 2 * S);
   unsigned int *count_d = thr_d + S;
   ctx->cur_keys_d = keys_d;
   ctx->cur_key_bytes = key_bytes;
+  ctx->cur_p_off = (const int64_t *)ctx->aux_d;
   char *dptr = (char *)ctx->aux_d;
   gpbo::ScoreLaunch p{};
   p.meta = model->meta_d + s_first;
@@ -350,6 +356,8 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.dbg_mu = out.dbg[0]; p.dbg_dmu = out.dbg[1]; p.dbg_var = out.dbg[2];
   p.dbg_dvar = out.dbg[3]; p.dbg_eilo = out.dbg[4]; p.dbg_eihi = out.dbg[5];
   p.trace = ctx->trace;
+  p.bound_scale = ctx->bound_scale >= 0.f ? ctx->bound_scale : 1.f;
+  p.break_bracket = ctx->bound_scale < 0.f ? 1 : 0;
   const int tiles = h_tiles[S];
   ctx->last_impl = direct ? 4 : use_tcs ? 3 : use_tc ? 2 : 1;
   const int64_t floats_all = xo;
@@ -424,6 +432,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   r.Linv64 = model->Linv64;
   r.keys = keys_d;
   r.thr = thr_d;
+  r.viol = viol_d;
   if (mode == gpbo::kModeArgmax) {
     r.list = ctx->list_d;
     r.list_count = count_d;
@@ -450,11 +459,12 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
                              Outputs(), host_src);
   if (st) return st;
   unsigned long long *keys_d = ctx->cur_keys_d;
-  if (ctx->comm) {  // H10: every rank ends with the same per-search keys
-    NK(ncclAllReduce(keys_d, keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+  unsigned long long *viol_d = keys_d + S;
+  if (ctx->comm) {  // H10: every rank ends with the same per-search keys (and violation flags)
+    NK(ncclAllReduce(keys_d, keys_d, 2 * S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
     ctx->collectives += 1;
   }
-  // keys, thresholds and the refine count in one read-back
+  // keys, violations, thresholds and the refine count in one read-back
   CK(cudaMemcpyAsync(ctx->keys_h, keys_d, ctx->cur_key_bytes, cudaMemcpyDeviceToHost,
                      ctx->stream));
   if (model->meta_pending)  // the fit results ride along with the keys
@@ -464,7 +474,49 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
   model->meta_pending = false;
   CK(cudaGetLastError());
   harvest_events(ctx);
-  ctx->last_refine = (int64_t)((const unsigned int *)(ctx->keys_h + S))[S];
+  ctx->last_refine = (int64_t)((const unsigned int *)(ctx->keys_h + 2 * S))[S];
+  // Soundness check of the argmax filter: a refined (or audited) candidate whose float64 EI lies
+  // outside its fast-phase bracket means an error bound failed, so the filter may have dropped
+  // the true winner.  Such a search is re-scored exactly -- every local row in float64, the
+  // oracle's arithmetic -- and, across ranks, combined again (the flags were max-reduced with the
+  // keys, so every rank takes the same decision and joins the second all-reduce).
+  ctx->last_violations = 0;
+  bool any_viol = false;
+  for (int s = 0; s < S; ++s) {
+    ctx->last_violations += (int64_t)ctx->keys_h[S + s];
+    any_viol = any_viol || ctx->keys_h[S + s] != 0ull;
+  }
+  if (any_viol) {
+    gpbo::RefineLaunch r{};
+    r.meta = model->meta_d;
+    r.Xstar = xd;
+    r.m_off = ctx->cur_p_off; r.m_base = ctx->cur_p_off + (S + 1); r.x_off = r.m_base + S;
+    r.best = (const double *)(r.x_off + S);
+    r.Xs64 = model->Xs64;
+    r.ls32 = model->ls32;
+    r.alpha64 = model->alpha64;
+    r.Linv64 = model->Linv64;
+    r.keys = keys_d;
+    r.dense_keys = 1;
+    for (int s = 0; s < S; ++s) {
+      if (ctx->keys_h[S + s] == 0ull) continue;
+      const int64_t rows = m_off[s + 1] - m_off[s];
+      const SearchMeta &q = model->meta[s];
+      CK(cudaMemsetAsync(keys_d + s, 0, 8, ctx->stream));
+      if (rows <= 0 || (q.status != GPBO_OK && q.status != GPBO_WDEGENERATE)) continue;
+      r.dense_s = s;
+      r.dense_rows = rows;
+      CK(gpbo::launch_refine(r, rows, ctx->num_sms, model->nmax, ctx->stream));
+      ctx->launches += 1;
+    }
+    if (ctx->comm) {
+      NK(ncclAllReduce(keys_d, keys_d, S, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+      ctx->collectives += 1;
+    }
+    CK(cudaMemcpyAsync(ctx->keys_h, keys_d, S * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+  }
   for (int s = 0; s < S; ++s) {
     const unsigned long long k = ctx->keys_h[s];
     const SearchMeta &q = model->meta[s];
@@ -569,6 +621,16 @@ int64_t gpbo_launch_count(const gpbo_ctx *ctx) { return ctx ? ctx->launches : -1
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_refine : -1; }
 
 int64_t gpbo_collective_count(const gpbo_ctx *ctx) { return ctx ? ctx->collectives : -1; }
+
+int64_t gpbo_last_bracket_violations(const gpbo_ctx *ctx) {
+  return ctx ? ctx->last_violations : -1;
+}
+
+gpbo_status gpbo_debug_bound_scale(gpbo_ctx *ctx, float scale) {
+  if (!ctx || !std::isfinite(scale)) return GPBO_EINVAL;
+  ctx->bound_scale = scale;
+  return GPBO_OK;
+}
 
 int gpbo_last_score_impl(const gpbo_ctx *ctx) { return ctx ? ctx->last_impl : -1; }
 

@@ -72,13 +72,20 @@ struct SearchMeta {
   int64_t kt_off;       // kernel matrix k(X, X) without noise / jitter, tile-packed, in model.Kt64
 };
 
-// Candidate flagged by the fast phase for the float64 refine phase.
+// Candidate flagged by the fast phase for the float64 refine phase.  The refine re-scores it in
+// float64 and checks the fast phase's bracket ei_lo <= EI <= ei_hi (the argmax filter's
+// soundness); a violation re-scores the whole search exactly (api.cu, argmax_tail).
 struct RefineEntry {
-  int32_t s;      // search (launch-relative)
+  uint32_t s;     // search (launch-relative) | kEntryAudit
   uint32_t row;   // local candidate row
-  float var;      // standardised latent variance from the fast phase (float32-accurate)
+  float ei_lo;    // lower bound of EI~ from the fast phase (0 when not evaluated)
   float ei_hi;    // upper bound of EI~ from the fast phase
 };
+// Audit entry: a candidate the fast phase did NOT flag, sampled deterministically (1 in 2^14 by
+// a multiplicative hash of its global index: (u32)(gidx * 0x9E3779B1) >> kAuditShift == 0) so the
+// refine also checks the upper bound that excluded it; never skipped by the threshold test.
+constexpr uint32_t kEntryAudit = 0x80000000u;
+constexpr uint32_t kAuditShift = 18;
 
 enum ScoreMode : int32_t {
   kModeArgmax = 0,     // fast phase flags candidates, refine computes the final keys
@@ -111,6 +118,8 @@ struct ScoreLaunch {
   uint32_t list_cap;
   float *dbg_mu, *dbg_dmu, *dbg_var, *dbg_dvar, *dbg_eilo, *dbg_eihi;  // debug mode
   unsigned long long *trace;   // optional clock64 event trace of CTA 0 (gpbo_debug_trace)
+  float bound_scale;           // error-bound multiplier: 1 (test hook gpbo_debug_bound_scale)
+  int32_t break_bracket;       // test hook: halve every EI bracket (deliberately unsound)
 };
 
 // Float64 refine phase (refine.cu).
@@ -131,6 +140,8 @@ struct RefineLaunch {
   int64_t dense_rows;          // posterior mode: number of rows
   const float *dense_var;      // posterior mode: var~ per row from the fast phase
   float *out_mu, *out_var, *out_ei;
+  int32_t dense_keys;          // dense mode: argmax keys of every row instead of outputs
+  unsigned long long *viol;    // [S] bracket violations found by the refine (argmax mode)
 };
 
 }  // namespace gpbo

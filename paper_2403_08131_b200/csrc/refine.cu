@@ -43,6 +43,13 @@ __device__ __forceinline__ double tau64(double z) {
   return exp(-0.5 * z * z) * (inv_sqrt2pi - 0.5 * x * erfcx(x * inv_sqrt2));
 }
 
+// The fast phase's EI bracket must contain the float64 EI (up to float32 rounding of the
+// bounds); anything else means an error bound failed and the argmax filter may have dropped the
+// winner -- the caller re-scores the search exactly (api.cu, argmax_tail).
+__device__ __forceinline__ bool bracket_violated(double ei, float lo, float hi) {
+  return ei > (double)hi * (1.0 + 1e-6) + 1e-37 || ei < (double)lo * (1.0 - 1e-6) - 1e-37;
+}
+
 __device__ __forceinline__ double block_sum2(double v, double *red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -67,10 +74,13 @@ refine_kernel(const RefineLaunch p) {
   for (int64_t e = blockIdx.x; e < nent; e += gridDim.x) {
     int s;
     uint32_t row;
+    RefineEntry en{};
     if (p.list) {
-      const RefineEntry en = p.list[e];
-      if (en.ei_hi < __uint_as_float(p.thr[en.s])) continue;  // cannot be the argmax (uniform)
-      s = en.s; row = en.row;
+      en = p.list[e];
+      s = (int)(en.s & ~kEntryAudit);
+      // cannot be the argmax (uniform over the block); audit entries are always checked
+      if (!(en.s & kEntryAudit) && en.ei_hi < __uint_as_float(p.thr[s])) continue;
+      row = en.row;
     } else {
       s = p.dense_s; row = (uint32_t)e;
     }
@@ -145,9 +155,10 @@ refine_kernel(const RefineLaunch p) {
       const double sig = sqrt(var64);
       const double imp = resolve_best(p.best[s], m) - mu;
       const double ei = !fin ? NAN : sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
-      if (p.list) {
+      if (p.list || p.dense_keys) {
         const unsigned long long key = fin ? make_key((float)ei, (uint64_t)(p.m_base[s] + row)) : 0ull;
         if (key) atomicMax(p.keys + s, key);
+        if (p.list && fin && bracket_violated(ei, en.ei_lo, en.ei_hi)) atomicAdd(p.viol + s, 1ull);
       } else {
         if (p.out_mu) p.out_mu[e] = fin ? (float)(m.mean + m.std * mu) : NAN;
         if (p.out_var) p.out_var[e] = fin ? (float)(m.std * m.std * var64) : NAN;
@@ -182,8 +193,9 @@ refine_split_kernel(const RefineLaunch p) {
   const int64_t nent = (int64_t)*p.list_count;
   for (int64_t e = cid; e < nent; e += ncl) {
     const RefineEntry en = p.list[e];
-    if (en.ei_hi < __uint_as_float(p.thr[en.s])) continue;  // uniform over the cluster
-    const int s = en.s;
+    const int s = (int)(en.s & ~kEntryAudit);
+    // uniform over the cluster; audit entries are always checked
+    if (!(en.s & kEntryAudit) && en.ei_hi < __uint_as_float(p.thr[s])) continue;
     const uint32_t row = en.row;
     const SearchMeta &m = p.meta[s];
     const int n = m.n, d = m.d;
@@ -259,6 +271,7 @@ refine_split_kernel(const RefineLaunch p) {
       const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
       const unsigned long long key = fin ? make_key((float)ei, (uint64_t)(p.m_base[s] + row)) : 0ull;
       if (key) atomicMax(p.keys + s, key);
+      if (fin && bracket_violated(ei, en.ei_lo, en.ei_hi)) atomicAdd(p.viol + s, 1ull);
     }
     cluster.sync();  // CTA 0 has read the partials before the next entry overwrites them
   }

@@ -147,6 +147,10 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, const F
       }
     }
   }
+  if (p.break_bracket) {  // test hook (gpbo_debug_bound_scale < 0): a deliberately wrong bracket
+    ei_lo *= 0.5f;
+    ei_hi *= 0.5f;
+  }
   if (p.mode == kModePosterior) {
     if (valid) p.out_var[row0 + row] = var;
     return;
@@ -194,15 +198,19 @@ __device__ __forceinline__ void finish_fast(const ScoreLaunch &p, int s, const F
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
   const float thr_fin = __uint_as_float(s_thr[0]);
   const bool flag = ok && ei_hi > 0.f && ei_hi >= thr_fin;
-  const unsigned int mask = __ballot_sync(0xffffffffu, flag);
+  // audit sample of the candidates the filter excludes (their ei_hi bound is checked too)
+  const bool audit = ok && !flag && ((uint32_t)gidx * 0x9E3779B1u) >> kAuditShift == 0u;
+  const unsigned int mask = __ballot_sync(0xffffffffu, flag || audit);
   if (mask) {
     const int leader = __ffs(mask) - 1;
     unsigned int base = 0;
     if (lane == leader) base = atomicAdd(p.list_count, (unsigned int)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (flag) {
+    if (flag || audit) {
       const unsigned int pos = base + __popc(mask & ((1u << lane) - 1u));
-      if (pos < p.list_cap) p.list[pos] = RefineEntry{s, (uint32_t)row, var, ei_hi};
+      if (pos < p.list_cap)
+        p.list[pos] = RefineEntry{(uint32_t)s | (audit ? kEntryAudit : 0u), (uint32_t)row,
+                                  ei_lo, ei_hi};
     }
   }
 }

@@ -473,8 +473,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const float var = fmaxf(sf2 - s2, 0.f);
         // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for
         // the float16x3 augmented GEMM; margin x4
-        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f);
-        const float dvar = vbk * (sf2 + s2);
+        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f) * p.bound_scale;
+        const float dvar = vbk * (sf2 + s2) * p.bound_scale;
 #ifndef GPBO_EXP_NOFINISH  // timing experiment only
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
                     (flags & kFlagUnsafe) != 0u, 2, 128, 8);

@@ -432,8 +432,8 @@ score_tcs_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int kb_max, 
         const float s2 = vv * vun2;
         const float var = fmaxf(sf2 - s2, 0.f);
         // error bounds as in score_tc.cu
-        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f);
-        const float dvar = vbk * (sf2 + s2);
+        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f) * p.bound_scale;
+        const float dvar = vbk * (sf2 + s2) * p.bound_scale;
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
                     (flags & kFlagUnsafe) != 0u, 2, 128, 8);
       }

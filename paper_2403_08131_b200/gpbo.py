@@ -72,6 +72,8 @@ def load():
         "gpbo_launch_count": (i64, [vp]),
         "gpbo_last_refine_count": (i64, [vp]),
         "gpbo_collective_count": (i64, [vp]),
+        "gpbo_last_bracket_violations": (i64, [vp]),
+        "gpbo_debug_bound_scale": (C.c_int, [vp, C.c_float]),
         "gpbo_last_score_impl": (C.c_int, [vp]),
         "gpbo_set_profiling": (C.c_int, [vp, C.c_int]),
         "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
@@ -99,7 +101,8 @@ def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
             "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_stats", "gp_model_export",
-            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
+            "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_last_bracket_violations",
+            "gpbo_debug_bound_scale", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
             "gpbo_tc_bench", "gpbo_space_create", "gpbo_space_free", "gpbo_space_dim",
@@ -239,6 +242,15 @@ class Context:
     def collectives(self):
         """ncclAllReduce calls issued on this ctx's communicator (H10)."""
         return int(load().gpbo_collective_count(self.handle))
+
+    @property
+    def last_violations(self):
+        """Bracket violations found by the last argmax call (searches re-scored exactly)."""
+        return int(load().gpbo_last_bracket_violations(self.handle))
+
+    def debug_bound_scale(self, scale):
+        """Test hook: multiply the fast phase's error bounds by `scale`."""
+        _check(self, load().gpbo_debug_bound_scale(self.handle, float(scale)))
 
     @property
     def last_refine_count(self):
