@@ -134,6 +134,66 @@ gpbo_status gp_model_sync(gpbo_ctx *ctx, const gpbo_model *model, int32_t *statu
                           int32_t *jitter_k);
 void gp_model_free(gpbo_model *model);
 
+/* ---------------------------------------------------------------- append
+ * Sequential BO's surrogate update ("re-training the surrogate model"): a new model
+ * whose search s holds the previous model's n_s observations plus ONE new one (x_new: d_s
+ * encoded values, concatenated over s; y_new[s] raw objective), with the same hyper-parameters
+ * and jitter, in O(n^2) per search instead of the O(n^3) refit: the bordered Cholesky
+ *   l = L^-1 k(X, x_new),  delta = sqrt(sf2 + sn2 + j - |l|^2),  L' = [L 0; l^T delta],
+ *   L'^-1 = [L^-1 0; -(l^T L^-1)/delta 1/delta],
+ * then y re-standardised over the n + 1 values (reading R7), alpha = L'^-T L'^-1 y~ and the
+ * diagnostics / LML recomputed.  Equal to a full gp_fit of the n + 1 observations up to float64
+ * rounding (Cholesky is unique and the full fit's jitter ladder stops at the same k).  If the
+ * bordered matrix is not positive definite at the old jitter (delta^2 <= 0) the whole batch is
+ * refitted from scratch with the jitter ladder (gpbo_last_append_refit(ctx) = 1).  x_new / y_new
+ * are host or device arrays per `mem`; `prev` is left unchanged (free it when done).  Outputs and
+ * return codes as gp_fit; GPBO_EINVAL if a previous search has no fit, n_s + 1 > 512 or a new
+ * value is non-finite.  Synchronous. */
+gpbo_status gp_fit_append(gpbo_ctx *ctx, const gpbo_model *prev, const float *x_new,
+                          const double *y_new, gpbo_mem mem, gpbo_model **out, int32_t *status,
+                          int32_t *jitter_k);
+int64_t gpbo_last_append_refit(const gpbo_ctx *ctx);
+
+/* Log marginal likelihood of every search's fit (host array lml[S], standardised targets):
+ *   log p(y~ | X, theta) = -1/2 y~^T alpha - sum_i log L_ii - n/2 log(2 pi)
+ * with K = k(X, X) + (sn2 + j_k) I the (jittered) matrix actually factored (Rasmussen & Williams
+ * eq. 2.30; the GP "training" whose O(N^3) cost PAPER.md L249 names).  -inf for failed fits. */
+gpbo_status gp_model_lml(const gpbo_model *model, double *lml);
+
+/* ---------------------------------------------------------------- ML-II
+ * Hyper-parameters by maximising the log marginal likelihood (type-II maximum likelihood), per
+ * search, with multi-start Nelder-Mead in log space (8 seeded starts, 200
+ * iterations each; bounds lengthscale [1e-3, 10], signal [1e-3, 1e3], noise [1e-6, 1] in
+ * standardised units).  theta = (log l_1 .. log l_d, log sf2, log sn2); start 0 is the theta in
+ * `args`, starts 1.. are uniform in the log box from a counter-based generator (splitmix64, see
+ * ml2.cuh); simplex step `step` (log units); reflection 1, expansion 2, contraction 1/2, shrink
+ * 1/2; points clamped to the box; exactly `iters` iterations.  All (search, start) simplices
+ * advance together: each round evaluates every requested point as ONE batched gp_fit launch
+ * (fit.cu, one CTA per point).  Inputs: `args` with mem = GPBO_HOST (its lengthscale /
+ * signal_var / noise_var = start 0).  Outputs (host): the best theta per search (ls_out [sum d],
+ * sf2_out [S], sn2_out [S], as float32 exactly as evaluated), its LML (lml_out [S], may be NULL)
+ * and the LML of every start point (lml_starts [S * starts], may be NULL).  Invariant:
+ * lml_out[s] >= lml_starts[s * starts + k] for every k.  Refit with gp_fit to score. */
+typedef struct {
+  int32_t starts;   /* multi-start count (SPEC: 8)                                        */
+  int32_t iters;    /* Nelder-Mead iterations per start (SPEC: 200)                       */
+  uint64_t seed;    /* start-point generator seed                                         */
+  double step;      /* initial simplex step in log units (0.5)                            */
+  double ls_lo, ls_hi, sf2_lo, sf2_hi, sn2_lo, sn2_hi;  /* bounds (SPEC L376 above)        */
+} gpbo_ml2_opts;
+gpbo_status gp_fit_ml2(gpbo_ctx *ctx, const gpbo_fit_args *args, const gpbo_ml2_opts *opts,
+                       float *ls_out, float *sf2_out, float *sn2_out, double *lml_out,
+                       double *lml_starts);
+/* LML evaluations (batched fit searches) the last gp_fit_ml2 call on ctx ran. */
+int64_t gpbo_last_ml2_evals(const gpbo_ctx *ctx);
+/* Host-only test hook (no GPU needed): run gp_fit_ml2's Nelder-Mead state machine on a caller
+ * objective f (evaluated in request order) from x0 in the box [lo, hi]; returns the best vertex,
+ * its f, f(x0) and the number of evaluations.  Lets CPU tests pin the optimiser itself. */
+gpbo_status gpbo_nm_selftest(int dim, const double *x0, const double *lo, const double *hi,
+                             double step, int iters, double (*f)(const double *x, void *user),
+                             void *user, double *best_x, double *best_f, double *start_f,
+                             int64_t *nevals);
+
 /* Fitted per-search statistics (host copies, any may be NULL): y mean and std (raw units),
  * best = min y~ (standardised), alpha_l1 = ||alpha||_1 (the mu-tier diagnostic, reading R13). */
 gpbo_status gp_model_stats(const gpbo_model *model, int32_t s, double *mean, double *std,

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "gpbo_internal.cuh"
+#include "ml2.cuh"
 #include "score_tc.cuh"
 #include "space_internal.cuh"
 
@@ -30,6 +31,8 @@ struct gpbo_ctx {
   size_t cur_key_bytes = 0;
   const int64_t *cur_p_off = nullptr;  // this call's device m_off | m_base | x_off | best (aux_d)
   int64_t last_violations = 0;  // bracket violations found by the last argmax call
+  int64_t last_ml2_evals = 0;   // LML evaluations of the last gp_fit_ml2 call
+  int64_t last_append_refit = 0;  // the last gp_fit_append fell back to a full refit
   float bound_scale = 1.f;      // error-bound multiplier of the fast phase (test hook)
   gpbo::RefineEntry *list_d = nullptr;   // refine list of the argmax path
   size_t list_cap = 0;
@@ -80,6 +83,7 @@ struct gpbo_model {
   mutable bool simt_ready = false;  // Xs32 / LT32 built (on first CUDA-core scoring call)
   mutable bool packed = false;      // tcgen05 operand images built (on first tcgen05 call)
   mutable bool meta_pending = false;  // gp_fit_async: host meta not yet refreshed from the device
+  int64_t nx_total = 0, nls_total = 0, ny_total = 0;  // sum n d, sum d, sum n
 };
 
 namespace {
@@ -622,6 +626,8 @@ int64_t gpbo_last_refine_count(const gpbo_ctx *ctx) { return ctx ? ctx->last_ref
 
 int64_t gpbo_collective_count(const gpbo_ctx *ctx) { return ctx ? ctx->collectives : -1; }
 
+int64_t gpbo_last_ml2_evals(const gpbo_ctx *ctx) { return ctx ? ctx->last_ml2_evals : -1; }
+
 int64_t gpbo_last_bracket_violations(const gpbo_ctx *ctx) {
   return ctx ? ctx->last_violations : -1;
 }
@@ -672,22 +678,20 @@ void gp_model_free(gpbo_model *model) {
 }
 
 namespace {
-gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bool wait,
-                     int32_t *status, int32_t *jitter_k) {
-  if (!ctx) return GPBO_EINVAL;
-  if (!a || !out) return fail(ctx, GPBO_EINVAL, "null args/out");
+// Model allocation shared by gp_fit and gp_fit_append: the per-search meta records (shapes,
+// offsets, tcgen05 geometry) and one stream-ordered device block holding every array.
+struct ModelScratch {
+  SearchMeta *meta_in = nullptr;  // device staging of the input meta records
+  double *Wscr64 = nullptr, *Kt64 = nullptr, *pm_part = nullptr;
+  int smem_max = 0;
+};
+
+gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t *d_in, int kernel,
+                        bool lml_only, gpbo_model **out, ModelScratch *sc) {
   *out = nullptr;
-  if (a->S < 1 || !a->n || !a->d || !a->X || !a->y || !a->lengthscale || !a->signal_var ||
-      !a->noise_var)
-    return fail(ctx, GPBO_EINVAL, "S < 1 or null input array");
-  if (a->kernel != GPBO_RBF && a->kernel != GPBO_MATERN52)
-    return fail(ctx, GPBO_EINVAL, "unknown kernel");
-  if (a->mem != GPBO_HOST && a->mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
-  CK(cudaSetDevice(ctx->device));
-  const int S = a->S;
   gpbo_model *m = new gpbo_model();
   m->S = S;
-  m->kernel = a->kernel;
+  m->kernel = kernel;
   m->device = ctx->device;
   m->stream = ctx->stream;
   m->meta.resize(S);
@@ -698,11 +702,11 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   // resident image would not fit in shared memory, or when the ctx forces it (impl 3)
   bool stream_layout = ctx->score_impl == 3;
   for (int s = 0; s < S; ++s)
-    if (a->n[s] >= 1 && a->n[s] <= GPBO_MAX_N && a->d[s] >= 1 && a->d[s] <= GPBO_MAX_D &&
-        gpbo::tc_needs_stream(a->n[s], a->d[s]))
+    if (n_in[s] >= 1 && n_in[s] <= GPBO_MAX_N && d_in[s] >= 1 && d_in[s] <= GPBO_MAX_D &&
+        gpbo::tc_needs_stream(n_in[s], d_in[s]))
       stream_layout = true;
   for (int s = 0; s < S; ++s) {
-    const int n = a->n[s], d = a->d[s];
+    const int n = n_in[s], d = d_in[s];
     if (n < 1 || n > GPBO_MAX_N || d < 1 || d > GPBO_MAX_D) {
       delete m;
       return fail(ctx, GPBO_EINVAL, "n_s must be in [1, 512] and d_s in [1, 64]");
@@ -713,7 +717,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     q.d = d;
     q.n_pad = (int)round_up(n, 64);
     q.d_pad = (int)round_up(d, 8);
-    q.kernel = a->kernel;
+    q.kernel = kernel;
     q.x_off = nx; nx += (int64_t)n * d;
     q.ls_off = nls; nls += d;
     q.y_off = ny; ny += n;
@@ -723,7 +727,8 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     q.a_off = na; na += q.n_pad;
     q.tc_stream = stream_layout ? 1 : 0;
     gpbo::tc_fill_geometry(q);
-    q.img_off = nimg; nimg += gpbo::tc_image_bytes(q);
+    q.img_off = nimg;
+    if (lml_only) q.tc_ok = 0; else nimg += gpbo::tc_image_bytes(q);
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
     q.kt_off = nkt; nkt += gpbo::fit_tile_doubles(n);
@@ -733,9 +738,6 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     m->nmax = std::max(m->nmax, n);
     m->dmax = std::max(m->dmax, q.d_pad);
   }
-  // hyper-parameters: host arrays go into the meta records; device arrays are read by the kernel
-  if (a->mem == GPBO_HOST)
-    for (int s = 0; s < S; ++s) { m->meta[s].sf2 = a->signal_var[s]; m->meta[s].sn2 = a->noise_var[s]; }
   // one device block: meta | X | ls | Xs | LT | y | L | Linv | alpha | img
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += round_up((int64_t)bytes, 256); return o; };
@@ -748,7 +750,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
   if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
   m->meta_d = (SearchMeta *)(m->block + o_meta);
-  SearchMeta *meta_in = m->meta_d + S;
+  sc->meta_in = m->meta_d + S;
   m->X32 = (float *)(m->block + o_x);
   m->ls32 = (float *)(m->block + o_ls);
   m->Xs32 = (float *)(m->block + o_xs);
@@ -759,9 +761,44 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   m->alpha64 = (double *)(m->block + o_a);
   m->img = (unsigned char *)(m->block + o_img);
   m->Xs64 = (double *)(m->block + o_x64);
-  double *Wscr64 = (double *)(m->block + o_scr);
-  double *Kt64 = (double *)(m->block + o_kt);
+  sc->Wscr64 = (double *)(m->block + o_scr);
+  sc->Kt64 = (double *)(m->block + o_kt);
+  sc->pm_part = (double *)(m->block + o_pm);
+  sc->smem_max = smem_max;
   m->img_bytes = nimg;
+  m->nx_total = nx; m->nls_total = nls; m->ny_total = ny;
+  *out = m;
+  return GPBO_OK;
+}
+
+// lml_only (ML-II objective evaluations): no tcgen05 operand image is reserved; the model is
+// read for its statistics and freed, never scored.
+gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bool wait,
+                     int32_t *status, int32_t *jitter_k, bool lml_only = false) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!a || !out) return fail(ctx, GPBO_EINVAL, "null args/out");
+  *out = nullptr;
+  if (a->S < 1 || !a->n || !a->d || !a->X || !a->y || !a->lengthscale || !a->signal_var ||
+      !a->noise_var)
+    return fail(ctx, GPBO_EINVAL, "S < 1 or null input array");
+  if (a->kernel != GPBO_RBF && a->kernel != GPBO_MATERN52)
+    return fail(ctx, GPBO_EINVAL, "unknown kernel");
+  if (a->mem != GPBO_HOST && a->mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
+  CK(cudaSetDevice(ctx->device));
+  const int S = a->S;
+  gpbo_model *m = nullptr;
+  ModelScratch sc;
+  {
+    gpbo_status ast = alloc_model(ctx, S, a->n, a->d, a->kernel, lml_only, &m, &sc);
+    if (ast) return ast;
+  }
+  SearchMeta *meta_in = sc.meta_in;
+  double *Wscr64 = sc.Wscr64, *Kt64 = sc.Kt64;
+  const int smem_max = sc.smem_max;
+  const int64_t nx = m->nx_total, nls = m->nls_total, ny = m->ny_total;
+  // hyper-parameters: host arrays go into the meta records; device arrays are read by the kernel
+  if (a->mem == GPBO_HOST)
+    for (int s = 0; s < S; ++s) { m->meta[s].sf2 = a->signal_var[s]; m->meta[s].sn2 = a->noise_var[s]; }
   const cudaMemcpyKind kind = a->mem == GPBO_HOST ? cudaMemcpyHostToDevice
                                                   : cudaMemcpyDeviceToDevice;
   auto cleanup_fail = [&](gpbo_status st, const std::string &msg) {
@@ -780,7 +817,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   io.L64 = m->L64; io.Linv64 = m->Linv64; io.Xs64 = m->Xs64; io.alpha64 = m->alpha64;
   io.Wscr64 = Wscr64;
   io.Kt64 = Kt64;
-  io.pm_part = (double *)(m->block + o_pm);
+  io.pm_part = sc.pm_part;
   if (a->mem == GPBO_HOST) {  // stage into the model's arrays
     CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
     CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));
@@ -841,6 +878,278 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
 gpbo_status gp_fit(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, int32_t *status,
                    int32_t *jitter_k) {
   return fit_impl(ctx, a, out, true, status, jitter_k);
+}
+
+gpbo_status gpbo_nm_selftest(int dim, const double *x0, const double *lo, const double *hi,
+                             double step, int iters, double (*f)(const double *x, void *user),
+                             void *user, double *best_x, double *best_f, double *start_f,
+                             int64_t *nevals) {
+  if (dim < 1 || !x0 || !lo || !hi || !f || !best_x || !(step > 0) || iters < 0)
+    return GPBO_EINVAL;
+  gpbo::NelderMead nm(dim, x0, lo, hi, step, iters);
+  int64_t ne = 0;
+  std::vector<double> fv;
+  while (!nm.done()) {
+    const std::vector<double> &req = nm.request();
+    const int np = (int)(req.size() / dim);
+    fv.resize(np);
+    for (int p = 0; p < np; ++p) fv[p] = f(&req[(size_t)p * dim], user);
+    ne += np;
+    nm.deliver(fv.data());
+  }
+  for (int i = 0; i < dim; ++i) best_x[i] = nm.best_x()[i];
+  if (best_f) *best_f = nm.best_f();
+  if (start_f) *start_f = nm.start_f();
+  if (nevals) *nevals = ne;
+  return GPBO_OK;
+}
+
+gpbo_status gp_fit_append(gpbo_ctx *ctx, const gpbo_model *prev, const float *x_new,
+                          const double *y_new, gpbo_mem mem, gpbo_model **out, int32_t *status,
+                          int32_t *jitter_k) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!prev || !x_new || !y_new || !out) return fail(ctx, GPBO_EINVAL, "null argument");
+  *out = nullptr;
+  if (mem != GPBO_HOST && mem != GPBO_DEVICE) return fail(ctx, GPBO_EINVAL, "bad mem");
+  CK(cudaSetDevice(ctx->device));
+  if (refresh_meta(prev)) return fail(ctx, GPBO_ECUDA, "meta download failed");
+  const int S = prev->S;
+  std::vector<int32_t> n1(S), d(S);
+  int64_t dsum = 0;
+  for (int s = 0; s < S; ++s) {
+    const SearchMeta &q = prev->meta[s];
+    if (q.status != GPBO_OK && q.status != GPBO_WDEGENERATE)
+      return fail(ctx, GPBO_EINVAL, "gp_fit_append: a search of the previous model has no fit");
+    if (q.n + 1 > GPBO_MAX_N) return fail(ctx, GPBO_EINVAL, "gp_fit_append: n would exceed 512");
+    n1[s] = q.n + 1;
+    d[s] = q.d;
+    dsum += q.d;
+  }
+  gpbo_model *m = nullptr;
+  ModelScratch sc;
+  gpbo_status st = alloc_model(ctx, S, n1.data(), d.data(), prev->kernel, false, &m, &sc);
+  if (st) return st;
+  for (int s = 0; s < S; ++s) { m->meta[s].sf2 = prev->meta[s].sf2; m->meta[s].sn2 = prev->meta[s].sn2; }
+  auto cleanup_fail = [&](gpbo_status e, const std::string &msg) {
+    cudaStreamSynchronize(ctx->stream);
+    gp_model_free(m);
+    return fail(ctx, e, msg);
+  };
+#define CKA(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return cleanup_fail(GPBO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+  // new observations: host values staged through the scratch the fit would use (Kt64, unused
+  // by an appended model), device values read in place
+  const float *xd = x_new;
+  const double *yd = y_new;
+  if (mem == GPBO_HOST) {
+    gpbo_status e = ensure_stage(ctx, (size_t)dsum * 4 + (size_t)S * 8 + 64);
+    if (e) { gp_model_free(m); return e; }
+    double *ys = (double *)ctx->stage_d;
+    float *xs = (float *)(ys + S);
+    CKA(cudaMemcpyAsync(ys, y_new, (size_t)S * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CKA(cudaMemcpyAsync(xs, x_new, (size_t)dsum * 4, cudaMemcpyHostToDevice, ctx->stream));
+    xd = xs;
+    yd = ys;
+  }
+  gpbo_status pst = ensure_meta_h(ctx, sizeof(SearchMeta) * S);
+  if (pst) { gp_model_free(m); return pst; }
+  if (ctx->meta_ev) CKA(cudaEventSynchronize(ctx->meta_ev));
+  std::memcpy(ctx->meta_h, m->meta.data(), sizeof(SearchMeta) * S);
+  CKA(cudaMemcpyAsync(sc.meta_in, ctx->meta_h, sizeof(SearchMeta) * S, cudaMemcpyHostToDevice,
+                      ctx->stream));
+  if (!ctx->meta_ev) CKA(cudaEventCreateWithFlags(&ctx->meta_ev, cudaEventDisableTiming));
+  CKA(cudaEventRecord(ctx->meta_ev, ctx->stream));
+  gpbo::AppendIO io{};
+  io.prev_meta = prev->meta_d;
+  io.prev_X32 = prev->X32; io.prev_ls32 = prev->ls32; io.prev_y64 = prev->y64;
+  io.prev_L64 = prev->L64; io.prev_Linv64 = prev->Linv64; io.prev_Xs64 = prev->Xs64;
+  io.x_new = xd; io.y_new = yd;
+  io.X32 = m->X32; io.ls32 = m->ls32; io.y64 = m->y64; io.L64 = m->L64;
+  io.Linv64 = m->Linv64; io.Xs64 = m->Xs64; io.alpha64 = m->alpha64;
+  {
+    KernTimer t(ctx, kKernFit);
+    CKA(gpbo::launch_append(sc.meta_in, S, io, m->meta_d, ctx->stream));
+  }
+  ctx->launches += 1;
+  CKA(cudaMemcpyAsync(ctx->meta_h, m->meta_d, sizeof(SearchMeta) * S, cudaMemcpyDeviceToHost,
+                      ctx->stream));
+  CKA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(m->meta.data(), ctx->meta_h, sizeof(SearchMeta) * S);
+  harvest_events(ctx);
+#undef CKA
+  bool einval = false, refit = false;
+  for (int s = 0; s < S; ++s) {
+    einval = einval || m->meta[s].status == GPBO_EINVAL;
+    refit = refit || (m->meta[s].status == GPBO_ENOTPD && m->meta[s].jitter_k == -2);
+  }
+  if (einval) {
+    gp_model_free(m);
+    return fail(ctx, GPBO_EINVAL, "non-finite new observation");
+  }
+  ctx->last_append_refit = refit ? 1 : 0;
+  if (refit) {
+    // the bordered matrix is not positive definite at the old jitter: refit every search from
+    // the appended data (already on the device) with the full jitter ladder
+    std::vector<float> sf2(S), sn2(S);
+    for (int s = 0; s < S; ++s) { sf2[s] = prev->meta[s].sf2; sn2[s] = prev->meta[s].sn2; }
+    // device hyper-parameter arrays for the device-input fit: staged after the new data
+    gpbo_status e = ensure_stage(ctx, (size_t)S * 8 + 64);
+    if (e) { gp_model_free(m); return e; }
+    float *hp = (float *)ctx->stage_d;
+    if (cudaMemcpyAsync(hp, sf2.data(), (size_t)S * 4, cudaMemcpyHostToDevice, ctx->stream) ||
+        cudaMemcpyAsync(hp + S, sn2.data(), (size_t)S * 4, cudaMemcpyHostToDevice, ctx->stream)) {
+      gp_model_free(m);
+      return fail(ctx, GPBO_ECUDA, "staging failed");
+    }
+    gpbo_fit_args fa{};
+    fa.S = S; fa.n = n1.data(); fa.d = d.data(); fa.X = m->X32; fa.y = m->y64;
+    fa.lengthscale = m->ls32; fa.signal_var = hp; fa.noise_var = hp + S;
+    fa.kernel = (gpbo_kernel)prev->kernel; fa.mem = GPBO_DEVICE;
+    gpbo_model *r = nullptr;
+    st = fit_impl(ctx, &fa, &r, true, status, jitter_k);  // synchronous: m's arrays are read
+    gp_model_free(m);
+    if (r) *out = r;
+    return st;
+  }
+  gpbo_status worst = GPBO_OK;
+  for (int s = 0; s < S; ++s) {
+    if (status) status[s] = m->meta[s].status;
+    if (jitter_k) jitter_k[s] = m->meta[s].jitter_k;
+    if (m->meta[s].status == GPBO_WDEGENERATE) worst = GPBO_WDEGENERATE;
+  }
+  *out = m;
+  return worst;
+}
+
+int64_t gpbo_last_append_refit(const gpbo_ctx *ctx) { return ctx ? ctx->last_append_refit : -1; }
+
+gpbo_status gp_model_lml(const gpbo_model *model, double *lml) {
+  if (!model || !lml) return GPBO_EINVAL;
+  if (refresh_meta(model)) return GPBO_ECUDA;
+  for (int s = 0; s < model->S; ++s) lml[s] = model->meta[s].lml;
+  return GPBO_OK;
+}
+
+gpbo_status gp_fit_ml2(gpbo_ctx *ctx, const gpbo_fit_args *a, const gpbo_ml2_opts *opt,
+                       float *ls_out, float *sf2_out, float *sn2_out, double *lml_out,
+                       double *lml_starts) {
+  if (!ctx) return GPBO_EINVAL;
+  if (!a || !opt || !ls_out || !sf2_out || !sn2_out)
+    return fail(ctx, GPBO_EINVAL, "null args/opts/outputs");
+  if (a->mem != GPBO_HOST) return fail(ctx, GPBO_EINVAL, "gp_fit_ml2 takes host inputs");
+  if (a->S < 1 || !a->n || !a->d || !a->X || !a->y || !a->lengthscale || !a->signal_var ||
+      !a->noise_var)
+    return fail(ctx, GPBO_EINVAL, "S < 1 or null input array");
+  if (opt->starts < 1 || opt->iters < 0 || !(opt->ls_lo > 0) || !(opt->ls_hi >= opt->ls_lo) ||
+      !(opt->sf2_lo > 0) || !(opt->sf2_hi >= opt->sf2_lo) || !(opt->sn2_lo > 0) ||
+      !(opt->sn2_hi >= opt->sn2_lo) || !(opt->step > 0))
+    return fail(ctx, GPBO_EINVAL, "bad ML-II options");
+  const int S = a->S, K = opt->starts;
+  std::vector<int64_t> xo(S + 1, 0), yo(S + 1, 0), lo_(S + 1, 0);
+  for (int s = 0; s < S; ++s) {
+    if (a->n[s] < 1 || a->n[s] > GPBO_MAX_N || a->d[s] < 1 || a->d[s] > GPBO_MAX_D)
+      return fail(ctx, GPBO_EINVAL, "n_s must be in [1, 512] and d_s in [1, 64]");
+    xo[s + 1] = xo[s] + (int64_t)a->n[s] * a->d[s];
+    yo[s + 1] = yo[s] + a->n[s];
+    lo_[s + 1] = lo_[s] + a->d[s];
+  }
+  // theta of search s in log space: (log l_1 .. log l_d, log sf2, log sn2), dim d + 2
+  std::vector<gpbo::NelderMead> lanes;
+  std::vector<int> lane_s;
+  lanes.reserve((size_t)S * K);
+  for (int s = 0; s < S; ++s) {
+    const int d = a->d[s], dim = d + 2;
+    std::vector<double> lo(dim), hi(dim), x0(dim);
+    for (int i = 0; i < d; ++i) { lo[i] = std::log(opt->ls_lo); hi[i] = std::log(opt->ls_hi); }
+    lo[d] = std::log(opt->sf2_lo); hi[d] = std::log(opt->sf2_hi);
+    lo[d + 1] = std::log(opt->sn2_lo); hi[d + 1] = std::log(opt->sn2_hi);
+    for (int k = 0; k < K; ++k) {
+      if (k == 0) {  // start 0: the caller's theta
+        for (int i = 0; i < d; ++i) x0[i] = std::log((double)a->lengthscale[lo_[s] + i]);
+        x0[d] = std::log((double)a->signal_var[s]);
+        x0[d + 1] = std::log((double)a->noise_var[s]);
+        for (int i = 0; i < dim; ++i)
+          if (!std::isfinite(x0[i])) return fail(ctx, GPBO_EINVAL, "start theta must be > 0");
+      } else {  // seeded uniform starts in the log box
+        for (int i = 0; i < dim; ++i)
+          x0[i] = lo[i] + gpbo::ml2_uniform(opt->seed, s, k, i, dim, K) * (hi[i] - lo[i]);
+      }
+      lanes.emplace_back(dim, x0.data(), lo.data(), hi.data(), opt->step, opt->iters);
+      lane_s.push_back(s);
+    }
+  }
+  // rounds: every unfinished simplex contributes its requested points to one batched fit
+  std::vector<int32_t> bn, bd;
+  std::vector<float> bX, bls, bsf2, bsn2;
+  std::vector<double> by, fvals;
+  std::vector<std::pair<int, int>> owner;  // (lane, point count) per lane in the batch
+  int64_t evals = 0;
+  for (;;) {
+    bn.clear(); bd.clear(); bX.clear(); bls.clear(); bsf2.clear(); bsn2.clear(); by.clear();
+    owner.clear();
+    for (size_t l = 0; l < lanes.size(); ++l) {
+      if (lanes[l].done()) continue;
+      const int s = lane_s[l], d = a->d[s], dim = d + 2;
+      const std::vector<double> &req = lanes[l].request();
+      const int np = (int)(req.size() / dim);
+      for (int p = 0; p < np; ++p) {
+        const double *x = &req[(size_t)p * dim];
+        bn.push_back(a->n[s]);
+        bd.push_back(d);
+        bX.insert(bX.end(), a->X + xo[s], a->X + xo[s + 1]);
+        by.insert(by.end(), a->y + yo[s], a->y + yo[s + 1]);
+        for (int i = 0; i < d; ++i) bls.push_back((float)std::exp(x[i]));
+        bsf2.push_back((float)std::exp(x[d]));
+        bsn2.push_back((float)std::exp(x[d + 1]));
+      }
+      owner.push_back({(int)l, np});
+    }
+    if (owner.empty()) break;
+    gpbo_fit_args fa{};
+    fa.S = (int32_t)bn.size();
+    fa.n = bn.data(); fa.d = bd.data(); fa.X = bX.data(); fa.y = by.data();
+    fa.lengthscale = bls.data(); fa.signal_var = bsf2.data(); fa.noise_var = bsn2.data();
+    fa.kernel = a->kernel; fa.mem = GPBO_HOST;
+    gpbo_model *m = nullptr;
+    gpbo_status st = fit_impl(ctx, &fa, &m, true, nullptr, nullptr, true);
+    if (st != GPBO_OK && st != GPBO_ENOTPD && st != GPBO_WDEGENERATE) {
+      if (m) gp_model_free(m);
+      return st;
+    }
+    evals += fa.S;
+    int q = 0;
+    for (auto &o : owner) {
+      fvals.assign(o.second, 0.0);
+      for (int p = 0; p < o.second; ++p, ++q) {
+        const SearchMeta &r = m->meta[q];
+        const bool ok = (r.status == GPBO_OK || r.status == GPBO_WDEGENERATE) && std::isfinite(r.lml);
+        fvals[p] = ok ? -r.lml : INFINITY;  // minimise -LML
+      }
+      lanes[o.first].deliver(fvals.data());
+    }
+    gp_model_free(m);
+  }
+  ctx->last_ml2_evals = evals;
+  // per search: the best vertex over its starts (ties -> the lowest start)
+  for (int s = 0; s < S; ++s) {
+    const int d = a->d[s];
+    int bl = s * K;
+    for (int k = 0; k < K; ++k) {
+      const int l = s * K + k;
+      if (lanes[l].best_f() < lanes[bl].best_f()) bl = l;
+      if (lml_starts) lml_starts[(size_t)s * K + k] = -lanes[l].start_f();
+    }
+    const double *x = lanes[bl].best_x();
+    for (int i = 0; i < d; ++i) ls_out[lo_[s] + i] = (float)std::exp(x[i]);
+    sf2_out[s] = (float)std::exp(x[d]);
+    sn2_out[s] = (float)std::exp(x[d + 1]);
+    if (lml_out) lml_out[s] = -lanes[bl].best_f();
+  }
+  return GPBO_OK;
 }
 
 gpbo_status gp_fit_async(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out) {

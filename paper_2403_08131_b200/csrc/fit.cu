@@ -173,7 +173,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   bad |= !(m.sf2 > 0.f) || !isfinite(m.sf2) || !(m.sn2 >= 0.f) || !isfinite(m.sn2);
   bad = __syncthreads_or(bad);
   if (bad) {
-    if (tid == 0) { m.status = GPBO_EINVAL; m.jitter_k = -1; meta_out[s] = m; }
+    if (tid == 0) { m.status = GPBO_EINVAL; m.jitter_k = -1; m.lml = -INFINITY; meta_out[s] = m; }
     return;
   }
 
@@ -512,7 +512,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   __syncthreads();
   if (jk < 0) {
     if (tid == 0) {
-      m.status = GPBO_ENOTPD; m.jitter_k = -1; m.jitter = NAN;
+      m.status = GPBO_ENOTPD; m.jitter_k = -1; m.jitter = NAN; m.lml = -INFINITY;
       m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = 0.0;
       meta_out[s] = m;
     }
@@ -522,7 +522,9 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   // per tile row, lane -> row gid of the tile, columns 2 tig + {0, 1} (one 16-byte load per lane
   // and tile); the tiles go to the row-major L^-1 on the way (the refine phase, the tcgen05
   // image and the CUDA-core operands read only k <= i).
-  double rs = 0.0, lam = 0.0;
+  // (ld = sum_i log L_ii = -sum_i log (L^-1)_ii and ww = |w|^2 = y~^T alpha feed the log marginal
+  // likelihood, §8(f)1 ML-II)
+  double rs = 0.0, lam = 0.0, ld = 0.0, ww = 0.0;
   for (int R = warp; R < nt; R += kWarps) {
     const int i = 8 * R + gid;
     double a2 = 0.0, a3 = 0.0;
@@ -538,12 +540,17 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
       lam = fmax(lam, fmax(fabs(v0), fabs(v1)));
       if (in0) dst[c0] = v.x;
       if (in1) dst[c0 + 1] = v.y;
+      if (in0 && c0 == i) ld -= log(v.x);
+      if (in1 && c0 + 1 == i) ld -= log(v.y);
     }
     a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
     a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
     a3 += __shfl_xor_sync(0xffffffffu, a3, 1);
     a3 += __shfl_xor_sync(0xffffffffu, a3, 2);
-    if (tig == 0 && i < n) w[i] = a2;
+    if (tig == 0 && i < n) {
+      w[i] = a2;
+      ww = fma(a2, a2, ww);
+    }
     rs = fmax(rs, a3);
   }
   __syncthreads();
@@ -580,30 +587,33 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     }
   }
   for (int kk = n + tid; kk < m.n_pad; kk += kFitThreads) alpha64[m.a_off + kk] = 0.0;
-  // the four statistics in one block reduction
+  // the six statistics in one block reduction (sums: l1, ld, ww; maxima: amx, rs, lam), in a
+  // fixed order (deterministic)
   {
-    double v[4] = {l1, amx, rs, lam};
+    double v[6] = {l1, ld, ww, amx, rs, lam};
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 6; ++q)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double t = __shfl_xor_sync(0xffffffffu, v[q], o);
-        v[q] = q == 0 ? v[q] + t : fmax(v[q], t);
+        v[q] = q < 3 ? v[q] + t : fmax(v[q], t);
       }
     if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) red[4 * warp + q] = v[q];
+      for (int q = 0; q < 6; ++q) red[6 * warp + q] = v[q];
     __syncthreads();
-    if (tid < 4) {
+    if (tid < 6) {
       double t = red[tid];
-      for (int w2 = 1; w2 < kWarps; ++w2) t = tid == 0 ? t + red[4 * w2] : fmax(t, red[4 * w2 + tid]);
-      red[4 * kWarps + tid] = t;
+      for (int w2 = 1; w2 < kWarps; ++w2) t = tid < 3 ? t + red[6 * w2 + tid] : fmax(t, red[6 * w2 + tid]);
+      red[6 * kWarps + tid] = t;
     }
     __syncthreads();
-    l1 = red[4 * kWarps];
-    amx = red[4 * kWarps + 1];
-    rs = red[4 * kWarps + 2];
-    lam = red[4 * kWarps + 3];
+    l1 = red[6 * kWarps];
+    ld = red[6 * kWarps + 1];
+    ww = red[6 * kWarps + 2];
+    amx = red[6 * kWarps + 3];
+    rs = red[6 * kWarps + 4];
+    lam = red[6 * kWarps + 5];
   }
   FIT_T(5);
 #ifdef GPBO_FIT_TIMING
@@ -619,6 +629,9 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     m.mean = mean; m.std = stdv; m.best = best; m.alpha_l1 = l1;
     m.pmax = (float)pmax; m.alpha_max = (float)amx; m.linv_rowsum = (float)rs;
     m.linv_absmax = lam;
+    // log marginal likelihood of y~ at this theta (the jittered K actually factored):
+    // -1/2 y~^T alpha - sum_i log L_ii - n/2 log 2 pi  (Rasmussen & Williams eq. 2.30)
+    m.lml = -0.5 * ww - ld - 0.5 * n * 1.8378770664093454836;
     meta_out[s] = m;
   }
 }
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(kFitThreads, 1)
 fit_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
            SearchMeta *__restrict__ meta_out) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[4 * kWarps + 4];
+  __shared__ double red[6 * kWarps + 6];
   if (meta_in[blockIdx.x].use_smem)
     fit_body<true>(sm, red, meta_in, io, meta_out);
   else

@@ -47,6 +47,7 @@ struct SearchMeta {
   int64_t img_off;      // tcgen05 operand image (bytes)      into model.img
   // fit results
   double mean, std, best, alpha_l1;
+  double lml;           // log marginal likelihood of y~ (standardised), -inf if the fit failed
   float pmax;           // max_j |x_j / l|^2 (error-bound input of the fast phase)
   float alpha_max;      // max_j |alpha_j|
   float linv_rowsum;    // max_j sum_k |(L^-1)_jk| (variance error-bound input)
@@ -170,6 +171,18 @@ cudaError_t launch_score_simt(const ScoreLaunch &p, int total_tiles, int dmax, i
                               cudaStream_t stream);
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms, int nmax,
                           cudaStream_t stream);
+// O(n^2) append update (append.cu): the previous model's arrays -> the new model's arrays.
+struct AppendIO {
+  const SearchMeta *prev_meta;   // device meta of the previous model
+  const float *prev_X32, *prev_ls32;
+  const double *prev_y64, *prev_L64, *prev_Linv64, *prev_Xs64;
+  const float *x_new;            // [sum d_s] device
+  const double *y_new;           // [S] device
+  float *X32, *ls32;
+  double *y64, *L64, *Linv64, *Xs64, *alpha64;
+};
+cudaError_t launch_append(const SearchMeta *meta_in, int S, const AppendIO &io,
+                          SearchMeta *meta_out, cudaStream_t stream);
 // Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
 constexpr int kDirectMaxN = 64;
 cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream);

@@ -36,6 +36,13 @@ class SpaceDesc(C.Structure):
                 ("tuple_off", C.c_void_p), ("tuples", C.c_void_p)]
 
 
+class Ml2Opts(C.Structure):
+    _fields_ = [("starts", C.c_int32), ("iters", C.c_int32), ("seed", C.c_uint64),
+                ("step", C.c_double), ("ls_lo", C.c_double), ("ls_hi", C.c_double),
+                ("sf2_lo", C.c_double), ("sf2_hi", C.c_double), ("sn2_lo", C.c_double),
+                ("sn2_hi", C.c_double)]
+
+
 class FitArgs(C.Structure):
     _fields_ = [("S", C.c_int32), ("n", C.c_void_p), ("d", C.c_void_p), ("X", C.c_void_p),
                 ("y", C.c_void_p), ("lengthscale", C.c_void_p), ("signal_var", C.c_void_p),
@@ -65,6 +72,13 @@ def load():
         "gp_fit_async": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(vp)]),
         "gp_model_sync": (C.c_int, [vp, vp, vp, vp]),
         "gp_model_free": (None, [vp]),
+        "gp_model_lml": (C.c_int, [vp, vp]),
+        "gp_fit_append": (C.c_int, [vp, vp, vp, vp, C.c_int, C.POINTER(vp), vp, vp]),
+        "gpbo_last_append_refit": (i64, [vp]),
+        "gp_fit_ml2": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(Ml2Opts), vp, vp, vp, vp, vp]),
+        "gpbo_last_ml2_evals": (i64, [vp]),
+        "gpbo_nm_selftest": (C.c_int, [C.c_int, vp, vp, vp, C.c_double, C.c_int, vp, vp, vp, vp,
+                                       vp, vp]),
         "gp_model_stats": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "gp_model_export": (C.c_int, [vp, vp, i32, vp, vp, vp]),
         "gp_posterior": (C.c_int, [vp, vp, i32, vp, i64, C.c_int, vp, vp, vp]),
@@ -100,7 +114,7 @@ def load():
 def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
-            "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_stats", "gp_model_export",
+            "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_lml", "gp_fit_append", "gpbo_last_append_refit", "gp_fit_ml2", "gpbo_last_ml2_evals", "gpbo_nm_selftest", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_last_bracket_violations",
             "gpbo_debug_bound_scale", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
@@ -165,6 +179,12 @@ class Model:
         vals = [C.c_double() for _ in range(4)]
         _check(self.ctx, lib.gp_model_stats(self.handle, s, *[C.byref(v) for v in vals]))
         return dict(zip(("mean", "std", "best", "alpha_l1"), (v.value for v in vals)))
+
+    def lml(self):
+        """gp_model_lml: log marginal likelihood per search (float64 [S])."""
+        out = np.zeros(self.S)
+        _check(self.ctx, load().gp_model_lml(self.handle, out.ctypes.data))
+        return out
 
     def export(self, s):
         """float64 (L, L^-1, alpha) of search s (row-major lower triangles)."""
@@ -306,6 +326,54 @@ class Context:
         _check(self, st, ok=(OK, ENOTPD, WDEGENERATE))
         return Model(self, h, S, n_a, d_a, status, jk)
 
+    def fit_append(self, model, x_new, y_new):
+        """gp_fit_append: model + one new observation per search (x_new [sum d], y_new [S]) ->
+        a new Model (O(n^2) bordered update; the previous model is unchanged)."""
+        px, m1 = _ptr(x_new, np.float32)
+        py, m2 = _ptr(y_new, np.float64)
+        mem = _mem_of((px, m1), (py, m2))
+        S = model.S
+        h = C.c_void_p()
+        status = np.zeros(S, np.int32)
+        jk = np.zeros(S, np.int32)
+        st = load().gp_fit_append(self.handle, model.handle, px, py, mem, C.byref(h),
+                                  status.ctypes.data, jk.ctypes.data)
+        _check(self, st, ok=(OK, ENOTPD, WDEGENERATE))
+        m = Model(self, h, S, [n + 1 for n in model.n], model.d, status, jk)
+        m._inputs = (x_new, y_new)
+        return m
+
+    @property
+    def last_append_refit(self):
+        return int(load().gpbo_last_append_refit(self.handle))
+
+    def fit_ml2(self, n, d, X, y, lengthscale, signal_var, noise_var, kernel=MATERN52,
+                starts=8, iters=200, seed=0, step=0.5, bounds=((1e-3, 10.0), (1e-3, 1e3),
+                                                               (1e-6, 1.0))):
+        """gp_fit_ml2 (host numpy inputs; theta = start 0) -> dict(ls, sf2, sn2, lml,
+        lml_starts [S, starts], evals)."""
+        S = len(n)
+        n_a = np.ascontiguousarray(n, dtype=np.int32)
+        d_a = np.ascontiguousarray(d, dtype=np.int32)
+        arrs = [np.ascontiguousarray(X, np.float32), np.ascontiguousarray(y, np.float64),
+                np.ascontiguousarray(lengthscale, np.float32),
+                np.ascontiguousarray(signal_var, np.float32),
+                np.ascontiguousarray(noise_var, np.float32)]
+        args = FitArgs(S, n_a.ctypes.data, d_a.ctypes.data, *[a.ctypes.data for a in arrs],
+                       int(kernel), HOST)
+        (l0, l1), (f0, f1), (s0, s1) = bounds
+        opts = Ml2Opts(int(starts), int(iters), int(seed), float(step), l0, l1, f0, f1, s0, s1)
+        ls = np.zeros(int(d_a.sum()), np.float32)
+        sf2 = np.zeros(S, np.float32)
+        sn2 = np.zeros(S, np.float32)
+        lml = np.zeros(S)
+        lst = np.zeros((S, int(starts)))
+        _check(self, load().gp_fit_ml2(self.handle, C.byref(args), C.byref(opts), ls.ctypes.data,
+                                       sf2.ctypes.data, sn2.ctypes.data, lml.ctypes.data,
+                                       lst.ctypes.data))
+        return dict(ls=ls, sf2=sf2, sn2=sn2, lml=lml, lml_starts=lst,
+                    evals=int(load().gpbo_last_ml2_evals(self.handle)))
+
     def posterior(self, model, s, Xstar, want=("mu", "var", "ei")):
         """gp_posterior: raw-unit (mu, var, ei) for every row of X* (same space as X*)."""
         px, mem = _ptr(Xstar, np.float32)
@@ -350,6 +418,26 @@ class Context:
             base.ctypes.data if base is not None else None,
             b.ctypes.data if b is not None else None, mem, idx.ctypes.data, ei.ctypes.data))
         return idx, ei
+
+
+NM_OBJ = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_double), C.c_void_p)
+
+
+def nm_selftest(f, x0, lo, hi, step=0.5, iters=200):
+    """Host-only: the library's Nelder-Mead on a Python objective f(x) -> (x, f, f0, nevals)."""
+    x0 = np.ascontiguousarray(x0, np.float64)
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    dim = x0.size
+    cb = NM_OBJ(lambda p, u: float(f(np.ctypeslib.as_array(p, shape=(dim,)).copy())))
+    bx = np.zeros(dim)
+    bf, sf, ne = C.c_double(), C.c_double(), C.c_int64()
+    st = load().gpbo_nm_selftest(dim, x0.ctypes.data, lo.ctypes.data, hi.ctypes.data, step, iters,
+                                 C.cast(cb, C.c_void_p), None, bx.ctypes.data, C.byref(bf),
+                                 C.byref(sf), C.byref(ne))
+    if st != OK:
+        raise GpboError(st, "nm_selftest failed")
+    return bx, bf.value, sf.value, ne.value
 
 
 def tc_selftest(A, B, row_bytes, b_row_off=0):

@@ -40,7 +40,7 @@ def _argmax_vs_oracle(G, w, label, impl=0, S_check=None):
         idx, ei = ctx.score_argmax(m, Xs, off)
         viol, refined, used = ctx.last_violations, ctx.last_refine_count, ctx.last_impl
         oms = H.oracle_fits(w)
-        for s in range(w.S if S_check is None else S_check):
+        for s in range(w.S if S_check is None else min(w.S, S_check)):
             assert m.jitter_k[s] == oms[s].jitter_k, (label, s)
             res = gp.score(oms[s], w.Xstar[s])
             H.check_argmax(res, int(idx[s]), f"{label}[{s}]")

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--M", type=int, default=1 << 18)
     ap.add_argument("--seed", type=int, default=5)
+    ap.add_argument("--update", default="append", choices=["append", "refit"],
+                    help="append: O(n^2) gp_fit_append per iteration (§8(f)2); refit: gp_fit")
     args = ap.parse_args()
     params, blocks, _ = rttddft.table_iv()
     stream = torch.cuda.current_stream()
@@ -52,21 +54,30 @@ def main():
         gpbo.suggest(ctx, m, [sp], [args.M], args.seed + 1, 0, dedup=True)
         m.free()
     torch.cuda.synchronize()
-    dev_ms, impls = [], {}
+    dev_ms, impls, refits = [], {}, 0
+    m = None
     t0 = time.perf_counter()
     for it in range(args.iters):
         e0.record(stream)
-        m = ctx.fit([len(y)], [d], np.ascontiguousarray(X.ravel()), y, ls, sf2, sn2)
+        if m is None or args.update == "refit":
+            if m is not None:
+                m.free()
+            m = ctx.fit([len(y)], [d], np.ascontiguousarray(X.ravel()), y, ls, sf2, sn2)
+        else:  # the surrogate update: one new observation, O(n^2) (gp_fit_append)
+            m2 = ctx.fit_append(m, np.ascontiguousarray(X[-1]), y[-1:].copy())
+            refits += ctx.last_append_refit
+            m.free()
+            m = m2
         idx, xr, ei = gpbo.suggest(ctx, m, [sp], [args.M], args.seed, it, dedup=True)
         e1.record(stream)
         e1.synchronize()
         dev_ms.append(e0.elapsed_time(e1))
         impls[ctx.last_impl] = impls.get(ctx.last_impl, 0) + 1
-        m.free()
         raw = np.asarray(xr[0], np.float64)
         vnew = _vidx(params, raw)
         X = np.concatenate([X, sp.encode(raw[None, :]).astype(np.float32)])
         y = np.concatenate([y, rttddft.objective(vnew[None, :], params)])
+    m.free()
     wall = time.perf_counter() - t0
     names = {1: "cuda-core", 2: "tcgen05", 3: "tcgen05-stream"}
     line = {"metric": "BO iterations/s (config 5 replay)", "value": args.iters / wall,
@@ -76,6 +87,7 @@ def main():
                                    "last": float(dev_ms[-1])},
             "candidates_per_s_device": args.M * args.iters / (np.sum(dev_ms) / 1e3),
             "scoring_kernels": {names.get(k, str(k)): v for k, v in impls.items()},
+            "update": args.update, "append_refits": refits,
             "best_y": float(np.min(y)), "initial_best_y": float(np.min(y[:5]))}
     print(json.dumps(line), flush=True)
     ctx.close()
