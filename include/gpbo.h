@@ -290,6 +290,52 @@ gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
                              int32_t iteration, int32_t dedup, int64_t *idx, double *x_raw,
                              float *ei);
 
+/* ---------------------------------------------------------------- planner
+ * Host-only (no GPU needed): the methodology's interdependence analysis, which emits the batch of
+ * sub-searches the calls above fit and score (§IV.B-D, §VIII).
+ *
+ * gpbo_influence (§IV.B): matrix[r * P + p] = (1/V') sum_i |(baseline[r] - t_i) /
+ *   baseline[r]| over the valid variations i of parameter p (valid [P * V] may be NULL = all;
+ *   V' = their count; NaN when none is valid -- "unknown", not 0), t_i = variations[(p * V + i) *
+ *   R + r] (routine r's runtime with parameter p at its i-th variation, all others at baseline).
+ *   GPBO_EINVAL for a zero or non-finite baseline.
+ * gpbo_plan: routines r (parent[r] = enclosing region or -1; has_metric[r] = its own runtime is
+ *   measured) own parameters (owners[owner_off[p] .. owner_off[p+1]): >= 1 routine; several =
+ *   one kernel used in several regions); shared[p] = 1 when p must keep one value across the
+ *   application.  Routines with a metric and no children are the stage-2 candidates; the others
+ *   (outer regions, routines without a metric such as the MPI grid) get stage-1 searches against
+ *   their metric or the total objective (target -1).  Steps (deterministic, ties -> lower index):
+ *   shared kernels -> owner of highest influence (step 5, L545); a child parameter above the
+ *   cut-off on its parent and on >= 2 sibling children moves to the parent's search (L543);
+ *   cross edges >= cutoff (L235, L254) merge the two routines (shared[p]; union-find) or
+ *   duplicate p into the target's search ("tune twice", L237); a search above dim_cap keeps its
+ *   dim_cap most influential parameters (max over its routines; L167, L249) and drops the rest
+ *   to defaults; budget = max(budget_floor, budget_mult * dims) (L256).
+ *   Outputs (caller arrays sized for R searches): nsearch; per search s: stage (1, 2), target
+ *   routine (-1 = total), budget, dims; tuned[s * P + p] = 1 if s tunes p; dropped[p] = 1 if no
+ *   search tunes p (fixed at its default). */
+typedef struct {
+  int32_t R, P;
+  const int32_t *parent;      /* [R] */
+  const int32_t *has_metric;  /* [R] */
+  const int32_t *owner_off;   /* [P + 1] */
+  const int32_t *owners;      /* [owner_off[P]] */
+  const int32_t *shared;      /* [P] */
+  const double *matrix;       /* [R * P] variability (fractions; 1.0 = 100 %) */
+  double cutoff;              /* e.g. 0.25 synthetic (L254), 0.10 RT-TDDFT (L543) */
+  int32_t dim_cap;            /* 10 (L167) */
+  int32_t budget_mult, budget_floor;  /* 10, 10 (L256 "at least 10 x num_parameters") */
+} gpbo_plan_args;
+typedef struct {
+  int32_t nsearch;
+  int32_t *search_stage, *search_target, *search_budget, *search_dims;  /* [R] */
+  uint8_t *tuned;    /* [R * P] */
+  uint8_t *dropped;  /* [P] */
+} gpbo_plan_out;
+gpbo_status gpbo_influence(int32_t R, int32_t P, int32_t V, const double *baseline,
+                           const double *variations, const uint8_t *valid, double *matrix);
+gpbo_status gpbo_plan(const gpbo_plan_args *args, gpbo_plan_out *out);
+
 /* Number of CUDA kernels the library launched on ctx since creation (for bench accounting). */
 int64_t gpbo_launch_count(const gpbo_ctx *ctx);
 

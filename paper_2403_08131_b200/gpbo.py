@@ -43,6 +43,19 @@ class Ml2Opts(C.Structure):
                 ("sn2_hi", C.c_double)]
 
 
+class PlanArgs(C.Structure):
+    _fields_ = [("R", C.c_int32), ("P", C.c_int32), ("parent", C.c_void_p),
+                ("has_metric", C.c_void_p), ("owner_off", C.c_void_p), ("owners", C.c_void_p),
+                ("shared", C.c_void_p), ("matrix", C.c_void_p), ("cutoff", C.c_double),
+                ("dim_cap", C.c_int32), ("budget_mult", C.c_int32), ("budget_floor", C.c_int32)]
+
+
+class PlanOut(C.Structure):
+    _fields_ = [("nsearch", C.c_int32), ("search_stage", C.c_void_p),
+                ("search_target", C.c_void_p), ("search_budget", C.c_void_p),
+                ("search_dims", C.c_void_p), ("tuned", C.c_void_p), ("dropped", C.c_void_p)]
+
+
 class FitArgs(C.Structure):
     _fields_ = [("S", C.c_int32), ("n", C.c_void_p), ("d", C.c_void_p), ("X", C.c_void_p),
                 ("y", C.c_void_p), ("lengthscale", C.c_void_p), ("signal_var", C.c_void_p),
@@ -77,6 +90,8 @@ def load():
         "gpbo_last_append_refit": (i64, [vp]),
         "gp_fit_ml2": (C.c_int, [vp, C.POINTER(FitArgs), C.POINTER(Ml2Opts), vp, vp, vp, vp, vp]),
         "gpbo_last_ml2_evals": (i64, [vp]),
+        "gpbo_influence": (C.c_int, [i32, i32, i32, vp, vp, vp, vp]),
+        "gpbo_plan": (C.c_int, [C.POINTER(PlanArgs), C.POINTER(PlanOut)]),
         "gpbo_nm_selftest": (C.c_int, [C.c_int, vp, vp, vp, C.c_double, C.c_int, vp, vp, vp, vp,
                                        vp, vp]),
         "gp_model_stats": (C.c_int, [vp, i32, vp, vp, vp, vp]),
@@ -114,7 +129,7 @@ def load():
 def exported_symbols():
     """Names of the entry points include/gpbo.h declares (for the load/export test)."""
     return ["gpbo_nccl_unique_id", "gpbo_ctx_create", "gpbo_ctx_destroy", "gpbo_last_error",
-            "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_lml", "gp_fit_append", "gpbo_last_append_refit", "gp_fit_ml2", "gpbo_last_ml2_evals", "gpbo_nm_selftest", "gp_model_stats", "gp_model_export",
+            "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_lml", "gp_fit_append", "gpbo_last_append_refit", "gp_fit_ml2", "gpbo_last_ml2_evals", "gpbo_nm_selftest", "gpbo_influence", "gpbo_plan", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_last_bracket_violations",
             "gpbo_debug_bound_scale", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
             "gpbo_set_profiling", "gpbo_kernel_time",
@@ -418,6 +433,49 @@ class Context:
             base.ctypes.data if base is not None else None,
             b.ctypes.data if b is not None else None, mem, idx.ctypes.data, ei.ctypes.data))
         return idx, ei
+
+
+def influence(baseline, variations, valid=None):
+    """gpbo_influence (host-only): baseline [R], variations [P, V, R] (routine runtimes),
+    valid [P, V] bool or None -> variability matrix [R, P]."""
+    b = np.ascontiguousarray(baseline, np.float64)
+    v = np.ascontiguousarray(variations, np.float64)
+    P, V, R = v.shape
+    ok = None if valid is None else np.ascontiguousarray(valid, np.uint8)
+    out = np.zeros((R, P))
+    st = load().gpbo_influence(R, P, V, b.ctypes.data, v.ctypes.data,
+                               ok.ctypes.data if ok is not None else None, out.ctypes.data)
+    if st != OK:
+        raise GpboError(st, "gpbo_influence: bad arguments (zero baseline?)")
+    return out
+
+
+def plan(matrix, owners, parent=None, has_metric=None, shared=None, cutoff=0.25, dim_cap=10,
+         budget_mult=10, budget_floor=10):
+    """gpbo_plan (host-only): matrix [R, P]; owners: list (per parameter) of owning routine
+    indices -> list of dicts (stage, target, budget, params) and the dropped parameter list."""
+    M = np.ascontiguousarray(matrix, np.float64)
+    R, P = M.shape
+    par = np.ascontiguousarray(parent if parent is not None else [-1] * R, np.int32)
+    hm = np.ascontiguousarray(has_metric if has_metric is not None else [1] * R, np.int32)
+    off = np.zeros(P + 1, np.int32)
+    off[1:] = np.cumsum([len(o) for o in owners])
+    own = np.ascontiguousarray([r for o in owners for r in o] + [0], np.int32)
+    sh = np.ascontiguousarray(shared if shared is not None else [1] * P, np.int32)
+    args = PlanArgs(R, P, par.ctypes.data, hm.ctypes.data, off.ctypes.data, own.ctypes.data,
+                    sh.ctypes.data, M.ctypes.data, float(cutoff), int(dim_cap), int(budget_mult),
+                    int(budget_floor))
+    arr = [np.zeros(R, np.int32) for _ in range(4)]
+    tuned = np.zeros((R, P), np.uint8)
+    dropped = np.zeros(P, np.uint8)
+    out = PlanOut(0, *[a.ctypes.data for a in arr], tuned.ctypes.data, dropped.ctypes.data)
+    st = load().gpbo_plan(C.byref(args), C.byref(out))
+    if st != OK:
+        raise GpboError(st, "gpbo_plan: bad arguments")
+    searches = [dict(stage=int(arr[0][s]), target=int(arr[1][s]), budget=int(arr[2][s]),
+                     params=[int(p) for p in np.flatnonzero(tuned[s])])
+                for s in range(out.nsearch)]
+    return searches, [int(p) for p in np.flatnonzero(dropped)]
 
 
 NM_OBJ = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_double), C.c_void_p)

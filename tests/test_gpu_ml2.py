@@ -64,7 +64,9 @@ def test_ml2_matches_oracle(G, seed, n, d, kernel):
                     np.full(1, 1e-2, np.float32), kernel=kernel, starts=4, iters=60, seed=11)
     o = ml2.fit_ml2(s.X, s.y, s.lengthscale, 1.0, 1e-2, kernel, starts=4, iters=60, seed=11)
     assert np.all(r["lml"][0] >= r["lml_starts"][0])
-    np.testing.assert_allclose(r["lml_starts"][0], o["lml_starts"], rtol=1e-10)
+    # random starts in the log box can be ill-conditioned (LML ~ -1e4: cond(K) ~ 1e10+), where
+    # both sides' LML carries ~cond u relative rounding
+    np.testing.assert_allclose(r["lml_starts"][0], o["lml_starts"], rtol=1e-7)
     # same algorithm on LML values equal to ~1e-12: the same iterates unless a comparison of two
     # nearly equal objective values flips; then both still satisfy the invariant and reach
     # comparable optima
