@@ -365,7 +365,8 @@ int gpbo_last_score_impl(const gpbo_ctx *ctx);
 /* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel
  * launch (for bench.py's roofline).  gpbo_set_profiling(ctx, 1) enables it and clears the
  * totals; gpbo_kernel_time returns the launch count and summed milliseconds of one kind:
- * 0 = fit (H1-H4), 1 = scoring fast phase (H6-H9), 2 = float64 refine phase, 3 = operand pack. */
+ * 0 = fit (H1-H4), 1 = scoring fast phase (H6-H9), 2 = float64 refine phase, 3 = operand pack,
+ * 4 = precise-mean tier (float64 mu~ for searches with sf2 |alpha|_1 > 1500, reading R13). */
 gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on);
 gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms);
 

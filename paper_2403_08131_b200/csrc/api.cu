@@ -51,8 +51,10 @@ struct gpbo_ctx {
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;
-  double kern_ms[4] = {0, 0, 0, 0};
-  int64_t kern_count[4] = {0, 0, 0, 0};
+  double kern_ms[5] = {0, 0, 0, 0, 0};
+  int64_t kern_count[5] = {0, 0, 0, 0, 0};
+  double *mean_d = nullptr;  // precise-tier float64 means of the current scoring call
+  size_t mean_cap = 0;
   int64_t last_refine = 0;
   int last_impl = 0;
   unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
@@ -110,7 +112,7 @@ gpbo_status fail(gpbo_ctx *ctx, gpbo_status st, const std::string &msg) {
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
-enum { kKernFit = 0, kKernFast = 1, kKernRefine = 2, kKernPack = 3 };
+enum { kKernFit = 0, kKernFast = 1, kKernRefine = 2, kKernPack = 3, kKernMean = 4 };
 
 cudaEvent_t take_event(gpbo_ctx *ctx) {
   if (!ctx->ev_pool.empty()) {
@@ -163,6 +165,18 @@ gpbo_status ensure_stage(gpbo_ctx *ctx, size_t bytes) {
   ctx->stage_cap = 0;
   CK(cudaMalloc(&ctx->stage_d, bytes));
   ctx->stage_cap = bytes;
+  return GPBO_OK;
+}
+
+gpbo_status ensure_mean(gpbo_ctx *ctx, size_t rows) {
+  if (rows <= ctx->mean_cap) return GPBO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->mean_d) CK(cudaFree(ctx->mean_d));
+  ctx->mean_d = nullptr;
+  ctx->mean_cap = 0;
+  const size_t cap = std::max<size_t>(rows, 1 << 16);
+  CK(cudaMalloc(&ctx->mean_d, cap * sizeof(double)));
+  ctx->mean_cap = cap;
   return GPBO_OK;
 }
 
@@ -399,6 +413,21 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     ctx->launches += 1;
     return GPBO_OK;
   }
+  // precise-mean tier (reading R13): float64 mu~ of the candidates of searches whose fit chose
+  // it (sf2 |alpha|_1 > kMeanTierL1) -- decided on the device when the fit is still pending
+  bool need_mean = false;
+  int dmax_raw = 1;
+  for (int i = 0; i < S; ++i) {
+    const SearchMeta &q = model->meta[s_first + i];
+    need_mean = need_mean || model->meta_pending || q.mean_tier;
+    dmax_raw = std::max(dmax_raw, q.d);
+  }
+  need_mean = need_mean && mode != gpbo::kModePosterior;
+  if (need_mean) {
+    st = ensure_mean(ctx, (size_t)rows);
+    if (st) return st;
+    p.mean64 = ctx->mean_d;
+  }
   for (int c = 0; c < nchunk; ++c) {
     const int ta = (int)((int64_t)tiles * c / nchunk), tb = (int)((int64_t)tiles * (c + 1) / nchunk);
     if (nchunk > 1) {
@@ -412,6 +441,12 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
                            (size_t)(e1 - e0) * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
       CK(cudaEventRecord(ctx->feed_ev[c], ctx->copy_stream));
       CK(cudaStreamWaitEvent(ctx->stream, ctx->feed_ev[c], 0));
+    }
+    if (need_mean) {
+      KernTimer tm(ctx, kKernMean);
+      CK(gpbo::launch_mean64(p, model->Xs64, tile, ta, tb - ta, dmax_raw, ctx->mean_d,
+                             ctx->stream));
+      ctx->launches += 1;
     }
     KernTimer t(ctx, kKernFast);
     if (use_tcs)
@@ -544,8 +579,9 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
 extern "C" {
 
 const char *gpbo_version(void) {
-  return "libgpbo 0.2 (sm_100a; fit fp64 1 CTA/search; score: tcgen05 fp16x3 resident / TMA-streamed, "
-         "fp64 direct for small problems, CUDA-core fallback; fp64 refine)";
+  return "libgpbo 0.3 (sm_100a; fit fp64 1 CTA/search + O(n^2) append + ML-II; score: tcgen05 "
+         "fp16x3 resident / TMA-streamed, fp64 precise-mean tier, fp64 direct for small problems, "
+         "CUDA-core fallback; fp64 refine with bracket self-check; host planner)";
 }
 
 gpbo_status gpbo_nccl_unique_id(void *out) {
@@ -612,6 +648,7 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->keys_d) cudaFree(ctx->keys_d);
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
   if (ctx->list_d) cudaFree(ctx->list_d);
+  if (ctx->mean_d) cudaFree(ctx->mean_d);
   harvest_events(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
@@ -651,12 +688,12 @@ gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on) {
   cudaStreamSynchronize(ctx->stream);
   harvest_events(ctx);
   ctx->profiling = on != 0;
-  for (int i = 0; i < 4; ++i) { ctx->kern_ms[i] = 0.0; ctx->kern_count[i] = 0; }
+  for (int i = 0; i < 5; ++i) { ctx->kern_ms[i] = 0.0; ctx->kern_count[i] = 0; }
   return GPBO_OK;
 }
 
 gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms) {
-  if (!ctx || kind < 0 || kind > 3) return GPBO_EINVAL;
+  if (!ctx || kind < 0 || kind > 4) return GPBO_EINVAL;
   cudaStreamSynchronize(ctx->stream);
   harvest_events(ctx);
   if (count) *count = ctx->kern_count[kind];

@@ -197,6 +197,7 @@ append_kernel(const SearchMeta *__restrict__ meta_in, const AppendIO io,
     m.linv_rowsum = fmaxf(P.linv_rowsum, (float)rabs);
     m.linv_absmax = fmax(P.linv_absmax, rmax);
     m.lml = -0.5 * ww - ld - 0.5 * n1 * 1.8378770664093454836;
+    m.mean_tier = sf2 * l1 > kMeanTierL1 ? 1 : 0;
     meta_out[s] = m;
   }
 }

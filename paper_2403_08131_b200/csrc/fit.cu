@@ -632,6 +632,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     // log marginal likelihood of y~ at this theta (the jittered K actually factored):
     // -1/2 y~^T alpha - sum_i log L_ii - n/2 log 2 pi  (Rasmussen & Williams eq. 2.30)
     m.lml = -0.5 * ww - ld - 0.5 * n * 1.8378770664093454836;
+    m.mean_tier = (double)m.sf2 * l1 > kMeanTierL1 ? 1 : 0;
     meta_out[s] = m;
   }
 }

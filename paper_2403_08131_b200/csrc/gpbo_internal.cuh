@@ -48,6 +48,7 @@ struct SearchMeta {
   // fit results
   double mean, std, best, alpha_l1;
   double lml;           // log marginal likelihood of y~ (standardised), -inf if the fit failed
+  int32_t mean_tier;    // 1: precise mean tier (mean64.cu), chosen at fit time (reading R13)
   float pmax;           // max_j |x_j / l|^2 (error-bound input of the fast phase)
   float alpha_max;      // max_j |alpha_j|
   float linv_rowsum;    // max_j sum_k |(L^-1)_jk| (variance error-bound input)
@@ -119,6 +120,7 @@ struct ScoreLaunch {
   uint32_t list_cap;
   float *dbg_mu, *dbg_dmu, *dbg_var, *dbg_dvar, *dbg_eilo, *dbg_eihi;  // debug mode
   unsigned long long *trace;   // optional clock64 event trace of CTA 0 (gpbo_debug_trace)
+  const double *mean64;        // precise-tier float64 mean per launch row (NULL: none)
   float bound_scale;           // error-bound multiplier: 1 (test hook gpbo_debug_bound_scale)
   int32_t break_bracket;       // test hook: halve every EI bracket (deliberately unsound)
 };
@@ -183,6 +185,12 @@ struct AppendIO {
 };
 cudaError_t launch_append(const SearchMeta *meta_in, int S, const AppendIO &io,
                           SearchMeta *meta_out, cudaStream_t stream);
+// Precise-mean tier (mean64.cu): float64 mu~ of every row of the precise-tier searches.
+// A search is precise when sf2 |alpha|_1 > kMeanTierL1 (the float32 mean error is
+// ~ (0.6-6) 1e-8 |alpha|_1, beyond the EI resolution the argmax filter needs from ~1.5e3 on).
+constexpr double kMeanTierL1 = 1500.0;
+cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, int tile_lo,
+                          int tiles, int dmax, double *mean64, cudaStream_t stream);
 // Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
 constexpr int kDirectMaxN = 64;
 cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream);

@@ -91,7 +91,11 @@ score_simt_kernel(const ScoreLaunch p) {
 #pragma unroll
   for (int c = 0; c < DMAX; ++c) q = fmaf(xs[c], xs[c], q);
   const float u = 5.9604645e-8f;
-  const float dmu = 0.2f * u * a1 * (2.f * (float)(d + 3) * (q + mref.pmax) + 64.f) * p.bound_scale;
+  float dmu = 0.2f * u * a1 * (2.f * (float)(d + 3) * (q + mref.pmax) + 64.f) * p.bound_scale;
+  if (p.mean64 != nullptr && mref.mean_tier && valid) {  // precise-mean tier (mean64.cu)
+    mu = p.mean64[row0 + row];
+    dmu = 1e-12f * a1 * p.bound_scale;
+  }
   const float var = fmaxf(sf2 - s2, 0.f);
   const float dvar = var_bound(u, sf2, s2, n, mref.linv_rowsum) * p.bound_scale;
   finish_fast(p, s, valid, row0, row, mu, dmu, var, dvar);

@@ -406,6 +406,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       const int64_t row0s = p.m_off[s];
       const float vun2 = m.vunscale2, sf2 = m.sf2, pmaxh = m.pmax_h, lrs = m.linv_rowsum;
       const int nn = m.n;
+      const bool mtier = p.mean64 != nullptr && m.mean_tier;  // precise-mean tier (mean64.cu)
       // variance bound 4 var_bound(u, sf2, s2, n, lrs) = vbk (sf2 + s2), its factor hoisted
       const float vbk = 4.f * 16.f * 5.9604645e-8f * sqrtf((float)nn) * (1.f + 0.01f * lrs * sqrtf(sf2));
       for (int tl = 0; tl < T; ++tl) {
@@ -459,7 +460,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         if (!dbl || vb == 1) ++vb1c;
         const uint32_t par = ti & 1u;
         tc::mbar_wait(bar(B_PF0 + par), (ti >> 1) & 1u);
-        const double mu_t = part_mu[par * 128 + row] + part_mu[(2 + par) * 128 + row];
+        double mu_t = part_mu[par * 128 + row] + part_mu[(2 + par) * 128 + row];
         const float a1_t = part_a1[par * 128 + row] + part_a1[(2 + par) * 128 + row];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_PE0 + par));
@@ -473,7 +474,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const float var = fmaxf(sf2 - s2, 0.f);
         // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for
         // the float16x3 augmented GEMM; margin x4
-        const float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f) * p.bound_scale;
+        float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f) * p.bound_scale;
+        if (mtier && rloc < Ms) {  // precise tier: the float64 mean (mean64.cu)
+          mu_t = p.mean64[row0s + rloc];
+          dmu = 1e-12f * a1_t * p.bound_scale;
+        }
         const float dvar = vbk * (sf2 + s2) * p.bound_scale;
 #ifndef GPBO_EXP_NOFINISH  // timing experiment only
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,

@@ -302,7 +302,7 @@ class Context:
     def set_profiling(self, on=True):
         _check(self, load().gpbo_set_profiling(self.handle, int(bool(on))))
 
-    KERNELS = ("fit", "fast", "refine", "pack")
+    KERNELS = ("fit", "fast", "refine", "pack", "mean")
 
     def kernel_time(self, kind):
         """(launches, total ms) of one library kernel kind since set_profiling(True)."""

@@ -1,0 +1,205 @@
+"""the paper's Table III protocol (§IV.D, Table III) replayed
+on the five synthetic cases with this library as the BO engine -- orderings only (the absolute
+minima and times are GPTune- and hardware-bound).
+
+Strategies per (case, seed), all on F = sum of the four groups' log|.| terms (Fig. 1 + Table I,
+noise sigma = 0.1 per eps occurrence, reading R15), raw domain [-50, 50]^20:
+  random       200 uniform configurations, min observed F
+  joint        one 20-D BO search, N = 200 (5 random initial points + 195 BO iterations)
+  independent  G1, G2, G3, G4: four 5-D BO searches, N = 50 each, each minimising its own group's
+               term with the other variables at the default configuration; run as ONE batched
+               BO (the searches are independent: one gp_fit / bo_suggest_batch call per round)
+  planned      the planner's searches (gpbo_plan on the noise-free sensitivity matrix of this
+               case at the 25 % cut-off): typically G1, G2, G3+G4 with N = 50, 50, 100,
+               batched the same way; a merged search minimises the sum of its groups' terms
+The joint search reports its best observed F (as random search does); the final configuration of
+a multi-search strategy combines every search's best point (the other variables at the default)
+and its F is evaluated once (noisy).  Wall time per strategy is reported beside the minimum.
+BO step: gp_fit (Matern-5/2; ML-II hyper-parameters by gp_fit_ml2 every `--ml2-every`
+iterations, gp_fit_append O(n^2) updates in between) + bo_suggest_batch over M on-device
+candidates (H5 generation, no dedup needed for reals).  The default configuration is the
+sensitivity analysis's random baseline (seeded).
+
+    python tools/table3_replay.py [--cases 1 2 3 4 5] [--seeds 5] [--M 16384] [--out file.json]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2403_08131_b200 import gpbo  # noqa: E402
+from workloads import synthetic as syn  # noqa: E402
+
+LO, HI = -50.0, 50.0
+SIGMA = 0.1
+
+
+def group_terms(X, case, rng):
+    """(n, 4) log|G_k| terms of F at raw configurations X (n, 20), noisy (12 eps draws each)."""
+    eps = rng.normal(0.0, SIGMA, size=(X.shape[0], syn.N_EPS))
+    e = [eps[:, 0:5], eps[:, 5:10], eps[:, 10], eps[:, 11]]
+    g = [syn.group1(X, eps), syn.group2(X, eps), syn.group3(X, case, eps), syn.group4(X, eps)]
+    del e
+    return np.stack([np.log(np.abs(v) + syn.DELTA) for v in g], 1)
+
+
+def sensitivity_plan(case, baseline, cutoff=0.25):
+    """Noise-free sensitivity (100 variations of +10 %) -> gpbo_plan (library)."""
+    def terms(X):
+        return np.stack([np.log(np.abs(v) + syn.DELTA) for v in
+                         (syn.group1(X), syn.group2(X), syn.group3(X, case), syn.group4(X))], 1)
+    base = terms(baseline[None, :])[0]
+    var = np.zeros((20, 100, 4))
+    for p in range(20):
+        X = np.repeat(baseline[None, :], 100, 0)
+        X[:, p] = baseline[p] * 1.1 ** np.arange(1, 101)
+        var[p] = terms(X)
+    M = gpbo.influence(base, var)
+    searches, dropped = gpbo.plan(M, [[p // 5] for p in range(20)], cutoff=cutoff)
+    return [s["params"] for s in searches], [s["budget"] for s in searches]
+
+
+ML2 = dict(starts=4, iters=60)
+
+
+def batched_bo(ctx, searches, budgets, groups, case, default, rng, seed, M, ml2_every, n0=5):
+    """Run len(searches) BO searches together.  searches[s]: parameter indices; groups[s]: the
+    group terms it minimises.  Returns per search (best raw sub-configuration, best y)."""
+    S = len(searches)
+    d = [len(p) for p in searches]
+    spaces = [gpbo.Space(ctx, [{"kind": 0, "lo": LO, "hi": HI}] * d[s]) for s in range(S)]
+    Xe = [np.zeros((0, d[s]), np.float32) for s in range(S)]   # encoded history
+    Xr = [np.zeros((0, d[s])) for s in range(S)]               # raw history
+    Y = [np.zeros(0) for _ in range(S)]
+
+    def evaluate(s, raw):
+        X = np.repeat(default[None, :], raw.shape[0], 0)
+        X[:, searches[s]] = raw
+        return group_terms(X, case, rng)[:, groups[s]].sum(1)
+
+    for s in range(S):  # initial design: n0 uniform points
+        raw = rng.uniform(LO, HI, size=(n0, d[s]))
+        Xr[s] = raw
+        Xe[s] = spaces[s].encode(raw)
+        Y[s] = evaluate(s, raw)
+    theta = [(np.full(d[s], 0.4 * np.sqrt(d[s]), np.float32), 1.0, 1e-3) for s in range(S)]
+    model, act_prev = None, None
+    it = 0
+    while True:
+        act = [s for s in range(S) if len(Y[s]) < budgets[s]]
+        if not act:
+            break
+        refit = it % ml2_every == 0 or model is None or act != act_prev
+        if it % ml2_every == 0:
+            r = ctx.fit_ml2([len(Y[s]) for s in act], [d[s] for s in act],
+                            np.concatenate([Xe[s].ravel() for s in act]),
+                            np.concatenate([Y[s] for s in act]),
+                            np.concatenate([theta[s][0] for s in act]),
+                            np.array([theta[s][1] for s in act], np.float32),
+                            np.array([theta[s][2] for s in act], np.float32),
+                            starts=ML2["starts"], iters=ML2["iters"], seed=seed * 1000 + it)
+            o = 0
+            for j, s in enumerate(act):
+                theta[s] = (r["ls"][o:o + d[s]].copy(), float(r["sf2"][j]), float(r["sn2"][j]))
+                o += d[s]
+        if refit:
+            if model is not None:
+                model.free()
+            model = ctx.fit([len(Y[s]) for s in act], [d[s] for s in act],
+                            np.concatenate([Xe[s].ravel() for s in act]),
+                            np.concatenate([Y[s] for s in act]),
+                            np.concatenate([theta[s][0] for s in act]),
+                            np.array([theta[s][1] for s in act], np.float32),
+                            np.array([theta[s][2] for s in act], np.float32))
+        else:  # same hyper-parameters: O(n^2) append of the last observations
+            m2 = ctx.fit_append(model, np.concatenate([Xe[s][-1] for s in act]),
+                                np.array([Y[s][-1] for s in act]))
+            model.free()
+            model = m2
+        act_prev = act
+        idx, xr, ei = gpbo.suggest(ctx, model, [spaces[s] for s in act], [M] * len(act),
+                                   seed, it, dedup=False)
+        for j, s in enumerate(act):
+            raw = np.asarray(xr[j], np.float64)[None, :]
+            Xr[s] = np.concatenate([Xr[s], raw])
+            Xe[s] = np.concatenate([Xe[s], spaces[s].encode(raw)])
+            Y[s] = np.concatenate([Y[s], evaluate(s, raw)])
+        it += 1
+    if model is not None:
+        model.free()
+    return [(Xr[s][int(np.argmin(Y[s]))], float(Y[s].min())) for s in range(S)]
+
+
+def run(ctx, case, seed, M, ml2_every, only=None):
+    rng = np.random.default_rng(1000 * case + seed)
+    default = rng.uniform(LO, HI, 20)
+    out = {}
+    # random search (parallelisable; one batch)
+    t0 = time.perf_counter()
+    R = rng.uniform(LO, HI, size=(200, 20))
+    out["random"] = dict(min=float(group_terms(R, case, rng).sum(1).min()),
+                         time=time.perf_counter() - t0)
+    strategies = {
+        "joint": ([list(range(20))], [200], [[0, 1, 2, 3]]),
+        "independent": ([list(range(5 * g, 5 * g + 5)) for g in range(4)], [50] * 4,
+                        [[g] for g in range(4)]),
+    }
+    ps, bs = sensitivity_plan(case, default)
+    strategies["planned"] = (ps, bs, [sorted({p // 5 for p in s}) for s in ps])
+    for name, (searches, budgets, groups) in strategies.items():
+        if only and name not in only:
+            continue
+        t0 = time.perf_counter()
+        best = batched_bo(ctx, searches, budgets, groups, case, default, rng,
+                          seed * 7 + len(name), M, ml2_every)
+        x = default.copy()
+        for (xb, _), params in zip(best, searches):
+            x[params] = xb
+        if len(searches) == 1 and len(searches[0]) == 20:
+            f = best[0][1]  # a search on F itself: its best observed value (as random search)
+        else:  # combined configuration of several searches: one (noisy) evaluation of F
+            f = float(group_terms(x[None, :], case, rng).sum())
+        out[name] = dict(min=f, time=time.perf_counter() - t0,
+                         searches=[len(s) for s in searches], budgets=budgets)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, nargs="+", default=[1, 2, 3, 4, 5])
+    ap.add_argument("--seeds", type=int, default=5)
+    ap.add_argument("--M", type=int, default=1 << 14)
+    ap.add_argument("--ml2-every", type=int, default=10)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--ml2-starts", type=int, default=4)
+    ap.add_argument("--ml2-iters", type=int, default=60)
+    ap.add_argument("--only", nargs="*", default=None)
+    args = ap.parse_args()
+    import torch
+    ctx = gpbo.Context(device=0, stream=torch.cuda.current_stream())
+    ML2.update(starts=args.ml2_starts, iters=args.ml2_iters)
+    res = {}
+    for case in args.cases:
+        runs = [run(ctx, case, seed, args.M, args.ml2_every, args.only)
+                for seed in range(args.seeds)]
+        agg = {k: dict(mean_min=float(np.mean([r[k]["min"] for r in runs])),
+                       std_min=float(np.std([r[k]["min"] for r in runs])),
+                       mean_time=float(np.mean([r[k]["time"] for r in runs])))
+               for k in runs[0]}
+        if "planned" in runs[0]:
+            agg["planned_searches"] = runs[0]["planned"]["searches"]
+        res[case] = agg
+        print(json.dumps({"case": case, **agg}), flush=True)
+    ctx.close()
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
