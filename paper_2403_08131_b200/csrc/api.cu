@@ -55,6 +55,7 @@ struct gpbo_ctx {
   int64_t kern_count[5] = {0, 0, 0, 0, 0};
   double *mean_d = nullptr;  // precise-tier float64 means of the current scoring call
   size_t mean_cap = 0;
+  double *etab_d = nullptr;  // e^{-k/16} table of the precise tier
   int64_t last_refine = 0;
   int last_impl = 0;
   unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
@@ -169,6 +170,12 @@ gpbo_status ensure_stage(gpbo_ctx *ctx, size_t bytes) {
 }
 
 gpbo_status ensure_mean(gpbo_ctx *ctx, size_t rows) {
+  if (!ctx->etab_d) {  // the precise tier's e^{-k/16} table (mean64.cu), once per ctx
+    std::vector<double> t(gpbo::mean64_exp_table_size());
+    gpbo::mean64_exp_table(t.data());
+    CK(cudaMalloc(&ctx->etab_d, t.size() * sizeof(double)));
+    CK(cudaMemcpy(ctx->etab_d, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   if (rows <= ctx->mean_cap) return GPBO_OK;
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->mean_d) CK(cudaFree(ctx->mean_d));
@@ -445,7 +452,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     if (need_mean) {
       KernTimer tm(ctx, kKernMean);
       CK(gpbo::launch_mean64(p, model->Xs64, tile, ta, tb - ta, dmax_raw, ctx->mean_d,
-                             ctx->stream));
+                             ctx->etab_d, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
     }
     KernTimer t(ctx, kKernFast);
@@ -649,6 +656,7 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   if (ctx->keys_h) cudaFreeHost(ctx->keys_h);
   if (ctx->list_d) cudaFree(ctx->list_d);
   if (ctx->mean_d) cudaFree(ctx->mean_d);
+  if (ctx->etab_d) cudaFree(ctx->etab_d);
   harvest_events(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;

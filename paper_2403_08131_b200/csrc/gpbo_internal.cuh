@@ -190,7 +190,10 @@ cudaError_t launch_append(const SearchMeta *meta_in, int S, const AppendIO &io,
 // ~ (0.6-6) 1e-8 |alpha|_1, beyond the EI resolution the argmax filter needs from ~1.5e3 on).
 constexpr double kMeanTierL1 = 1500.0;
 cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, int tile_lo,
-                          int tiles, int dmax, double *mean64, cudaStream_t stream);
+                          int tiles, int dmax, double *mean64, const double *etab, int num_sms,
+                          cudaStream_t stream);
+void mean64_exp_table(double *host);
+int mean64_exp_table_size();
 // Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
 constexpr int kDirectMaxN = 64;
 cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream);

@@ -16,6 +16,7 @@
 // One thread per candidate row, a block per tile of the scoring launch's tiling (tile_first);
 // the training points x_j / l (float64), |x_j / l|^2 and alpha_j are staged through shared
 // memory in chunks of kChunk points (broadcast reads).  Searches of the fast tier exit at once.
+#include <algorithm>
 #include <cmath>
 
 #include "gpbo_internal.cuh"
@@ -25,83 +26,138 @@ namespace gpbo {
 namespace {
 
 constexpr int kChunk = 64;
+constexpr int kExpTab = 1024;  // e^{-k/16}, k < 1024 (arguments >= 64: e^-64 ~ 1.6e-28 -> 0)
 
-__device__ __forceinline__ double kval64(double r2, double sf2, int kind) {
-  if (kind == GPBO_RBF) return sf2 * exp(-0.5 * r2);
-  const double r = sqrt(r2);
-  const double s5 = 2.23606797749978969640917366873;
-  return sf2 * (1.0 + s5 * r + (5.0 / 3.0) * r2) * exp(-s5 * r);
+// e^{-s} for s >= 0 in float64: s = k/16 + f, f in [0, 1/16): e^{-k/16} from the table times a
+// degree-9 Taylor polynomial of e^{-f} (truncation (1/16)^10/10! ~ 2.6e-19)
+__device__ __forceinline__ double exp_neg(double s, const double *tab) {
+  const double t = s * 16.0;
+  if (!(t < (double)kExpTab)) return 0.0;
+  const int k = (int)t;
+  const double f = -(s - (double)k * 0.0625);
+  double p = 2.7557319223985893e-06;   // 1/9!
+  p = fma(p, f, 2.4801587301587302e-05);  // 1/8!
+  p = fma(p, f, 1.9841269841269841e-04);  // 1/7!
+  p = fma(p, f, 1.3888888888888889e-03);  // 1/6!
+  p = fma(p, f, 8.3333333333333333e-03);  // 1/5!
+  p = fma(p, f, 4.1666666666666667e-02);  // 1/4!
+  p = fma(p, f, 1.6666666666666667e-01);  // 1/3!
+  p = fma(p, f, 0.5);
+  p = fma(p, f, 1.0);
+  p = fma(p, f, 1.0);
+  return tab[k] * p;
+}
+
+// sqrt(r2) in float64 from the MUFU reciprocal square root refined by two Newton steps
+__device__ __forceinline__ double sqrt_nr(double r2) {
+  if (!(r2 > 0.0)) return r2 == 0.0 ? 0.0 : r2;  // 0 -> 0, NaN -> NaN
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) y = fma(0.5 * y, fma(-r2, y * y, 1.0), y);
+  const double r = r2 * y;
+  return fma(0.5 * y, fma(-r, r, r2), r);  // one correction of r itself
+}
+
+__device__ __forceinline__ double kval64(double r2, double sf2, int kind, const double *tab) {
+  if (kind == GPBO_RBF) return sf2 * exp_neg(0.5 * r2, tab);
+  const double s = 2.23606797749978969640917366873 * sqrt_nr(r2);
+  return sf2 * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0) * exp_neg(s, tab);
 }
 
 template <int DMAX>
 __global__ void __launch_bounds__(128)
-mean64_kernel(const ScoreLaunch p, const double *__restrict__ Xs64, int tile, int tile_lo,
-              double *mean64) {
-  __shared__ double xs[kChunk][DMAX + 1];
+mean64_kernel(const ScoreLaunch p, const double *__restrict__ Xs64, const double *__restrict__ etab,
+              int tile, int tile_lo, int tiles, double *mean64) {
+  __shared__ __align__(16) double xs[kChunk][DMAX];
   __shared__ double qa[kChunk][2];  // |x_j / l|^2, alpha_j
-  const int t = tile_lo + (int)blockIdx.x;
-  const int s = search_of(p.tile_first, p.S, t);
-  const SearchMeta &m = p.meta[s];
-  if (!m.mean_tier || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
-  const int n = m.n, d = m.d;
-  const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
-  const int64_t row = (int64_t)(t - p.tile_first[s]) * tile + threadIdx.x;
-  const bool valid = threadIdx.x < tile && row < Ms;
-  const float *x = p.Xstar + p.x_off[s] + row * d;
-  const float *ls = p.ls32 + m.ls_off;
-  double xr[DMAX];
-  double q = 0.0;
+  __shared__ double tab[kExpTab];
+  // nothing to do unless a search of the launch is in the precise tier (decided by the fit,
+  // possibly still pending on the host): one early exit per block of the persistent grid
+  bool any = false;
+  for (int i = 0; i < p.S && !any; ++i)
+    any = p.meta[i].mean_tier && (p.meta[i].status == GPBO_OK || p.meta[i].status == GPBO_WDEGENERATE);
+  if (!any) return;
+  for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) tab[e] = etab[e];
+  for (int t = tile_lo + (int)blockIdx.x; t < tile_lo + tiles; t += gridDim.x) {
+    const int s = search_of(p.tile_first, p.S, t);
+    const SearchMeta &m = p.meta[s];
+    if (!m.mean_tier || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) continue;
+    const int n = m.n, d = m.d;
+    const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
+    const int64_t row = (int64_t)(t - p.tile_first[s]) * tile + threadIdx.x;
+    const bool valid = threadIdx.x < tile && row < Ms;
+    const float *x = p.Xstar + p.x_off[s] + (valid ? row : 0) * d;
+    const float *ls = p.ls32 + m.ls_off;
+    double xr[DMAX];
+    double q = 0.0;
 #pragma unroll
-  for (int c = 0; c < DMAX; ++c) {
-    xr[c] = (valid && c < d) ? (double)x[c] / (double)ls[c] : 0.0;
-    q = fma(xr[c], xr[c], q);
-  }
-  const double *Xj = Xs64 + m.x_off;  // column-major d x n
-  const double *alpha = p.alpha64 + m.a_off;
-  const double sf2 = m.sf2;
-  // padded coordinates c >= d stay 0 (they multiply zeros of xr; never NaN garbage)
-  for (int e = threadIdx.x; e < kChunk * (DMAX + 1); e += blockDim.x) (&xs[0][0])[e] = 0.0;
-  double mu = 0.0;
-  for (int j0 = 0; j0 < n; j0 += kChunk) {
-    const int cnt = min(kChunk, n - j0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt * d; e += blockDim.x) {
-      const int c = e / cnt, j = e - c * cnt;
-      xs[j][c] = Xj[(int64_t)c * n + j0 + j];
+    for (int c = 0; c < DMAX; ++c) {
+      xr[c] = (valid && c < d) ? (double)x[c] / (double)ls[c] : 0.0;
+      q = fma(xr[c], xr[c], q);  // NaN inputs stay NaN through q, dot and mu
     }
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-      double qj = 0.0;
-      for (int c = 0; c < d; ++c) {
-        const double v = Xj[(int64_t)c * n + j0 + j];
-        qj = fma(v, v, qj);
+    const double *Xj = Xs64 + m.x_off;  // column-major d x n
+    const double *alpha = p.alpha64 + m.a_off;
+    const double sf2 = m.sf2;
+    double mu = 0.0;
+    for (int j0 = 0; j0 < n; j0 += kChunk) {
+      const int cnt = min(kChunk, n - j0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kChunk * DMAX; e += blockDim.x) {
+        const int j = e / DMAX, c = e - j * DMAX;
+        xs[j][c] = (j < cnt && c < d) ? Xj[(int64_t)c * n + j0 + j] : 0.0;
       }
-      qa[j][0] = qj;
-      qa[j][1] = alpha[j0 + j];
-    }
-    __syncthreads();
-    for (int j = 0; j < cnt; ++j) {
-      double dot = 0.0;
+      for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        double qj = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double v = Xj[(int64_t)c * n + j0 + j];
+          qj = fma(v, v, qj);
+        }
+        qa[j][0] = qj;
+        qa[j][1] = alpha[j0 + j];
+      }
+      __syncthreads();
+      for (int j = 0; j < cnt; ++j) {
+        double d0 = 0.0, d1 = 0.0;  // two independent chains
+        const double2 *xj = reinterpret_cast<const double2 *>(xs[j]);
 #pragma unroll
-      for (int c = 0; c < DMAX; ++c) dot = fma(xr[c], xs[j][c], dot);  // padded c: xr = 0
-      const double r2 = fmax(q + qa[j][0] - 2.0 * dot, 0.0);
-      mu = fma(kval64(r2, sf2, m.kernel), qa[j][1], mu);
+        for (int c = 0; c < DMAX / 2; ++c) {
+          const double2 v = xj[c];
+          d0 = fma(xr[2 * c], v.x, d0);
+          d1 = fma(xr[2 * c + 1], v.y, d1);
+        }
+        double r2 = q + qa[j][0] - 2.0 * (d0 + d1);
+        r2 = r2 < 0.0 ? 0.0 : r2;  // (NaN propagates)
+        mu = fma(kval64(r2, sf2, m.kernel, tab), qa[j][1], mu);
+      }
     }
+    if (valid) mean64[p.m_off[s] + row] = mu;
   }
-  if (valid) mean64[p.m_off[s] + row] = mu;
 }
 
 }  // namespace
 
 cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, int tile_lo,
-                          int tiles, int dmax, double *mean64, cudaStream_t stream) {
+                          int tiles, int dmax, double *mean64, const double *etab, int num_sms,
+                          cudaStream_t stream) {
   if (tiles <= 0) return cudaSuccess;
   const int thr = tile <= 64 ? 64 : 128;
-  // xs[j][c] needs d <= DMAX; padded coordinates multiply zeros
-  if (dmax <= 8) mean64_kernel<8><<<tiles, thr, 0, stream>>>(p, Xs64, tile, tile_lo, mean64);
-  else if (dmax <= 16) mean64_kernel<16><<<tiles, thr, 0, stream>>>(p, Xs64, tile, tile_lo, mean64);
-  else if (dmax <= 32) mean64_kernel<32><<<tiles, thr, 0, stream>>>(p, Xs64, tile, tile_lo, mean64);
-  else mean64_kernel<64><<<tiles, thr, 0, stream>>>(p, Xs64, tile, tile_lo, mean64);
-  return cudaGetLastError();
+  const int grid = std::min(tiles, num_sms * 8);
+#define GPBO_MEAN64(D)                                                                          \
+  if (dmax <= D) {                                                                              \
+    mean64_kernel<D><<<grid, thr, 0, stream>>>(p, Xs64, etab, tile, tile_lo, tiles, mean64);    \
+    return cudaGetLastError();                                                                  \
+  }
+  GPBO_MEAN64(4) GPBO_MEAN64(8) GPBO_MEAN64(12) GPBO_MEAN64(16) GPBO_MEAN64(20) GPBO_MEAN64(24)
+  GPBO_MEAN64(32) GPBO_MEAN64(40) GPBO_MEAN64(48) GPBO_MEAN64(56) GPBO_MEAN64(64)
+#undef GPBO_MEAN64
+  return cudaErrorInvalidValue;
 }
+
+// e^{-k/16}, k < kExpTab, in float64 (host std::exp; the device table of exp_neg)
+void mean64_exp_table(double *host) {
+  for (int k = 0; k < kExpTab; ++k) host[k] = std::exp(-k / 16.0);
+}
+int mean64_exp_table_size() { return kExpTab; }
 
 }  // namespace gpbo

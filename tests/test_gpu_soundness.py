@@ -138,3 +138,26 @@ def test_no_violation_on_parity_workloads(G, name, make, impl):
         pytest.skip("outside the tcgen05 envelope")
     viol, refined, used = _argmax_vs_oracle(G, w, name, impl=impl, S_check=4)
     assert viol == 0, (name, impl, viol, refined)
+
+
+def test_precise_mean_tier_bo_layout(G):
+    """Reading R13: a BO-like training set (|alpha|_1 large) selects the float64 mean tier; the
+    fast phase then reports the float64 mean (to float32 output rounding) and the refine stays
+    sparse (it flagged ~all candidates without the tier)."""
+    gpbo, ctx = G
+    w = gen.make(2, M=1 << 18, layout="bo")
+    m = ctx.fit(*H.pack(w), kernel=w.kernel)
+    st = m.stats(0)
+    om = H.oracle_fits(w)[0]
+    assert st["alpha_l1"] * om.sf2 > 1500.0, st
+    import torch
+    Xs = torch.from_numpy(np.ascontiguousarray(w.Xstar[0][:8192])).cuda()
+    fp = ctx.debug_fast_phase(m, 0, Xs)
+    res = gp.score(om, w.Xstar[0][:8192])
+    mu = fp["mu"].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(mu - res.mu) / np.maximum(np.abs(res.mu), 1.0)) <= 2e-7
+    Xall, off = H.pack_candidates(w)
+    idx, _ = ctx.score_argmax(m, Xall, off)
+    assert ctx.last_refine_count < 4096 and ctx.last_violations == 0, ctx.last_refine_count
+    H.check_argmax(gp.score(om, w.Xstar[0]), int(idx[0]), "bo-tier")
+    m.free()
