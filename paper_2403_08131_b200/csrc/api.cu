@@ -816,6 +816,23 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
   return GPBO_OK;
 }
 
+// CTAs per search of the cluster fit, or 0 for the one-CTA kernel (GPBO_FIT=single)
+int fit_cluster_size(const gpbo_ctx *ctx, int S, int nmax) {
+  static const bool single = [] {
+    const char *e = getenv("GPBO_FIT");
+    return e && !strcmp(e, "single");
+  }();
+  // measured (profiles/r02): for n <= 216 the one-CTA kernel keeps its working matrix in shared
+  // memory and the cluster's DSMEM hops (~2.5 k cycles per panel) cost as much as the split
+  // trailing update saves (n = 200: 0.139 vs 0.140 ms; 64 x n = 100: 0.056 vs 0.084 ms); for
+  // n > 216 the one-CTA kernel streams W through L2 and the cluster wins (n = 500: 1.27 -> 0.68 ms)
+  if (single || nmax <= gpbo::kFitSmemMaxN) return 0;
+  const int per = ctx->num_sms / std::max(S, 1);
+  int Cc = per >= 8 ? 8 : per >= 4 ? 4 : per >= 2 ? 2 : 1;
+  while (Cc < 8 && gpbo::fit_cluster_smem(nmax, Cc) > gpbo::kFitSmemBudget) Cc *= 2;
+  return gpbo::fit_cluster_smem(nmax, Cc) <= gpbo::kFitSmemBudget ? Cc : 0;
+}
+
 // lml_only (ML-II objective evaluations): no tcgen05 operand image is reserved; the model is
 // read for its statistics and freed, never scored.
 gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bool wait,
@@ -883,8 +900,16 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   {
     KernTimer t(ctx, kKernFit);
     CKM(gpbo::launch_gram(meta_in, S, m->nmax, m->dmax, io, ctx->stream));
-    CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream,
-                         m->nmax <= gpbo::kFitSmemMaxN));
+    // the factorisation: a cluster of Cc CTAs per search (fit_cluster.cu) -- as many CTAs per
+    // search as the SMs allow (~148 / S), and enough that the distributed working matrix fits in
+    // their shared memory; GPBO_FIT=single selects the one-CTA kernel (fit.cu) for A/B runs
+    const int Cc = fit_cluster_size(ctx, S, m->nmax);
+    if (Cc > 0)
+      CKM(gpbo::launch_fit_cluster(meta_in, S, Cc, gpbo::fit_cluster_smem(m->nmax, Cc), io,
+                                   m->meta_d, ctx->stream));
+    else
+      CKM(gpbo::launch_fit(meta_in, S, smem_max, io, m->meta_d, ctx->stream,
+                           m->nmax <= gpbo::kFitSmemMaxN));
   }
   ctx->launches += 2;  // gram_kernel + fit_kernel
   // the tcgen05 operand images are packed by the first tcgen05 scoring call (run_score): small

@@ -166,6 +166,10 @@ cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, con
                         cudaStream_t stream);
 cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const FitIO &io,
                        SearchMeta *meta_out, cudaStream_t stream, bool pdl);
+// Cluster fit (fit_cluster.cu): Cc CTAs per search, the working matrix in their shared memory.
+int fit_cluster_smem(int n, int Cc);
+cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem_bytes,
+                               const FitIO &io, SearchMeta *meta_out, cudaStream_t stream);
 cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
                                  const float *ls32, const double *Linv64, float *Xs32,
                                  float *LT32, cudaStream_t stream);
@@ -186,9 +190,13 @@ struct AppendIO {
 cudaError_t launch_append(const SearchMeta *meta_in, int S, const AppendIO &io,
                           SearchMeta *meta_out, cudaStream_t stream);
 // Precise-mean tier (mean64.cu): float64 mu~ of every row of the precise-tier searches.
-// A search is precise when sf2 |alpha|_1 > kMeanTierL1 (the float32 mean error is
-// ~ (0.6-6) 1e-8 |alpha|_1, beyond the EI resolution the argmax filter needs from ~1.5e3 on).
-constexpr double kMeanTierL1 = 1500.0;
+// A search is precise when sf2 |alpha|_1 > kMeanTierL1.  SURVEY.md R13 put the float32 mean's
+// trouble at |alpha|_1 >~ 1.5e3, but the fast phase's per-candidate bound uses sum_j |k_j alpha_j|,
+// which is far smaller for most candidates: measured, the argmax filter stays sparse up to
+// |alpha|_1 ~ 3e4 (config 3's searches: 310 .. 2.98e4, ~2.2k refined of 2^24) and collapses for
+// BO-like training sets (configs 2/4 in the "bo" layout: |alpha|_1 ~ 1.7e5, every candidate
+// flagged).  The tier only changes the cost, never the result (the refine decides every key).
+constexpr double kMeanTierL1 = 5.0e4;
 cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, int tile_lo,
                           int tiles, int dmax, double *mean64, const double *etab, int num_sms,
                           cudaStream_t stream);
