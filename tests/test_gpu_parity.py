@@ -315,7 +315,9 @@ def test_fast_phase_brackets_contain_oracle(G, name, make, impl):
                               var_ratio=float((evar / o["dvar"]).max()),
                               mu_err=float(emu.max()), var_err=float(evar.max()),
                               alpha_l1=float(np.abs(oms[s].alpha).sum())))
-            assert np.all(emu <= o["dmu"]), (name, s, stats[-1])
+            # (the debug output stores mu~ as float32: its rounding, 2^-24 |mu~|, is not part of
+            # the fast phase's bound -- the precise-mean tier's float64 mean has dmu ~ 1e-12)
+            assert np.all(emu <= o["dmu"] + 6e-8 * np.abs(res.mu)), (name, s, stats[-1])
             assert np.all(evar <= o["dvar"]), (name, s, stats[-1])
             live = res.ei_all >= 1e-30  # below, float32 EI underflows on both sides (R11)
             assert np.all(o["ei_lo"][live] <= res.ei_all[live] * (1 + 1e-12)), (name, s)
