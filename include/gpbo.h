@@ -359,7 +359,8 @@ gpbo_status gpbo_debug_bound_scale(gpbo_ctx *ctx, float scale);
 int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
 /* Fast-phase implementation of the last scoring call: 1 = CUDA-core, 2 = tcgen05 with the
  * shared-memory-resident operand image, 3 = tcgen05 with streamed operands, 4 = float64 direct
- * (small problems; no refine phase). */
+ * (small problems; no refine phase), 5 = float64 dense refine of every row (gp_posterior beyond
+ * the direct kernel's envelope: no fast phase). */
 int gpbo_last_score_impl(const gpbo_ctx *ctx);
 
 /* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel

@@ -301,7 +301,12 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   const bool direct = mode != gpbo::kModeDebug && nmax <= gpbo::kDirectMaxN &&
                       (ctx->score_impl == 4 || (ctx->score_impl == 0 && work <= 16777216.0));
   if (direct) use_tc = use_tcs = false;
-  if (ctx->score_impl == 2 && !use_tc)
+  // gp_posterior outside the direct kernel's envelope: every row is scored by the float64 dense
+  // refine (its mu / var / EI outputs); the fast phase would only be recomputed there, so it is
+  // not launched (nor the operand pack)
+  const bool dense_only = mode == gpbo::kModePosterior && !direct;
+  if (dense_only) use_tc = use_tcs = false;
+  if (ctx->score_impl == 2 && !use_tc && !dense_only)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
   const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;  // (direct: any)
   h_tiles[0] = 0;
@@ -343,7 +348,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     ctx->launches += 1;
     model->packed = true;
   }
-  if (!use_tc && !direct && !model->simt_ready) {
+  if (!use_tc && !direct && !dense_only && !model->simt_ready) {
     CK(gpbo::launch_simt_operands(model->meta_d, model->S, model->X32, model->ls32,
                                   model->Linv64, model->Xs32, model->LT32, ctx->stream));
     ctx->launches += 1;
@@ -384,7 +389,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.bound_scale = ctx->bound_scale >= 0.f ? ctx->bound_scale : 1.f;
   p.break_bracket = ctx->bound_scale < 0.f ? 1 : 0;
   const int tiles = h_tiles[S];
-  ctx->last_impl = direct ? 4 : use_tcs ? 3 : use_tc ? 2 : 1;
+  ctx->last_impl = direct ? 4 : dense_only ? 5 : use_tcs ? 3 : use_tc ? 2 : 1;
   const int64_t floats_all = xo;
   // element offset in X* of the first row of tile t (tile indices of this call)
   auto tile_elem = [&](int t) -> int64_t {
@@ -435,7 +440,7 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     if (st) return st;
     p.mean64 = ctx->mean_d;
   }
-  for (int c = 0; c < nchunk; ++c) {
+  for (int c = 0; c < nchunk && !dense_only; ++c) {
     const int ta = (int)((int64_t)tiles * c / nchunk), tb = (int)((int64_t)tiles * (c + 1) / nchunk);
     if (nchunk > 1) {
       // chunk c's rows: from its first tile's row to the next chunk's (the last chunk: to the end)

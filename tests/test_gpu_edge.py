@@ -92,3 +92,4 @@ def test_nan_rows_on_direct_path(G, impl):
         m.free()
     finally:
         ctx.set_score_impl(0)
+

@@ -128,16 +128,16 @@ def test_posterior_matches_oracle(G, name, make, impl):
             # the implementation that ran: forced stream, or auto -> streamed tcgen05 whenever
             # the resident image cannot hold the search (n16 > 256 or large d); d + 2 > 64 is
             # outside both tcgen05 envelopes (CUDA-core kernel)
+            # (gp_posterior: the float64 direct kernel for small problems, else the float64
+            # dense refine of every row -- implementation 5, no fast phase)
             n, d = w.searches[s].X.shape
             n16 = (n + 15) // 16 * 16
-            if d + 2 <= 64 and (impl == 3 or (impl == 0 and n16 > 256)):
-                assert ctx.last_impl == 3, (name, ctx.last_impl)
-            elif impl == 1:
-                assert ctx.last_impl == 1
-            elif impl == 4 and n <= 64:
+            if impl == 4 and n <= 64:
                 assert ctx.last_impl == 4
             elif impl == 0 and n <= 64 and w.Xstar[s].shape[0] * n16 * n16 <= 1 << 24:
                 assert ctx.last_impl == 4, (name, ctx.last_impl)
+            else:
+                assert ctx.last_impl == 5, (name, ctx.last_impl)
     finally:
         ctx.set_score_impl(0)
 
