@@ -434,7 +434,8 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     need_mean = need_mean || model->meta_pending || q.mean_tier;
     dmax_raw = std::max(dmax_raw, q.d);
   }
-  need_mean = need_mean && mode != gpbo::kModePosterior;
+  static const bool no_tier = getenv("GPBO_NO_MEAN_TIER") != nullptr;  // diagnosis only
+  need_mean = need_mean && mode != gpbo::kModePosterior && !no_tier;
   if (need_mean) {
     st = ensure_mean(ctx, (size_t)rows);
     if (st) return st;
@@ -909,6 +910,9 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
     // search as the SMs allow (~148 / S), and enough that the distributed working matrix fits in
     // their shared memory; GPBO_FIT=single selects the one-CTA kernel (fit.cu) for A/B runs
     const int Cc = fit_cluster_size(ctx, S, m->nmax);
+    // (packing the scoring image in the one-CTA fit's tail, io.img, measured 52 us slower than
+    // the 64-CTA pack kernel's 15 us at n = 200: one SM converting 129 KB; kept off)
+    io.img = nullptr;
     if (Cc > 0)
       CKM(gpbo::launch_fit_cluster(meta_in, S, Cc, gpbo::fit_cluster_smem(m->nmax, Cc), io,
                                    m->meta_d, ctx->stream));

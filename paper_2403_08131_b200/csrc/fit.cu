@@ -31,6 +31,7 @@
 #include <cstdio>
 
 #include "gpbo_internal.cuh"
+#include "score_pack.cuh"
 
 namespace gpbo {
 namespace {
@@ -634,6 +635,14 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     m.lml = -0.5 * ww - ld - 0.5 * n * 1.8378770664093454836;
     m.mean_tier = (double)m.sf2 * l1 > kMeanTierL1 ? 1 : 0;
     meta_out[s] = m;
+  }
+  // the tcgen05 operand image while L^-1, alpha and x / l are hot (saves the pack launch; small
+  // problems, n <= kDirectMaxN, are scored by the float64 direct kernel and need no image)
+  if (io.img != nullptr && n > kDirectMaxN && kSmem) {
+    __syncthreads();  // meta_out[s], L^-1 (row-major) and alpha written by this block
+    const SearchMeta mf = meta_out[s];
+    pack_body(meta_out + s, mf, io.Linv64, io.Xs64, io.alpha64, io.ls32, io.img, tid, kFitThreads,
+              true, sm, sm + 4);  // (the working matrix's space is free now)
   }
 }
 

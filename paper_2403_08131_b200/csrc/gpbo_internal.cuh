@@ -160,6 +160,8 @@ struct FitIO {
   double *y64, *L64, *Linv64, *Xs64, *alpha64, *Wscr64;
   double *Kt64;                  // the Gram pre-pass output (tile-packed, no noise / jitter)
   double *pm_part;               // [16 S] per-CTA max |x / l|^2 of the pre-pass
+  unsigned char *img;            // non-NULL: the one-CTA fit packs the tcgen05 operand image of
+                                 // searches with n > kDirectMaxN in its tail (score_pack.cuh)
 };
 // Gram pre-pass on many CTAs (fit.cu): x / l (Xs64) then the kernel matrix tiles (Kt64).
 cudaError_t launch_gram(const SearchMeta *meta_d, int S, int nmax, int dmax, const FitIO &io,

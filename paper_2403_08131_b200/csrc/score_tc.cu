@@ -40,6 +40,7 @@
 #include "score_tc.cuh"
 #include "tc_prims.cuh"
 #include "score_tc_helpers.cuh"
+#include "score_pack.cuh"
 
 namespace gpbo {
 
@@ -73,26 +74,6 @@ enum {
 };
 
 enum : uint32_t { kFlagInvalid = 1u, kFlagUnsafe = 2u };
-
-struct TcGeom {
-  int n16, kb, npan, off_l, off_a, off_w, img;
-};
-
-__host__ __device__ inline int align1k(int v) { return (v + 1023) & ~1023; }
-
-__host__ __device__ inline TcGeom tc_geom(int n, int d) {
-  TcGeom g;
-  g.n16 = (n + 15) & ~15;
-  g.kb = (d + 2 + 15) / 16;
-  g.npan = (g.n16 + 31) / 32;
-  int lrows = 0;
-  for (int p = 0; p < g.npan; ++p) lrows += g.n16 - 32 * p;
-  g.off_l = align1k(g.kb * 2 * g.n16 * 32);
-  g.off_a = align1k(g.off_l + lrows * 128);
-  g.off_w = g.off_a + g.n16 * 8;
-  g.img = align1k(g.off_w + GPBO_MAX_D * 4);
-  return g;
-}
 
 // dynamic shared memory: image | A tiles x2 | staging x2 | row info x4 | partials x2
 struct TcSmem {
@@ -642,142 +623,17 @@ __device__ double block_max_d(double v, double *red) {
   return r;
 }
 
-// One CTA per search.  Scales (powers of two, exact): x^ = g x/l 2^-e with g = sqrt5 (Matern)
-// or 1/sqrt2 (RBF) and e chosen so max(|x^*|^2 over the unit box, |x^_j|^2) <= 2^13;
-// K* 2^tK <= 2^13; L^-1 2^uL <= 2^14.  V = L^-1 K* then carries 2^(tK + uL).
+// One CTA per search (several for one search: gridDim.y chunks share every loop), the body in
+// score_pack.cuh (also run by the one-CTA fit kernel's tail, fit.cu).
 __global__ void __launch_bounds__(256)
 pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const double *alpha64,
                const float *ls32, unsigned char *img_all) {
   __shared__ double sc[4];
-  __shared__ double il2[GPBO_MAX_D];  // 1 / l_c^2, loaded by all threads at once
-  const int s = blockIdx.x;
+  __shared__ double il2[GPBO_MAX_D];
   asm volatile("griddepcontrol.launch_dependents;");  // the scoring kernel may start its setup
-  const int nch = gridDim.y, ch = blockIdx.y;  // blocks of one search split every loop below
-  SearchMeta m = meta[s];
-  if (!m.tc_ok || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) return;
-  const int n = m.n, d = m.d;
-  const TcGeom g = tc_geom(n, d);
-  const TcsGeom gs = tcs_geom(n, d);
-  const bool stream = m.tc_stream != 0;
-  unsigned char *img = img_all + m.img_off;
-  const double *Li = Linv64 + m.mat_off;
-  const double *X = Xs64 + m.x_off;
-  const double gk = m.kernel == GPBO_RBF ? 0.70710678118654752440 : 2.2360679774997896964;
-  const double lmax = m.linv_absmax;
-  const int t0 = ch * blockDim.x + threadIdx.x, tstep = nch * blockDim.x;
-  // the lengthscale loads in parallel (thread 0 alone made d dependent global round trips)
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    const double l = (double)ls32[m.ls_off + c];
-    il2[c] = 1.0 / (l * l);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double qbox = 0.0;
-    for (int c = 0; c < d; ++c) qbox += il2[c];
-    const double Qm = fmax(gk * gk * qbox, gk * gk * (double)m.pmax);
-    const int e = (int)ceil(0.5 * log2(fmax(Qm, 1e-30) / 8192.0));
-    const int tK = (int)floor(log2(8192.0 / (double)m.sf2));
-    const int uL = (int)floor(log2(16384.0 / fmax(lmax, 1e-300)));
-    sc[0] = ldexp(gk, -e);   // x^ = x/l * sc0
-    sc[1] = (double)e;
-    sc[2] = (double)tK;
-    sc[3] = (double)uL;
-    const double sf2 = m.sf2;
-    const double log2e = 1.4426950408889634074;
-    const double c0 = ldexp(sf2, tK);
-    if (m.kernel == GPBO_RBF) {
-      m.c0 = (float)log2(c0);
-      m.c1 = (float)(-ldexp(1.0, 2 * e) * log2e);
-      m.c2 = m.c3 = 0.f;
-    } else {
-      m.c0 = (float)c0;
-      m.c1 = (float)(-ldexp(1.0, e) * log2e);
-      m.c2 = (float)ldexp(c0, e);
-      m.c3 = (float)(ldexp(c0, 2 * e) / 3.0);
-    }
-    m.hscale = (float)ldexp(1.0, 2 * e);
-    m.vunscale2 = (float)ldexp(1.0, -2 * (tK + uL));
-    m.pmax_h = (float)(gk * gk * (double)m.pmax);
-    if (ch == 0) meta[s] = m;
-  }
-  __syncthreads();
-  const double xs = sc[0];
-  const int e = (int)sc[1], tK = (int)sc[2], uL = (int)sc[3];
-  auto put = [&](unsigned char *base_hi, unsigned char *base_lo, uint32_t off, double v) {
-    const __half hi = __double2half(v);
-    const __half lo = __double2half(v - (double)__half2float(hi));
-    *reinterpret_cast<__half *>(base_hi + off) = hi;
-    *reinterpret_cast<__half *>(base_lo + off) = lo;
-  };
-  // augmented training operand [-2 x^_j, 1, |x^_j|^2], K blocks of 16, rows n16
-  for (int idx = t0; idx < g.n16 * g.kb * 16; idx += tstep) {
-    const int j = idx / (g.kb * 16), k = idx % (g.kb * 16);
-    double v = 0.0;
-    if (j < n) {
-      if (k < d) v = -2.0 * xs * X[(size_t)k * n + j];
-      else if (k == d) v = 1.0;
-      else if (k == d + 1) {
-        double pj = 0.0;
-        for (int c = 0; c < d; ++c) pj += (xs * X[(size_t)c * n + j]) * (xs * X[(size_t)c * n + j]);
-        v = pj;
-      }
-    }
-    const int kblk = k >> 4;
-    if (stream) {  // chunk-major: chunk q, K block, hi / lo blocks of 64 rows x 32 B
-      unsigned char *hi = img + (((j >> 6) * g.kb + kblk) * 2) * 2048;
-      put(hi, hi + 2048, tc::sw_offset(j & 63, (k & 15) * 2, 32), v);
-    } else {
-      unsigned char *hi = img + kblk * 2 * g.n16 * 32;
-      put(hi, hi + g.n16 * 32, tc::sw_offset(j, (k & 15) * 2, 32), v);
-    }
-  }
-  if (stream) {
-    // L^-1 slabs in the streamed kernel's consumption order (score_tc.cuh)
-    int off = gs.off_l;
-    for (int w = 0; w < gs.nw; ++w) {
-      for (int pp = 0; pp < tcs_window_panels(gs.n16, w); ++pp) {
-        const int R = tcs_slab_rows(gs.n16, w, pp);
-        const int r0 = tcs_window_end(gs.n16, w) - R;
-        unsigned char *hi = img + off;
-        for (int idx = t0; idx < R * 32; idx += tstep) {
-          const int r = idx >> 5, k = idx & 31;
-          const int j = r0 + r, kk = 32 * pp + k;
-          const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
-          put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
-        }
-        off += R * 128;
-      }
-    }
-    float2 *ap = reinterpret_cast<float2 *>(img + gs.off_a);
-    for (int j = t0; j < gs.n16; j += tstep) {
-      const double a = j < n ? alpha64[m.a_off + j] : 0.0;
-      ap[j] = make_float2((float)ldexp(a, -tK), (float)ldexp(fabs(a), -tK));
-    }
-    float *wp = reinterpret_cast<float *>(img + gs.off_w);
-    for (int c = t0; c < GPBO_MAX_D; c += tstep)
-      wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
-    return;
-  }
-  // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32)
-  for (int pp = 0; pp < g.npan; ++pp) {
-    const int R = g.n16 - 32 * pp;
-    unsigned char *hi = img + g.off_l + (pp * g.n16 - 16 * pp * (pp - 1)) * 128;
-    for (int idx = t0; idx < R * 32; idx += tstep) {
-      const int r = idx >> 5, k = idx & 31;
-      const int j = 32 * pp + r, kk = 32 * pp + k;
-      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
-      put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
-    }
-  }
-  float2 *ap = reinterpret_cast<float2 *>(img + g.off_a);
-  for (int j = t0; j < g.n16; j += tstep) {
-    const double a = j < n ? alpha64[m.a_off + j] : 0.0;
-    ap[j] = make_float2((float)ldexp(a, -tK), (float)ldexp(fabs(a), -tK));
-  }
-  float *wp = reinterpret_cast<float *>(img + g.off_w);
-  for (int c = t0; c < GPBO_MAX_D; c += tstep)
-    wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
-  (void)e;
+  pack_body(meta + blockIdx.x, meta[blockIdx.x], Linv64, Xs64, alpha64, ls32, img_all,
+            blockIdx.y * blockDim.x + threadIdx.x, gridDim.y * blockDim.x, blockIdx.y == 0, sc,
+            il2);
 }
 
 }  // namespace
