@@ -356,6 +356,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
             Lg[(size_t)(J + u) * n + i] = d0;
             Lg[(size_t)(J + u + 1) * n + i] = d1;
           }
+          __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
           *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
         } else {
           const int C = it - nrt;
@@ -369,6 +370,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
           const int kc = 8 * C + 2 * tig;
           Gc[gid * gs + kc] = d0;
           Gc[gid * gs + kc + 1] = d1;
+          __syncwarp();
           *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
         }
       }

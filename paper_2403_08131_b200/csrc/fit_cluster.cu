@@ -356,6 +356,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       diag_block(0);
       broadcast_maps();
     }
+    __syncthreads();  // (the mbarrier already orders the maps; explicit for the race checker)
     FCT(1);
     wait_maps(0);
     FCT(2);
@@ -382,7 +383,9 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
             }
             GT[i * 9 + 2 * tig] = d0;      // (the L panel goes to global memory in T)
             GT[i * 9 + 2 * tig + 1] = d1;
-            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
+            __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
+            __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
+          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
           } else {
             const int C = it - nrows;
             double *Wt = at(JT, C);
@@ -395,7 +398,9 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
             const int kc = 8 * C + 2 * tig;
             GT[kc * 9 + gid] = d0;
             GT[(kc + 1) * 9 + gid] = d1;
-            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
+            __syncwarp();
+            __syncwarp();
+          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
           }
         }
       }
