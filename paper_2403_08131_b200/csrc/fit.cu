@@ -84,13 +84,7 @@ struct MinOp { __device__ double operator()(double a, double b) const { return f
 // pivot is flagged by the caller and its values discarded).
 __device__ __forceinline__ double rsqrt_fast(double p) {
   double y;
-  if (p > 1e-30 && p < 1e30) {  // the float32 MUFU seed is shorter on the D chain
-    float yf;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"((float)p));
-    y = (double)yf;
-  } else {
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
-  }
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const double e = fma(-p, y * y, 1.0);
@@ -222,49 +216,51 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   auto diag_block = [&](int J) {
     const int bb = min(kFitB, n - J);
     double *Wd = W + tb(J >> 3, J >> 3);
-    {  // warp-parallel elimination [A | I] -> [L^T | L^-1] of the 8 x 8 block (as fit_cluster.cu:
-       // lane l holds row l / 4, columns 4 (l % 4) .. + 3 of the 8 x 16 array; one pivot and one
-       // row broadcast by shuffles per step -- the former one-lane version was ~3x longer)
-      const int i = lane >> 2, cb = 4 * (lane & 3);
-      double v[4];
+    if (lane == 0) {
+      double a[36];  // packed lower, row-major: (i, k) at i (i + 1) / 2 + k
+      double rr[8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = cb + e;
-        if (col < 8)
-          v[e] = (i < bb && col < bb) ? (col <= i ? Wd[8 * i + col] : Wd[8 * col + i])
-                                      : (i == col ? 1.0 : 0.0);
-        else
-          v[e] = col - 8 == i ? 1.0 : 0.0;
-      }
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k <= i; ++k)
+          a[i * (i + 1) / 2 + k] = i < bb ? Wd[8 * i + k] : (i == k ? 1.0 : 0.0);
       bool fail = false;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double pj = __shfl_sync(0xffffffffu, v[j & 3], 4 * j + (j >> 2));
-        fail |= !(pj > 0.0) || !isfinite(pj);
-        const double r = rsqrt_fast(pj);
-        const double bij = __shfl_sync(0xffffffffu, v[j & 3], 4 * i + (j >> 2));
-        double rj[4];
+      for (int j = 0; j < 8; ++j) {  // right-looking Cholesky
+        const double p = a[j * (j + 1) / 2 + j];
+        fail |= !(p > 0.0) || !isfinite(p);
+        const double r = rsqrt_fast(p);
+        rr[j] = r;
+        a[j * (j + 1) / 2 + j] = p * r;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) rj[e] = __shfl_sync(0xffffffffu, v[e], 4 * j + (lane & 3));
-        if (i > j) {
-          const double f = bij * r * r;  // B[i][j] / p
+        for (int i = j + 1; i < 8; ++i) a[i * (i + 1) / 2 + j] *= r;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) v[e] = fma(-f, rj[e], v[e]);
-        } else if (i == j) {
+        for (int i = j + 1; i < 8; ++i)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) v[e] *= r;
+          for (int k = j + 1; k <= i; ++k)
+            a[i * (i + 1) / 2 + k] = fma(-a[i * (i + 1) / 2 + j], a[k * (k + 1) / 2 + j],
+                                         a[i * (i + 1) / 2 + k]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)  // L11 -> Nm (scratch until the maps are formed)
+#pragma unroll
+        for (int k = 0; k <= i; ++k) Nm[8 * i + k] = a[i * (i + 1) / 2 + k];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // X = L^-1 in place: X_ij = -r_i sum_{k=j}^{i-1} L_ik X_kj
+        a[j * (j + 1) / 2 + j] = rr[j];
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = j; k < i; ++k) t = fma(a[i * (i + 1) / 2 + k], a[k * (k + 1) / 2 + j], t);
+          a[i * (i + 1) / 2 + j] = -rr[i] * t;
         }
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = cb + e;
-        if (col < 8) {
-          if (col >= i) Nm[8 * col + i] = v[e];  // L11[col][i] = B[i][col]
-        } else {
-          Rm[8 * i + col - 8] = col - 8 <= i ? v[e] : 0.0;  // X[i][col - 8]
-        }
-      }
-      if (lane == 0) piv[16] = fail ? 1.0 : 0.0;
+      for (int i = 0; i < 8; ++i)  // X -> Rm (lower part)
+#pragma unroll
+        for (int k = 0; k <= i; ++k) Rm[8 * i + k] = a[i * (i + 1) / 2 + k];
+      piv[16] = fail ? 1.0 : 0.0;
     }
     __syncwarp();
     // the warp spreads the outputs: L11 to L64, X to the diagonal tile, R = X, N = X^T
