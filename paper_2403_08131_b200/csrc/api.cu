@@ -496,7 +496,10 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   }
   {
     KernTimer t(ctx, kKernRefine);
-    CK(gpbo::launch_refine(r, rows, ctx->num_sms, nmax, ctx->stream));
+    if (dense_only)  // gp_posterior: every row in float64, candidate-tiled
+      CK(gpbo::launch_posterior64(r, nmax, dmax_raw, ctx->num_sms, ctx->stream));
+    else
+      CK(gpbo::launch_refine(r, rows, ctx->num_sms, nmax, ctx->stream));
   }
   ctx->launches += 1;
   return GPBO_OK;

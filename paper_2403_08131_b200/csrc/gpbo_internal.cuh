@@ -204,6 +204,9 @@ cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, in
                           cudaStream_t stream);
 void mean64_exp_table(double *host);
 int mean64_exp_table_size();
+// gp_posterior's dense float64 path, candidate-tiled (refine.cu).
+cudaError_t launch_posterior64(const RefineLaunch &p, int nmax, int dmax, int num_sms,
+                               cudaStream_t stream);
 // Small problems: float64 scoring of every row, thread per candidate (refine.cu); n <= 64.
 constexpr int kDirectMaxN = 64;
 cudaError_t launch_direct(const RefineLaunch &p, int S, int64_t rows, cudaStream_t stream);

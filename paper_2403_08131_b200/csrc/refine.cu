@@ -369,7 +369,107 @@ direct_kernel(const RefineLaunch p, int S, int64_t rows) {
   }
 }
 
+// gp_posterior's dense path: every row of search dense_s in float64 (the refine's arithmetic:
+// direct differences of x / l, the float64 kernel, mu~ = k*^T alpha, v = L^-1 k*, tau), but
+// candidate-TILED: a CTA scores kPostTile candidates together, so each row of L^-1 is read once
+// per tile (a broadcast load shared by the tile's lanes) instead of once per candidate -- the
+// per-candidate refine streams n^2 / 2 float64 per candidate from L2 (56x the argmax path's time
+// at config 2).  Thread (c, g): candidate c of the tile, rows j = g (mod groups) of v.
+constexpr int kPostTile = 32;
+
+// groups per tile = blockDim.x / 32 (8, 16 or 32: more row groups for larger n)
+__global__ void __launch_bounds__(1024)
+posterior64_kernel(const RefineLaunch p, int nmax, int dmax) {
+  const int kPostGroups = blockDim.x / kPostTile;
+  extern __shared__ __align__(16) double psm[];
+  double *ks = psm;                                  // [n][kPostTile]  k*(c, j) at j * 32 + c
+  double *xs = ks + (size_t)nmax * kPostTile;        // [kPostTile][dmax] x* / l
+  double *red = xs + (size_t)kPostTile * dmax;       // [kPostGroups][kPostTile] x 2
+  const int tid = threadIdx.x, c = tid % kPostTile, g = tid / kPostTile;
+  const int s = p.dense_s;
+  const SearchMeta &m = p.meta[s];
+  const int n = m.n, d = m.d;
+  const double *Xj = p.Xs64 + m.x_off;      // column-major d x n
+  const double *alpha = p.alpha64 + m.a_off;
+  const double *Li = p.Linv64 + m.mat_off;  // row-major, lower part
+  const float *ls = p.ls32 + m.ls_off;
+  const double sf2 = (double)m.sf2;
+  const int64_t ntile = (p.dense_rows + kPostTile - 1) / kPostTile;
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t row0 = t * kPostTile;
+    const int cnt = (int)min((int64_t)kPostTile, p.dense_rows - row0);
+    __syncthreads();  // the previous tile is done with ks / xs / red
+    for (int e = tid; e < kPostTile * d; e += blockDim.x) {
+      const int cc = e / d, dim = e - cc * d;
+      xs[cc * dmax + dim] =
+          cc < cnt ? (double)p.Xstar[p.x_off[s] + (row0 + cc) * d + dim] / (double)ls[dim] : 0.0;
+    }
+    __syncthreads();
+    double mu = 0.0;
+    for (int j = g; j < n; j += kPostGroups) {  // k* and the mean partials
+      double r2 = 0.0;
+      for (int dim = 0; dim < d; ++dim) {
+        const double t2 = xs[c * dmax + dim] - Xj[(size_t)dim * n + j];
+        r2 = fma(t2, t2, r2);
+      }
+      const double k = kernel64(r2, sf2, m.kernel);
+      ks[j * kPostTile + c] = k;
+      mu = fma(k, alpha[j], mu);
+    }
+    __syncthreads();  // ks complete
+    double vv = 0.0;
+    for (int j = g; j < n; j += kPostGroups) {  // v_j = sum_{k <= j} L^-1_jk k*_k
+      const double *row = Li + (size_t)j * n;
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 1 <= j; k += 2) {
+        a0 = fma(row[k], ks[k * kPostTile + c], a0);
+        a1 = fma(row[k + 1], ks[(k + 1) * kPostTile + c], a1);
+      }
+      if (k == j) a0 = fma(row[k], ks[k * kPostTile + c], a0);
+      const double v = a0 + a1;
+      vv = fma(v, v, vv);
+    }
+    red[g * kPostTile + c] = mu;
+    red[(kPostGroups + g) * kPostTile + c] = vv;
+    __syncthreads();
+    if (g == 0 && c < cnt) {
+      double mu_s = 0.0, vv_s = 0.0;
+      for (int q = 0; q < kPostGroups; ++q) {  // fixed order: deterministic
+        mu_s += red[q * kPostTile + c];
+        vv_s += red[(kPostGroups + q) * kPostTile + c];
+      }
+      const int64_t e = row0 + c;
+      const bool fin = isfinite(mu_s) && isfinite(vv_s);  // NaN rows: NaN outputs
+      const double var64 = fmax(sf2 - vv_s, 0.0);
+      const double sig = sqrt(var64);
+      const double imp = resolve_best(p.best[s], m) - mu_s;
+      const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
+      if (p.out_mu) p.out_mu[e] = fin ? (float)(m.mean + m.std * mu_s) : NAN;
+      if (p.out_var) p.out_var[e] = fin ? (float)(m.std * m.std * var64) : NAN;
+      if (p.out_ei) p.out_ei[e] = fin ? (float)(m.std * ei) : NAN;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_posterior64(const RefineLaunch &p, int nmax, int dmax, int num_sms,
+                               cudaStream_t stream) {
+  if (p.dense_rows <= 0) return cudaSuccess;
+  const int groups = nmax <= 128 ? 8 : nmax <= 256 ? 16 : 32;
+  const size_t smem = ((size_t)nmax * kPostTile + (size_t)kPostTile * dmax +
+                       2 * groups * kPostTile) * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(posterior64_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t tiles = (p.dense_rows + kPostTile - 1) / kPostTile;
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms * 8);
+  posterior64_kernel<<<grid, kPostTile * groups, smem, stream>>>(p, nmax, dmax);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms, int nmax,
                           cudaStream_t stream) {
