@@ -644,7 +644,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     __syncthreads();  // meta_out[s], L^-1 (row-major) and alpha written by this block
     const SearchMeta mf = meta_out[s];
     pack_body(meta_out + s, mf, io.Linv64, io.Xs64, io.alpha64, io.ls32, io.img, tid, kFitThreads,
-              true, sm, sm + 4);  // (the working matrix's space is free now)
+              true, sm, sm + 8);  // (the working matrix's space is free now)
   }
 }
 

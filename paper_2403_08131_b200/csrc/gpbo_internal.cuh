@@ -64,6 +64,7 @@ struct SearchMeta {
   float c0, c1, c2, c3; // kernel-value constants in the scaled MMA units (see pack_tc)
   float hscale;         // true h = MMA h * hscale
   float vunscale2;      // |v|^2 = sum of squared V accumulator * vunscale2
+  float munscale;       // mu~ = (V[n16] + V[n16 + 2] 2^-11) * munscale (mean rows of the image)
   float pmax_h;         // max_j p^_j in true h units (error-bound input)
   double jitter;
   int32_t jitter_k;

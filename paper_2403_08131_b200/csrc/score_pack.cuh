@@ -10,6 +10,13 @@
 
 namespace gpbo {
 
+// B rows appended to every resident L^-1 panel (score_tc.cu): row n16 = alpha hi, n16 + 1 =
+// |alpha| hi (both in the hi image only), n16 + 2 = alpha lo 2^11 (lo image only), rest zero, so
+// the fp16x3 variance MMA also accumulates V[n16] = K* alpha_hi, V[n16 + 1] = K* |alpha| and
+// V[n16 + 2] = K*_hi alpha_lo 2^11 (the mean of north star (b) "mu = K* alpha" on the tensor
+// cores instead of FMAs in the K* epilogue).
+constexpr int kMeanRows = 16;
+
 struct TcGeom {
   int n16, kb, npan, off_l, off_a, off_w, img;
 };
@@ -21,8 +28,10 @@ __host__ __device__ inline TcGeom tc_geom(int n, int d) {
   g.n16 = (n + 15) & ~15;
   g.kb = (d + 2 + 15) / 16;
   g.npan = (g.n16 + 31) / 32;
+  // each 32-wide L^-1 panel carries 16 extra B rows after its n16 - 32 p rows: the mean rows
+  // (see pack_body) that make the variance MMA also accumulate mu~ and sum K* |alpha|
   int lrows = 0;
-  for (int p = 0; p < g.npan; ++p) lrows += g.n16 - 32 * p;
+  for (int p = 0; p < g.npan; ++p) lrows += g.n16 + kMeanRows - 32 * p;
   g.off_l = align1k(g.kb * 2 * g.n16 * 32);
   g.off_a = align1k(g.off_l + lrows * 128);
   g.off_w = g.off_a + g.n16 * 8;
@@ -36,7 +45,7 @@ __host__ __device__ inline TcGeom tc_geom(int n, int d) {
 // K* 2^tK <= 2^13; L^-1 2^uL <= 2^14.  V = L^-1 K* then carries 2^(tK + uL).
 // meta_s: the search's meta record (global; the tcgen05 constants are written back by the block
 // with write_meta), m: its current value; threads t0 = 0.. of stride tstep share every loop (all
-// threads of the block must call: block barriers inside); sc[4], il2[GPBO_MAX_D]: shared scratch.
+// threads of the block must call: block barriers inside); sc[5], il2[GPBO_MAX_D]: shared scratch.
 __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, const double *Linv64,
                                           const double *Xs64, const double *alpha64,
                                           const float *ls32, unsigned char *img_all, int t0,
@@ -83,6 +92,12 @@ __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, cons
     }
     m.hscale = (float)ldexp(1.0, 2 * e);
     m.vunscale2 = (float)ldexp(1.0, -2 * (tK + uL));
+    // mean rows: alpha 2^uA with max |alpha| 2^uA <= 2^14 (clamped so 2^-(tK + uA) is a normal
+    // float); V[n16] then carries 2^(tK + uA)
+    int uA = (int)floor(log2(16384.0 / fmax((double)m.alpha_max, 1e-300)));
+    uA = max(-100 - tK, min(100 - tK, uA));
+    sc[4] = (double)uA;
+    m.munscale = (float)ldexp(1.0, -(tK + uA));
     m.pmax_h = (float)(gk * gk * (double)m.pmax);
     if (write_meta) *meta_s = m;
   }
@@ -144,15 +159,30 @@ __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, cons
       wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
     return;
   }
-  // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32)
+  // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32), then the kMeanRows
+  // mean rows (j = n16 + t)
+  const int uA = (int)sc[4];
   for (int pp = 0; pp < g.npan; ++pp) {
-    const int R = g.n16 - 32 * pp;
-    unsigned char *hi = img + g.off_l + (pp * g.n16 - 16 * pp * (pp - 1)) * 128;
+    const int R = g.n16 + kMeanRows - 32 * pp;
+    unsigned char *hi = img + g.off_l + (pp * (g.n16 + kMeanRows) - 16 * pp * (pp - 1)) * 128;
     for (int idx = t0; idx < R * 32; idx += tstep) {
       const int r = idx >> 5, k = idx & 31;
       const int j = 32 * pp + r, kk = 32 * pp + k;
-      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
-      put(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), v);
+      const uint32_t off = tc::sw_offset(r, k * 2, 64);
+      if (j < g.n16) {
+        const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
+        put(hi, hi + R * 64, off, v);
+      } else {
+        const int t = j - g.n16;
+        const double a = kk < n ? ldexp(alpha64[m.a_off + kk], uA) : 0.0;
+        const __half ah = __double2half(a);
+        __half vh = __double2half(0.0), vl = __double2half(0.0);
+        if (t == 0) vh = ah;
+        else if (t == 1) vh = __double2half(fabs(a));
+        else if (t == 2) vl = __double2half(ldexp(a - (double)__half2float(ah), 11));
+        *reinterpret_cast<__half *>(hi + off) = vh;
+        *reinterpret_cast<__half *>(hi + R * 64 + off) = vl;
+      }
     }
   }
   float2 *ap = reinterpret_cast<float2 *>(img + g.off_a);

@@ -6,11 +6,13 @@
 //       the kernel argument: 5 r^2 for Matern-5/2, r^2/2 for RBF) -- the "GEMM-form squared
 //       distances on tensor cores" of the north star (a);
 //   (2) epilogue warps: tcgen05.ld the scratch, K* = k(h) (MUFU sqrt/ex2 + FMA polynomial),
-//       accumulate mu~ = K* alpha and sum |K* alpha| (mean error bound), split K* into
-//       float16 hi + lo and store the panel as the A operand of (3);
+//       split K* into float16 hi + lo and store the panel as the A operand of (3);
 //   (3) variance MMA  V[:, j >= 32p] += K*_p . (L^-1)[j, k in p]^T  into a TMEM accumulator of
-//       n16 columns: the triangular "panel TRSM" V = L^-1 K*^T of north star (c), with L^-1
-//       inverted at fit time; the k-step 16 of the panel only touches columns j >= 16 s.
+//       n16 + 16 columns: the triangular "panel TRSM" V = L^-1 K*^T of north star (c), with L^-1
+//       inverted at fit time; the k-step 16 of the panel only touches columns j >= 16 s.  The
+//       16 extra B rows of every panel (score_pack.cuh, kMeanRows) make the same MMAs accumulate
+//       mu~ = K* alpha and sum K* |alpha| (the mean error bound) in columns n16.. -- the mean of
+//       north star (b) on the tensor cores, not on the epilogue's FMA pipe.
 // After the last panel the epilogue drains V (sum V_j^2), forms s2~ = sf2 - |v|^2, EI and the
 // EI bracket, and flags the candidates that can still be the argmax for the float64 refine
 // phase (refine.cu) -- north star (d).
@@ -52,7 +54,7 @@ constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
 constexpr int kDepth = 2;           // 64-column distance scratch stages (TMEM), issued ahead
 constexpr int kKStages = 2;         // K* operand stages (TMEM), one 64-wide panel each
-// TMEM columns: V accumulator [0, n16 <= 256), distance scratch 2 x 64 [256, 384), K* operand
+// TMEM columns: V accumulator [0, n16 + 16 <= 256), distance scratch 2 x 64 [256, 384), K* operand
 // stages 2 x 64 [384, 512) (per stage: hi k-steps 0..3 at +0/+8/+16/+24, lo at +32..+56;
 // lane = row, one column packs the fp16 pair k = 2c, 2c+1).  A K* panel is 64 training points
 // wide (= one distance chunk): every TMEM round trip of the K* warps (distance load, K* store,
@@ -68,16 +70,15 @@ enum {
   B_KF0, B_KF1, B_KF2, B_KF3, B_KE0, B_KE1, B_KE2, B_KE3,  // K* panel stages
   B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
   B_SF0, B_SF1,                             // raw candidate rows landed in staging (TMA)
-  B_PF0, B_PF1, B_PE0, B_PE1,               // per-tile partial sums (mu, |mu| bound) K* -> drain
   B_VB0, B_VB1, B_VB2, B_VB3, B_VB4, B_VB5, B_VB6, B_VB7,  // V column block p final (per panel)
   B_IMG, B_COUNT
 };
 
 enum : uint32_t { kFlagInvalid = 1u, kFlagUnsafe = 2u };
 
-// dynamic shared memory: image | A tiles x2 | staging x2 | row info x4 | partials x2
+// dynamic shared memory: image | A tiles x2 | staging x2 | row info x8
 struct TcSmem {
-  int img, a, k, stage, rowinfo, part_mu, part_a1, bars, total;
+  int img, a, k, stage, rowinfo, bars, total;
 };
 
 __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
@@ -87,9 +88,7 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   s.k = s.a + 2 * kb_max * 8192;
   s.stage = s.k;
   s.rowinfo = s.stage + 2 * ((128 * d_max * 4 + 127) & ~127);
-  s.part_mu = s.rowinfo + 8 * 128 * 8;
-  s.part_a1 = s.part_mu + 4 * 128 * 8;
-  s.bars = s.part_a1 + 4 * 128 * 4;
+  s.bars = s.rowinfo + 8 * 128 * 8;
   s.total = s.bars + B_COUNT * 8 + 16 + 1024;  // + tmem slot, + alignment slack
   return s;
 }
@@ -104,8 +103,6 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   unsigned char *Abuf = sm + L.a;
   float *stage = reinterpret_cast<float *>(sm + L.stage);
   float2 *rowinfo = reinterpret_cast<float2 *>(sm + L.rowinfo);
-  double *part_mu = reinterpret_cast<double *>(sm + L.part_mu);
-  float *part_a1 = reinterpret_cast<float *>(sm + L.part_a1);
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L.bars);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + B_COUNT);
   auto bar = [&](int i) { return tc::smem_u32(bars + i); };
@@ -123,8 +120,6 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       tc::mbar_init(bar(B_VF0 + i), 1);
       tc::mbar_init(bar(B_VE0 + i), 4);
       tc::mbar_init(bar(B_SF0 + i), 1);
-      tc::mbar_init(bar(B_PF0 + i), 8);
-      tc::mbar_init(bar(B_PE0 + i), 4);
     }
     for (int i = 0; i < kDepth; ++i) {
       tc::mbar_init(bar(B_DF0 + i), 1);
@@ -171,10 +166,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     tc::mbar_wait(bar(B_IMG), img_phase);
     img_phase ^= 1u;
     const int n16 = m.n16, npan = m.npan, kb = m.kb;
-    // n16 <= 128: two V accumulators [0, 128) and [128, 256) alternate between tiles, so the
-    // next tile's variance MMAs never wait for the previous tile's drain; block barriers
+    // n16 + 16 <= 128: two V accumulators [0, 128) and [128, 256) alternate between tiles, so
+    // the next tile's variance MMAs never wait for the previous tile's drain; block barriers
     // B_VB0..3 / B_VB4..7 per buffer.  Otherwise one accumulator and 8 block barriers.
-    const bool dbl = n16 <= 128;
+    const int nv16 = n16 + kMeanRows;  // V accumulator columns (L^-1 rows + mean rows)
+    const bool dbl = nv16 <= 128;
     const uint32_t vbq = dbl ? 4u : 8u;
     const int T = tb - ta;
     const int P64 = (n16 + 63) / 64;  // 64-wide K* panels per tile
@@ -248,9 +244,9 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
             const int j0 = 64 * v_pp + 16 * sk;
             if (j0 < n16) {
               const int pp = 2 * v_pp + (sk >> 1), h = sk & 1;  // 32-wide L^-1 panel, its k step
-              const uint32_t R16 = (uint32_t)(n16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
-              const uint32_t lp = l0 + (uint32_t)(pp * n16 - 16 * pp * (pp - 1)) * 8u;
-              const uint32_t idn = tc::idesc_f16((uint32_t)(n16 - j0));
+              const uint32_t R16 = (uint32_t)(nv16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
+              const uint32_t lp = l0 + (uint32_t)(pp * nv16 - 16 * pp * (pp - 1)) * 8u;
+              const uint32_t idn = tc::idesc_f16((uint32_t)(nv16 - j0));
               const uint32_t dt = tbase + 128u * vb + (uint32_t)j0;
               const uint32_t ka = kt + 8u * sk;       // k step sk: hi at +8 sk, lo at +32 + 8 sk
               const uint32_t lb = lp + 66u * h;       // +1024 B rows, +32 B k-advance
@@ -386,6 +382,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       const FinishSeg fs = finish_seg(p, s);  // per-search values, once per segment
       const int64_t row0s = p.m_off[s];
       const float vun2 = m.vunscale2, sf2 = m.sf2, pmaxh = m.pmax_h, lrs = m.linv_rowsum;
+      const float mun = m.munscale;
+      // absolute floor of the MMA mean's error: K* entries below the float16 range of the lo
+      // part (|K*| 2^tK < 2^-14) are represented to 2^-25 2^-tK = 2^-38 sf2 (2^tK >= 2^12 / sf2),
+      // so |d mu~| <= 2^-38 sf2 |alpha|_1; 4x margin
+      const float dmu_abs = (float)((double)m.sf2 * m.alpha_l1 * 1.4551915228366852e-11);
       const int nn = m.n;
       const bool mtier = p.mean64 != nullptr && m.mean_tier;  // precise-mean tier (mean64.cu)
       // variance bound 4 var_bound(u, sf2, s2, n, lrs) = vbk (sf2 + s2), its factor hoisted
@@ -433,18 +434,19 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
             }
           }
         }
+        // the mean columns (final: the last block barrier above follows every MMA of the tile)
+        uint32_t rm[8];
+        tc::tmem_ld8(va + (uint32_t)n16, rm);
+        tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(bar(B_VE0 + vb));
         if (trd) trace_ev(p.trace, 17, 9, ti, trc);
         if (!dbl || vb == 0) ++vb0c;
         if (!dbl || vb == 1) ++vb1c;
-        const uint32_t par = ti & 1u;
-        tc::mbar_wait(bar(B_PF0 + par), (ti >> 1) & 1u);
-        double mu_t = part_mu[par * 128 + row] + part_mu[(2 + par) * 128 + row];
-        const float a1_t = part_a1[par * 128 + row] + part_a1[(2 + par) * 128 + row];
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_PE0 + par));
+        double mu_t = ((double)__uint_as_float(rm[0]) +
+                       (double)__uint_as_float(rm[2]) * 4.8828125e-4) * (double)mun;
+        const float a1_t = __uint_as_float(rm[1]) * mun;
         if (trd) trace_ev(p.trace, 18, 9, ti, trc);
         const float2 ri = rowinfo[(ti & 7u) * 128 + row];
         const uint32_t flags = __float_as_uint(ri.y);
@@ -455,7 +457,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const float var = fmaxf(sf2 - s2, 0.f);
         // K* relative error <= (dlog k / dh) dh + eval error; dh <= ~8 2^-22 (q^ + p^) for
         // the float16x3 augmented GEMM; margin x4
-        float dmu = u * a1_t * (32.f * (ri.x + pmaxh) + 128.f) * p.bound_scale;
+        // (+64: the float32 accumulation of the mean in the variance MMA, ~39 roundings)
+        float dmu = (u * a1_t * (32.f * (ri.x + pmaxh) + 192.f) + dmu_abs) * p.bound_scale;
         if (mtier && rloc < Ms) {  // precise tier: the float64 mean (mean64.cu)
           mu_t = p.mean64[row0s + rloc];
           dmu = 1e-12f * a1_t * p.bound_scale;
@@ -476,16 +479,12 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       // of the squared distances, K* = k(h), the mean partials, the float16 hi/lo split, two
       // tcgen05.st (x16) into the K* stage (k steps 2 half, 2 half + 1).
       const int lq = warp & 3, half = warp >> 2;
-      const int row = 32 * lq + lane;
       const uint32_t tl_addr = tbase + ((uint32_t)(32 * lq) << 16);
-      const float2 *ap = reinterpret_cast<const float2 *>(img + m.off_a);
       const int kind = m.kernel;
       const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
       uint32_t gk = gk_seg;
       uint32_t ec = gc_seg;  // distance chunk counter (= panel counter)
-      double mu = 0.0;
-      float a1 = 0.f;
-      int tl = 0, pp = 0;
+      int pp = 0;
       for (int g = 0; g < P; ++g) {
         const uint32_t st = ec % kDepth;
         const int jb = 64 * pp + 32 * half;
@@ -524,7 +523,6 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         }
-        float muf = 0.f, a1f = 0.f;
         if (nv > 0) {
           float kv[32];
 #ifdef GPBO_EXP_NOKSTAR  // timing experiment only: no kernel evaluation (wrong results)
@@ -549,17 +547,6 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           if (nv < 32) {  // points beyond n16: scratch columns the distance MMA did not write
 #pragma unroll
             for (int q = 16; q < 32; ++q) kv[q] = 0.f;
-          }
-          const float4 *ap4 = reinterpret_cast<const float4 *>(ap + jb);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            if (q < 8 || nv == 32) {  // alpha pairs exist for j < n16 only
-              const float4 a = ap4[q];
-              muf = fmaf(kv[2 * q], a.x, muf);
-              a1f = fmaf(kv[2 * q], a.y, a1f);
-              muf = fmaf(kv[2 * q + 1], a.z, muf);
-              a1f = fmaf(kv[2 * q + 1], a.w, a1f);
-            }
           }
           uint32_t hw[16], lw[16];
 #pragma unroll
@@ -586,20 +573,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         }
         if (trw) trace_ev(p.trace, 8, warp, gk, trc);
         ++gk;
-        mu += (double)muf;
-        a1 += a1f;
-        if (++pp == P64) {  // tile complete: hand the partial sums to the drain warps
-          const uint32_t ti = gi + tl, par = ti & 1u;
-          tc::mbar_wait(bar(B_PE0 + par), ((ti >> 1) & 1u) ^ 1u);
-          part_mu[(2 * half + par) * 128 + row] = mu;
-          part_a1[(2 * half + par) * 128 + row] = a1;
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(bar(B_PF0 + par));
-          mu = 0.0;
-          a1 = 0.f;
-          pp = 0;
-          ++tl;
-        }
+        if (++pp == P64) pp = 0;
       }
     }
     gi += (uint32_t)T;
@@ -628,7 +602,7 @@ __device__ double block_max_d(double v, double *red) {
 __global__ void __launch_bounds__(256)
 pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const double *alpha64,
                const float *ls32, unsigned char *img_all) {
-  __shared__ double sc[4];
+  __shared__ double sc[5];
   __shared__ double il2[GPBO_MAX_D];
   asm volatile("griddepcontrol.launch_dependents;");  // the scoring kernel may start its setup
   pack_body(meta + blockIdx.x, meta[blockIdx.x], Linv64, Xs64, alpha64, ls32, img_all,
@@ -640,7 +614,7 @@ pack_tc_kernel(SearchMeta *meta, const double *Linv64, const double *Xs64, const
 
 static bool resident_fits(int n, int d) {
   const TcGeom g = tc_geom(n, d);
-  if (g.n16 > 256 || d + 2 > 64) return false;
+  if (g.n16 + kMeanRows > 256 || d + 2 > 64) return false;
   return tc_smem(g.img, g.kb, d).total <= kMaxSmem;
 }
 
@@ -701,9 +675,9 @@ cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int 
                             int tile_lo, int total_tiles, int num_sms,
                             cudaStream_t stream) {
   int img_max = 0, kb_max = 1, d_max = 1;
-  bool merged = true;  // every search double-buffers V (n16 <= 128)
+  bool merged = true;  // every search double-buffers V (n16 + 16 <= 128)
   for (int i = 0; i < S; ++i) {
-    merged = merged && meta_h[i].n16 <= 128;
+    merged = merged && meta_h[i].n16 + kMeanRows <= 128;
     img_max = std::max(img_max, meta_h[i].img_bytes);
     kb_max = std::max(kb_max, meta_h[i].kb);
     d_max = std::max(d_max, meta_h[i].d);
