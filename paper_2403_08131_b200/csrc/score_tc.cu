@@ -24,7 +24,7 @@
 // (SURVEY.md Appendix A).
 //
 // Warp roles (512 threads, one persistent CTA per SM, static contiguous tile ranges):
-//   warps 0-7   K* (2 warps per TMEM lane quarter, 16 columns of each panel each)
+//   warps 0-7   K* (2 warps per TMEM lane quarter, 32 training points of each panel each)
 //   warps 8-11  drain + finish of the previous tile (overlaps the K* work of the next one)
 //   warps 12-13 candidate loader (X* -> A_aug)
 //   warp 14     TMEM allocator, image TMA, distance MMA issuer
@@ -48,7 +48,21 @@ namespace gpbo {
 
 namespace {
 
-constexpr int kThreads = 512;
+// K* warps: 2 per sub-partition (8), each evaluating 32 of a panel's 64 training points;
+// -DGPBO_KWARPS=16 builds 4 per sub-partition x 16 points (measured: config 2 fast phase
+// 0.254 -> 0.275 ms -- the K* warps then wait on the MMA handoffs instead, and the 768-thread
+// block caps registers at 80; config 3 -2 %).
+#ifndef GPBO_KWARPS
+#define GPBO_KWARPS 8
+#endif
+constexpr int kKWarps = GPBO_KWARPS;
+static_assert(kKWarps == 8 || kKWarps == 16, "K* warps: 2 or 4 per TMEM lane quarter");
+constexpr int kCW = 256 / kKWarps;           // training points per K* warp and panel (32 / 16)
+constexpr int kDrainW0 = kKWarps;            // drain + finish warps kDrainW0 .. + 3
+constexpr int kLoadW0 = kKWarps + 4;         // candidate loader warps kLoadW0, + 1
+constexpr int kDistW = kKWarps + 6;          // TMEM allocator, image TMA, distance MMA issuer
+constexpr int kVarW = kKWarps + 7;           // variance MMA issuer (highest warp id)
+constexpr int kThreads = 32 * (kKWarps + 8);
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageBytes = 16384;  // one K* panel stage: hi (128 x 64 B) + lo (128 x 64 B)
@@ -70,7 +84,7 @@ enum {
   B_KF0, B_KF1, B_KF2, B_KF3, B_KE0, B_KE1, B_KE2, B_KE3,  // K* panel stages
   B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
   B_SF0, B_SF1,                             // raw candidate rows landed in staging (TMA)
-  B_VB0, B_VB1, B_VB2, B_VB3, B_VB4, B_VB5, B_VB6, B_VB7,  // V column block p final (per panel)
+  B_VB0, B_VB1, B_VB2, B_VB3,               // V column block [64 p, 64 p + 64) final (per panel)
   B_IMG, B_COUNT
 };
 
@@ -123,17 +137,17 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     }
     for (int i = 0; i < kDepth; ++i) {
       tc::mbar_init(bar(B_DF0 + i), 1);
-      tc::mbar_init(bar(B_DE0 + i), 8);
+      tc::mbar_init(bar(B_DE0 + i), kKWarps);
     }
     for (int i = 0; i < kKStages; ++i) {
-      tc::mbar_init(bar(B_KF0 + i), 8);
+      tc::mbar_init(bar(B_KF0 + i), kKWarps);
       tc::mbar_init(bar(B_KE0 + i), 1);
     }
-    for (int i = 0; i < 8; ++i) tc::mbar_init(bar(B_VB0 + i), 1);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(bar(B_VB0 + i), 1);
     tc::mbar_init(bar(B_IMG), 1);
     tc::fence_mbar_init();
   }
-  if (warp == 14) tc::tmem_alloc(tc::smem_u32(tmem_slot), kTmemCols);
+  if (warp == kDistW) tc::tmem_alloc(tc::smem_u32(tmem_slot), kTmemCols);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -143,13 +157,17 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   // The refine kernel may be scheduled on SMs this grid frees.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+#if defined(GPBO_TC_TRACE) || defined(GPBO_TC_CTATIME)
+  unsigned long long cta_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_t0));
+#endif
 
   // Counters are CTA-global across segments (mbarrier phases continue): tiles gi, distance
   // panels gd, K* panels gk.  Every role advances them identically.
   uint32_t gi = 0, gc_seg = 0, gk_seg = 0;
   uint32_t trc = 0;  // trace event count of this thread
   uint32_t img_phase = 0;
-  // completions of B_VE0 / B_VE1 (V buffer freed) and of the block-barrier groups B_VB0..3 /
+  // completions of B_VE0 / B_VE1 (V buffer freed) and of the block-barrier groups B_VB0..1 /
   // B_VB4..7 so far: the single- and double-buffered modes can alternate between segments
   uint32_t ve0 = 0, ve1 = 0, vb0c = 0, vb1c = 0;
 
@@ -159,7 +177,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     const int tb = min(t1, p.tile_first[s + 1]);
     const SearchMeta &m = p.meta[s];
     __syncthreads();  // previous segment fully drained (epilogue consumed the last commit)
-    if (threadIdx.x == 448) {
+    if (threadIdx.x == 32 * kDistW) {
       tc::mbar_arrive_expect_tx(bar(B_IMG), (uint32_t)m.img_bytes);
       tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off, (uint32_t)m.img_bytes, bar(B_IMG));
     }
@@ -168,18 +186,19 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     const int n16 = m.n16, npan = m.npan, kb = m.kb;
     // n16 + 16 <= 128: two V accumulators [0, 128) and [128, 256) alternate between tiles, so
     // the next tile's variance MMAs never wait for the previous tile's drain; block barriers
-    // B_VB0..3 / B_VB4..7 per buffer.  Otherwise one accumulator and 8 block barriers.
+    // B_VB0..1 / B_VB2..3 per buffer.  Otherwise one accumulator and 4 block barriers (one per
+    // 64-wide column block: one commit per panel besides the K* stage release).
     const int nv16 = n16 + kMeanRows;  // V accumulator columns (L^-1 rows + mean rows)
     const bool dbl = nv16 <= 128;
-    const uint32_t vbq = dbl ? 4u : 8u;
+    const uint32_t vbq = dbl ? 2u : 4u;
     const int T = tb - ta;
     const int P64 = (n16 + 63) / 64;  // 64-wide K* panels per tile
     const int P = T * P64;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
     const int tile0 = ta - p.tile_first[s];  // local index of the segment's first tile
 
-    if (warp == 14) {
-      // ===================================================== distance MMA issuer (warp 14)
+    if (warp == kDistW) {
+      // ===================================================== distance MMA issuer
       // 64-wide chunks (one chunk feeds two K* panels; a tcgen05.mma costs max(40, N/2)
       // cycles, so N = 64 halves the issue cost of N = 32), issued as soon as a TMEM ring stage
       // is free -- independent of the variance MMAs, so the K* warps never wait on them.
@@ -202,6 +221,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           const uint32_t dt = tbase + kScratch0 + 64u * (uint32_t)d_st;
           uint32_t a = abase + ab * (uint32_t)kb * 512u;  // 8192 B per K block
           uint32_t bq = x0 + (uint32_t)q * 128u;          // rows 64 q (2048 B)
+          if (lane == 0) trace_ev(p.trace, 24, 11, gc, trc);
           for (int k = 0; k < kb; ++k) {
             tc::mma_f16_split(dt, a, H32, bq, H32, idn, k > 0);
 #ifndef GPBO_EXP_NODIST  // timing experiment only: 1 of the 3 distance products
@@ -219,8 +239,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         tc::mma_commit_warp(bar(B_AE0 + ab));  // A tile consumed
       }
       __syncwarp();
-    } else if (warp == 15) {
-      // ===================================================== variance MMA issuer (warp 15)
+    } else if (warp == kVarW) {
+      // ===================================================== variance MMA issuer
       {
         const uint32_t H64 = tc::sdesc_hi(64);
         const uint32_t l0 = tc::sdesc_lo(tc::smem_u32(img + m.off_l));
@@ -255,17 +275,17 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
               tc::mma_f16_ts(dt, ka, lb + R16, H64, idn, 1u);
               tc::mma_f16_ts(dt, ka + 32u, lb, H64, idn, 1u);
 #endif
+              if (lane == 0) trace_ev(p.trace, 20 + sk, 11, gk, trc);
             }
           }
           tc::mma_commit_warp(bar(B_KE0 + ks));
           // V columns [64 q, 64 q + 64) receive no later contribution: the drain may read them
-          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + 2 * v_pp));
-          if (2 * v_pp + 1 < npan) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + 2 * v_pp + 1));
+          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
           if (++v_pp == P64) {
             // the unused block barriers complete too: every B_VB completes once per tile
-            for (int q = npan; q < (int)vbq; ++q) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
+            for (int q = P64; q < (int)vbq; ++q) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
             v_pp = 0;
             ++v_tl;
             if (vb) ++ve1; else ++ve0;
@@ -273,11 +293,11 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         }
       }
       __syncwarp();
-    } else if (warp == 12 || warp == 13) {
+    } else if (warp == kLoadW0 || warp == kLoadW0 + 1) {
       // ===================================================== candidate loader
       // Raw rows of tile t+1 are prefetched into the other staging buffer by one bulk copy
       // (TMA) while tile t is converted into the float16 hi/lo A operand.
-      const int lt = threadIdx.x - 384;
+      const int lt = threadIdx.x - 32 * kLoadW0;
       const int d = m.d;
       const float *w = reinterpret_cast<const float *>(img + m.off_w);
       const int stage_floats = ((128 * d_max * 4 + 127) & ~127) / 4;
@@ -371,8 +391,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         tc::mbar_arrive(bar(B_AF0 + ab));
         if (lt == 0) trace_ev(p.trace, 11, 8, ti, trc);
       }
-    } else if (warp >= 8 && warp < 12) {
-      // ===================================================== drain + finish (warps 8-11)
+    } else if (warp >= kDrainW0 && warp < kDrainW0 + 4) {
+      // ===================================================== drain + finish (4 warps)
       // One thread per candidate row: waits for the tile's V accumulator, sums V_j^2 over all
       // n16 columns, frees V, adds the K* warps' partial means, and finishes the tile (EI
       // bracket, threshold, refine list) -- while the K* warps already work on the next tile.
@@ -398,15 +418,17 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         // progressive drain: column block p of V is final once panel p's MMAs complete (each
         // barrier of the buffer's block group completes once per tile on that buffer, and the
         // buffer's next tile cannot start before B_VE)
-        const bool trd = warp == 8 && lane == 0;
+        const bool trd = warp == kDrainW0 && lane == 0;
         // the threshold read is issued before the V drain so its latency is hidden
         const float thr = p.mode == kModeArgmax ? read_thr(p, s) : 0.f;
         if (trd) trace_ev(p.trace, 16, 9, ti, trc);
         float vv = 0.f;
         for (int pb = 0; pb < npan; ++pb) {
-          const uint32_t blk = vbq * vb + (uint32_t)pb;
-          tc::mbar_wait(bar(B_VB0 + blk), ((blk >= 4u) ? vb1c : vb0c) & 1u);
-          tc::tc_fence_after();
+          if ((pb & 1) == 0) {  // one barrier per 64-wide block (two 32-wide drain blocks)
+            const uint32_t blk = vbq * vb + (uint32_t)(pb >> 1);
+            tc::mbar_wait(bar(B_VB0 + blk), (vb ? vb1c : vb0c) & 1u);
+            tc::tc_fence_after();
+          }
           const int c = 32 * pb;
 #ifdef GPBO_EXP_NODRAINLD  // timing experiment only: the drain does not read V
           if (false) {
@@ -466,19 +488,19 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const float dvar = vbk * (sf2 + s2) * p.bound_scale;
 #ifndef GPBO_EXP_NOFINISH  // timing experiment only
         finish_fast(p, s, fs, thr, valid, row0s, rloc, mu_t, dmu, var, dvar,
-                    (flags & kFlagUnsafe) != 0u, 2, 128, 8);
+                    (flags & kFlagUnsafe) != 0u, 2, 128, kDrainW0);
 #else
         (void)dmu; (void)dvar; (void)valid; (void)rloc;
 #endif
         if (trd) trace_ev(p.trace, 19, 9, ti, trc);
       }
-    } else if (warp < 8) {
-      // ===================================================== K* warps (0-7)
-      // Per 64-wide panel q (= distance chunk q): warp half `half` of lane quarter lq evaluates
-      // training points [64 q + 32 half, +32) for its 32 candidate rows: one tcgen05.ld (x32)
-      // of the squared distances, K* = k(h), the mean partials, the float16 hi/lo split, two
-      // tcgen05.st (x16) into the K* stage (k steps 2 half, 2 half + 1).
-      const int lq = warp & 3, half = warp >> 2;
+    } else if (warp < kKWarps) {
+      // ===================================================== K* warps
+      // Per 64-wide panel q (= distance chunk q): part `part` of lane quarter lq evaluates
+      // training points [64 q + kCW part, +kCW) for its 32 candidate rows: one tcgen05.ld of the
+      // squared distances, K* = k(h), the float16 hi/lo split, tcgen05.st into the K* stage
+      // (16-wide k steps kCW/16 part ..).
+      const int lq = warp & 3, part = warp >> 2;
       const uint32_t tl_addr = tbase + ((uint32_t)(32 * lq) << 16);
       const int kind = m.kernel;
       const float c0 = m.c0, c1 = m.c1, c2 = m.c2, c3 = m.c3;
@@ -487,33 +509,33 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       int pp = 0;
       for (int g = 0; g < P; ++g) {
         const uint32_t st = ec % kDepth;
-        const int jb = 64 * pp + 32 * half;
-        const int nv = min(32, n16 - jb);  // valid points of this warp (32, 16 or <= 0)
-        const bool trw = (warp == 0 || warp == 7) && lane == 0;
-        // kMerged (every search of the launch has n16 <= 128): one acquire for both resources --
-        // the distances (DF) and a free K* stage (KE) -- then one fence, and the distance stage
-        // released together with the K* hand-over (config 3: -12 %).  Otherwise separate
-        // acquires (the early DE release keeps the distance ring ahead; 2 % faster at config 2).
+        const int jb = 64 * pp + kCW * part;
+        const int nv = min(kCW, n16 - jb);  // valid points of this warp (kCW, 16 or <= 0)
+        const bool trw = (warp == 0 || warp == kKWarps - 1) && lane == 0;
+        // kMerged (every search of the launch has n16 + 16 <= 128): one acquire for both
+        // resources -- the distances (DF) and a free K* stage (KE) -- then one fence, and the
+        // distance stage released together with the K* hand-over (config 3: -12 %).  Otherwise
+        // separate acquires (the early DE release keeps the distance ring ahead).
         // A compile-time choice: the run-time branch cost registers and was slower in both cases.
         const uint32_t ks = gk % kKStages;
-        uint32_t hr[32];
+        const uint32_t da = tl_addr + kScratch0 + 64u * st + (uint32_t)(kCW * part);
+        uint32_t hr[kCW];
+        auto load_h = [&]() {
+          if constexpr (kCW == 32) tc::tmem_ld32(da, hr);
+          else tc::tmem_ld16(da, *reinterpret_cast<uint32_t(*)[16]>(hr));
+          tc::tmem_wait_ld();
+        };
         if (kMerged) {
           tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
           tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
           tc::tc_fence_after();
-          if (nv > 0) {
-            tc::tmem_ld32(tl_addr + kScratch0 + 64u * st + 32u * half, hr);
-            tc::tmem_wait_ld();
-          }
+          if (nv > 0) load_h();
           if (trw) trace_ev(p.trace, 6, warp, gk, trc);
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         } else {
           tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
           tc::tc_fence_after();
-          if (nv > 0) {
-            tc::tmem_ld32(tl_addr + kScratch0 + 64u * st + 32u * half, hr);
-            tc::tmem_wait_ld();
-          }
+          if (nv > 0) load_h();
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));  // the scratch stage is free
@@ -524,42 +546,48 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         }
         if (nv > 0) {
-          float kv[32];
+          float kv[kCW];
 #ifdef GPBO_EXP_NOKSTAR  // timing experiment only: no kernel evaluation (wrong results)
           if (true) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) kv[q] = __uint_as_float(hr[q]);
+            for (int q = 0; q < kCW; ++q) kv[q] = __uint_as_float(hr[q]);
           } else
 #endif
           // |h| (a free source modifier) rather than max(h, 0): the GEMM-form h can be a few ulps
           // negative; |h| stays within the same error bound of the true h >= 0
           if (kind == GPBO_RBF) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
+            for (int q = 0; q < kCW; ++q)
               kv[q] = ex2_approx(fmaf(fabsf(__uint_as_float(hr[q])), c1, c0));
           } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
+            for (int q = 0; q < kCW; ++q) {
               const float tq = sqrt_approx(fabsf(__uint_as_float(hr[q])));
               kv[q] = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
             }
           }
-          if (nv < 32) {  // points beyond n16: scratch columns the distance MMA did not write
+          if (nv < kCW) {  // points beyond n16: scratch columns the distance MMA did not write
 #pragma unroll
-            for (int q = 16; q < 32; ++q) kv[q] = 0.f;
+            for (int q = 16; q < kCW; ++q) kv[q] = 0.f;
           }
-          uint32_t hw[16], lw[16];
+          uint32_t hw[kCW / 2], lw[kCW / 2];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int q = 0; q < kCW / 2; ++q) {
             const float h0 = __uint_as_float(__float_as_uint(kv[2 * q]) & 0xFFFFE000u);
             const float h1 = __uint_as_float(__float_as_uint(kv[2 * q + 1]) & 0xFFFFE000u);
             hw[q] = tc::pack_f16x2(h0, h1);
             lw[q] = tc::pack_f16x2(kv[2 * q] - h0, kv[2 * q + 1] - h1);
           }
-          // this warp's 32 k values are k steps 2 half, 2 half + 1 of the panel
-          const uint32_t kt = tl_addr + kKstar0 + 64u * ks + 16u * half;
-          tc::tmem_st16(kt, hw);
-          tc::tmem_st16(kt + 32u, lw);
+          // this warp's kCW k values are k steps (kCW / 16) part .. of the panel: hi at +8 per
+          // k step, lo at +32
+          const uint32_t kt = tl_addr + kKstar0 + 64u * ks + (uint32_t)(kCW / 2 * part);
+          if constexpr (kCW == 32) {
+            tc::tmem_st16(kt, *reinterpret_cast<const uint32_t(*)[16]>(hw));
+            tc::tmem_st16(kt + 32u, *reinterpret_cast<const uint32_t(*)[16]>(lw));
+          } else {
+            tc::tmem_st8(kt, *reinterpret_cast<const uint32_t(*)[8]>(hw));
+            tc::tmem_st8(kt + 32u, *reinterpret_cast<const uint32_t(*)[8]>(lw));
+          }
 #ifndef GPBO_EXP_NOWAITST  // timing experiment only (races with the MMA)
           tc::tmem_wait_st();
 #endif
@@ -583,7 +611,16 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 14) tc::tmem_dealloc(tbase, kTmemCols);
+#if defined(GPBO_TC_TRACE) || defined(GPBO_TC_CTATIME)  // per-CTA start / end (globaltimer, ns):
+  // slice 5 of the trace buffer
+  if (threadIdx.x == 0 && p.trace != nullptr && blockIdx.x < 8192) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    p.trace[5 * 16384 + 2 * blockIdx.x] = cta_t0;
+    p.trace[5 * 16384 + 2 * blockIdx.x + 1] = t1;
+  }
+#endif
+  if (warp == kDistW) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
 // ------------------------------------------------------------------ operand images (fit time)

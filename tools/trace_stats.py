@@ -18,7 +18,7 @@ bypd = collections.defaultdict(list)
 for i in range(len(V) - 1):
     bypd[V[i][1] % npan].append(V[i + 1][0] - V[i][0])
 print("V issue interval by panel", {k: int(statistics.mean(v)) for k, v in sorted(bypd.items())})
-for role in ("r0", "r7"):
+for role in sorted({x[2] for x in ev if x[1] == "epi:kf_arrive"}):
     e = [x for x in ev if x[2] == role]
     by = collections.defaultdict(dict)
     for c, n, r, i in e:

@@ -29,13 +29,22 @@ for sl in range(5):
         ev.append((clk, key >> 56, (key >> 48) & 0xFF, key & 0xFFFFFFFFFFFF))
 n = len(ev)
 ev.sort()
-t0 = ev[0][0]
+t0 = ev[0][0] if ev else 0
 names = {1: "mma:wait_kf", 2: "mma:kf_ok", 3: "mma:V_issued", 4: "mma:dist_issued",
          5: "epi:wait_df", 6: "epi:df_ok", 7: "epi:ke_ok", 8: "epi:kf_arrive",
          9: "ld:wait", 10: "ld:go", 11: "ld:A_full", 12: "mma:wait_de", 13: "mma:de_ok",
          14: "mma:V_mmas_done", 15: "mma:V_start",
-         16: "drn:start", 17: "drn:v_done", 18: "drn:pf_ok", 19: "drn:finished"}
+         16: "drn:start", 17: "drn:v_done", 18: "drn:pf_ok", 19: "drn:finished",
+         20: "mma:V_k0", 21: "mma:V_k1", 22: "mma:V_k2", 23: "mma:V_k3", 24: "mma:dist_start"}
 lim = int(sys.argv[1]) if len(sys.argv) > 1 else 400
 for clk, tag, role, idx in ev[:lim]:
     print(f"{clk - t0:9d} {names.get(tag, tag):16s} r{role:<3d} #{idx}")
-print("events", n, "span cycles", ev[-1][0] - t0)
+print("events", n, "span cycles", ev[-1][0] - t0 if ev else 0)
+cta = b[5 * 16384:5 * 16384 + 2 * 8192].reshape(-1, 2).astype(np.int64)
+cta = cta[cta[:, 1] > 0]
+if len(cta):
+    g0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - g0) / 1e3, (cta[:, 1] - g0) / 1e3
+    print(f"CTAs {len(cta)}: start us min/med/max {st.min():.1f}/{np.median(st):.1f}/{st.max():.1f}"
+          f"  end us min/med/max {en.min():.1f}/{np.median(en):.1f}/{en.max():.1f}"
+          f"  dur med {np.median(en - st):.1f}  slowest CTAs {np.argsort(-(en - st))[:6].tolist()}")
