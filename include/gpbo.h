@@ -362,12 +362,16 @@ int64_t gpbo_last_refine_count(const gpbo_ctx *ctx);
  * (small problems; no refine phase), 5 = float64 dense refine of every row (gp_posterior beyond
  * the direct kernel's envelope: no fast phase). */
 int gpbo_last_score_impl(const gpbo_ctx *ctx);
+/* 1 if the last scoring call's tcgen05 fast phase (impl 2) ran as CTA pairs (cta_group::2,
+ * M = 256 MMAs over two SMs; chosen for models whose searches all have n > 112 and whose pair
+ * image fits; GPBO_TC_PAIR=0 in the environment disables it), else 0. */
+int gpbo_last_tc_pair(const gpbo_ctx *ctx);
 
 /* Per-kernel timing with CUDA events recorded on ctx's stream around every library kernel
  * launch (for bench.py's roofline).  gpbo_set_profiling(ctx, 1) enables it and clears the
  * totals; gpbo_kernel_time returns the launch count and summed milliseconds of one kind:
  * 0 = fit (H1-H4), 1 = scoring fast phase (H6-H9), 2 = float64 refine phase, 3 = operand pack,
- * 4 = precise-mean tier (float64 mu~ for searches with sf2 |alpha|_1 > 1500, reading R13). */
+ * 4 = precise-mean tier (float64 mu~ for searches with sf2 |alpha|_1 > 5e4, reading R13). */
 gpbo_status gpbo_set_profiling(gpbo_ctx *ctx, int on);
 gpbo_status gpbo_kernel_time(gpbo_ctx *ctx, int kind, int64_t *count, double *ms);
 

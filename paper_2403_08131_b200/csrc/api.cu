@@ -58,6 +58,7 @@ struct gpbo_ctx {
   double *etab_d = nullptr;  // e^{-k/16} table of the precise tier
   int64_t last_refine = 0;
   int last_impl = 0;
+  int last_pair = 0;  // the last tcgen05 fast phase ran as CTA pairs
   unsigned long long *trace = nullptr;  // device buffer for the next tcgen05 launch        // 1 = CUDA-core, 2 = tcgen05 fast phase in the last scoring call  // candidates the last argmax call flagged for the refine phase
   int num_sms = 148;
   // chunked host feed of ei_score_argmax (mem = GPBO_HOST): candidate chunks are copied on
@@ -309,6 +310,9 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   if (ctx->score_impl == 2 && !use_tc && !dense_only)
     return fail(ctx, GPBO_ENOTSUP, "tcgen05 scoring requested outside its supported envelope");
   const int tile = use_tc ? gpbo::kTcTile : gpbo::kSimtTile;  // (direct: any)
+  // CTA-pair kernel: every search gets an even tile count (whole 256-row pair tiles; the second
+  // half of a ragged pair tile scores nothing)
+  const bool pair = use_tc && !use_tcs && model->meta[s_first].tc_pair;
   h_tiles[0] = 0;
   int64_t xo = 0;
   for (int i = 0; i < S; ++i) {
@@ -324,7 +328,8 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     // an asynchronous fit's status is not known here: its tiles run and the kernels skip a
     // failed search on the device
     const bool fitted = model->meta_pending || st_i == GPBO_OK || st_i == GPBO_WDEGENERATE;
-    const int64_t t = fitted ? (Ms + tile - 1) / tile : 0;  // failed fits score nothing
+    int64_t t = fitted ? (Ms + tile - 1) / tile : 0;  // failed fits score nothing
+    if (pair) t = (t + 1) & ~(int64_t)1;
     if ((int64_t)h_tiles[i] + t > (1ll << 30))
       return fail(ctx, GPBO_EINVAL, "too many candidates in one call");
     h_tiles[i + 1] = h_tiles[i] + (int32_t)t;
@@ -390,12 +395,14 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
   p.break_bracket = ctx->bound_scale < 0.f ? 1 : 0;
   const int tiles = h_tiles[S];
   ctx->last_impl = direct ? 4 : dense_only ? 5 : use_tcs ? 3 : use_tc ? 2 : 1;
+  ctx->last_pair = pair && !direct && !dense_only ? 1 : 0;
   const int64_t floats_all = xo;
   // element offset in X* of the first row of tile t (tile indices of this call)
   auto tile_elem = [&](int t) -> int64_t {
     if (t >= tiles) return floats_all;
     int i = (int)(std::upper_bound(h_tiles, h_tiles + S + 1, t) - h_tiles) - 1;
-    return h_xoff[i] + (int64_t)(t - h_tiles[i]) * tile * model->meta[s_first + i].d;
+    const int64_t Ms_i = h_off[i + 1] - h_off[i];
+    return h_xoff[i] + std::min((int64_t)(t - h_tiles[i]) * tile, Ms_i) * model->meta[s_first + i].d;
   };
   const int nchunk = (host_src && use_tc) ? std::max(1, std::min(8, tiles / 1024)) : 1;
   if (host_src && nchunk <= 1 && floats_all > 0)
@@ -442,7 +449,10 @@ gpbo_status run_score(gpbo_ctx *ctx, const gpbo_model *model, int s_first, int S
     p.mean64 = ctx->mean_d;
   }
   for (int c = 0; c < nchunk && !dense_only; ++c) {
-    const int ta = (int)((int64_t)tiles * c / nchunk), tb = (int)((int64_t)tiles * (c + 1) / nchunk);
+    // (pair: chunk boundaries on whole pair tiles)
+    const int ts = pair ? 2 : 1, units = tiles / ts;
+    const int ta = ts * (int)((int64_t)units * c / nchunk);
+    const int tb = ts * (int)((int64_t)units * (c + 1) / nchunk);
     if (nchunk > 1) {
       // chunk c's rows: from its first tile's row to the next chunk's (the last chunk: to the end)
       const int64_t e0 = c == 0 ? 0 : tile_elem(ta), e1 = tile_elem(tb);
@@ -595,9 +605,11 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
 extern "C" {
 
 const char *gpbo_version(void) {
-  return "libgpbo 0.3 (sm_100a; fit fp64 1 CTA/search + O(n^2) append + ML-II; score: tcgen05 "
-         "fp16x3 resident / TMA-streamed, fp64 precise-mean tier, fp64 direct for small problems, "
-         "CUDA-core fallback; fp64 refine with bracket self-check; host planner)";
+  return "libgpbo 0.4 (sm_100a; fit fp64 1 CTA or 8-CTA cluster/search + O(n^2) append + ML-II; "
+         "score: tcgen05 fp16x3 resident (CTA pairs, cta_group::2, for n > 112) / TMA-streamed, "
+         "mean on the tensor cores, fp64 precise-mean tier, fp64 direct for small problems, "
+         "CUDA-core fallback; fp64 refine with bracket self-check; fp64 tiled posterior; host "
+         "planner)";
 }
 
 gpbo_status gpbo_nccl_unique_id(void *out) {
@@ -693,6 +705,7 @@ gpbo_status gpbo_debug_bound_scale(gpbo_ctx *ctx, float scale) {
 }
 
 int gpbo_last_score_impl(const gpbo_ctx *ctx) { return ctx ? ctx->last_impl : -1; }
+int gpbo_last_tc_pair(const gpbo_ctx *ctx) { return ctx ? ctx->last_pair : -1; }
 
 gpbo_status gpbo_debug_trace(gpbo_ctx *ctx, void *dev_buf) {
   if (!ctx) return GPBO_EINVAL;
@@ -759,6 +772,12 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
     if (n_in[s] >= 1 && n_in[s] <= GPBO_MAX_N && d_in[s] >= 1 && d_in[s] <= GPBO_MAX_D &&
         gpbo::tc_needs_stream(n_in[s], d_in[s]))
       stream_layout = true;
+  // the CTA-pair scoring layout when every search's resident image fits it (uniform per model)
+  bool pair_layout = !stream_layout;
+  for (int s = 0; s < S && pair_layout; ++s)
+    if (n_in[s] < 1 || n_in[s] > GPBO_MAX_N || d_in[s] < 1 || d_in[s] > GPBO_MAX_D ||
+        !gpbo::tc_pair_fits(n_in[s], d_in[s]))
+      pair_layout = false;
   for (int s = 0; s < S; ++s) {
     const int n = n_in[s], d = d_in[s];
     if (n < 1 || n > GPBO_MAX_N || d < 1 || d > GPBO_MAX_D) {
@@ -780,6 +799,7 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
     q.lt_off = nlt; nlt += (int64_t)q.n_pad * q.n_pad;
     q.a_off = na; na += q.n_pad;
     q.tc_stream = stream_layout ? 1 : 0;
+    q.tc_pair = pair_layout ? 1 : 0;
     gpbo::tc_fill_geometry(q);
     q.img_off = nimg;
     if (lml_only) q.tc_ok = 0; else nimg += gpbo::tc_image_bytes(q);

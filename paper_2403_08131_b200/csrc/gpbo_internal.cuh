@@ -56,6 +56,7 @@ struct SearchMeta {
   // ---- tcgen05 fast phase (score_tc.cu); valid when tc_ok
   int32_t tc_ok;
   int32_t tc_stream;    // streamed image layout (score_tcs.cu) instead of the resident one
+  int32_t tc_pair;      // resident CTA-pair layout (two half images, score_tc.cu kPair)
   int32_t n16;          // n rounded up to 16 (V accumulator columns)
   int32_t kb;           // 16-wide K blocks of the augmented distance operand [x, |x|^2, 1]
   int32_t npan;         // 32-wide training-point panels

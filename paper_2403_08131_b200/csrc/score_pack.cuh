@@ -40,6 +40,36 @@ __host__ __device__ inline TcGeom tc_geom(int n, int d) {
 }
 
 
+// CTA-pair layout (score_tc.cu, kPair): every search has two images of `half` bytes, one per CTA
+// of the pair, each holding half of every B operand's rows (the MMA's N split):
+//   [0, off_l)      X chunks: chunk q (training points [64 q, 64 q + N_q), N_q = min(64, n16 - 64 q)),
+//                   K block k: hi (32 rows x 32 B) then lo, SWIZZLE_32B K-major; CTA r holds
+//                   rows [64 q + r N_q / 2, + N_q / 2)
+//   [off_l, off_w)  L^-1 + mean-row slabs, one per 16-wide k step s (k in [16 s, 16 s + 16)):
+//                   rows j in [16 s, n16 + 16) (N_s = n16 + 16 - 16 s), CTA r holds rows
+//                   [16 s + r N_s / 2, + N_s / 2) as hi (N_s / 2 x 32 B) then lo, SWIZZLE_32B
+//   [off_w, half)   per-dimension candidate scales (GPBO_MAX_D floats)
+struct TcPairGeom {
+  int n16, kb, nchunk, nks, off_l, off_w, half;
+};
+
+// byte offset of k-step slab s in the L part: 32 sum_{s' < s} (nv16 - 16 s')
+__host__ __device__ inline int tc_pair_slab(int nv16, int s) {
+  return 32 * (s * nv16 - 8 * s * (s - 1));
+}
+
+__host__ __device__ inline TcPairGeom tc_pair_geom(int n, int d) {
+  TcPairGeom g;
+  g.n16 = (n + 15) & ~15;
+  g.kb = (d + 2 + 15) / 16;
+  g.nchunk = (g.n16 + 63) / 64;
+  g.nks = g.n16 / 16;
+  g.off_l = align1k(g.nchunk * g.kb * 2048);
+  g.off_w = align1k(g.off_l + tc_pair_slab(g.n16 + kMeanRows, g.nks));
+  g.half = align1k(g.off_w + GPBO_MAX_D * 4);
+  return g;
+}
+
 // One CTA per search.  Scales (powers of two, exact): x^ = g x/l 2^-e with g = sqrt5 (Matern)
 // or 1/sqrt2 (RBF) and e chosen so max(|x^*|^2 over the unit box, |x^_j|^2) <= 2^13;
 // K* 2^tK <= 2^13; L^-1 2^uL <= 2^14.  V = L^-1 K* then carries 2^(tK + uL).
@@ -110,19 +140,68 @@ __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, cons
     *reinterpret_cast<__half *>(base_hi + off) = hi;
     *reinterpret_cast<__half *>(base_lo + off) = lo;
   };
+  const int uA = (int)sc[4];
+  // one B-operand row j of the variance MMA at k-step column kk: L^-1 rows (j < n16) or the mean
+  // rows (j = n16 + t), written as the hi / lo fp16 pair at `off` of the two blocks
+  auto put_l = [&](unsigned char *bhi, unsigned char *blo, uint32_t off, int j, int kk) {
+    if (j < g.n16) {
+      const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
+      put(bhi, blo, off, v);
+      return;
+    }
+    const int t = j - g.n16;
+    const double a = kk < n ? ldexp(alpha64[m.a_off + kk], uA) : 0.0;
+    const __half ah = __double2half(a);
+    __half vh = __double2half(0.0), vl = __double2half(0.0);
+    if (t == 0) vh = ah;
+    else if (t == 1) vh = __double2half(fabs(a));
+    else if (t == 2) vl = __double2half(ldexp(a - (double)__half2float(ah), 11));
+    *reinterpret_cast<__half *>(bhi + off) = vh;
+    *reinterpret_cast<__half *>(blo + off) = vl;
+  };
+  // augmented training operand value [-2 x^_j, 1, |x^_j|^2] at (j, k)
+  auto xval = [&](int j, int k) -> double {
+    if (j >= n) return 0.0;
+    if (k < d) return -2.0 * xs * X[(size_t)k * n + j];
+    if (k == d) return 1.0;
+    if (k == d + 1) {
+      double pj = 0.0;
+      for (int c = 0; c < d; ++c) pj += (xs * X[(size_t)c * n + j]) * (xs * X[(size_t)c * n + j]);
+      return pj;
+    }
+    return 0.0;
+  };
+  if (m.tc_pair) {
+    const TcPairGeom pg = tc_pair_geom(n, d);
+    const int nv16 = pg.n16 + kMeanRows;
+    for (int r = 0; r < 2; ++r) {
+      unsigned char *base = img + r * pg.half;
+      for (int idx = t0; idx < pg.nchunk * pg.kb * 32 * 16; idx += tstep) {
+        const int k = idx & 15, rr = (idx >> 4) & 31, cb = idx >> 9;  // cb = q kb + kblk
+        const int q = cb / pg.kb, kblk = cb - q * pg.kb;
+        const int h = min(64, pg.n16 - 64 * q) / 2;
+        const double v = rr < h ? xval(64 * q + r * h + rr, 16 * kblk + k) : 0.0;
+        unsigned char *hi = base + cb * 2048;
+        put(hi, hi + 1024, tc::sw_offset(rr, k * 2, 32), v);
+      }
+      for (int s = 0; s < pg.nks; ++s) {
+        const int h = (nv16 - 16 * s) / 2;
+        unsigned char *hi = base + pg.off_l + tc_pair_slab(nv16, s);
+        for (int idx = t0; idx < h * 16; idx += tstep) {
+          const int rr = idx >> 4, kk = idx & 15;
+          put_l(hi, hi + h * 32, tc::sw_offset(rr, kk * 2, 32), 16 * s + r * h + rr, 16 * s + kk);
+        }
+      }
+      float *wp = reinterpret_cast<float *>(base + pg.off_w);
+      for (int c = t0; c < GPBO_MAX_D; c += tstep)
+        wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
+    }
+    return;
+  }
   // augmented training operand [-2 x^_j, 1, |x^_j|^2], K blocks of 16, rows n16
   for (int idx = t0; idx < g.n16 * g.kb * 16; idx += tstep) {
     const int j = idx / (g.kb * 16), k = idx % (g.kb * 16);
-    double v = 0.0;
-    if (j < n) {
-      if (k < d) v = -2.0 * xs * X[(size_t)k * n + j];
-      else if (k == d) v = 1.0;
-      else if (k == d + 1) {
-        double pj = 0.0;
-        for (int c = 0; c < d; ++c) pj += (xs * X[(size_t)c * n + j]) * (xs * X[(size_t)c * n + j]);
-        v = pj;
-      }
-    }
+    const double v = xval(j, k);
     const int kblk = k >> 4;
     if (stream) {  // chunk-major: chunk q, K block, hi / lo blocks of 64 rows x 32 B
       unsigned char *hi = img + (((j >> 6) * g.kb + kblk) * 2) * 2048;
@@ -161,28 +240,12 @@ __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, cons
   }
   // L^-1 panels: panel p holds rows j in [32p, n16), k in [32p, 32p + 32), then the kMeanRows
   // mean rows (j = n16 + t)
-  const int uA = (int)sc[4];
   for (int pp = 0; pp < g.npan; ++pp) {
     const int R = g.n16 + kMeanRows - 32 * pp;
     unsigned char *hi = img + g.off_l + (pp * (g.n16 + kMeanRows) - 16 * pp * (pp - 1)) * 128;
     for (int idx = t0; idx < R * 32; idx += tstep) {
       const int r = idx >> 5, k = idx & 31;
-      const int j = 32 * pp + r, kk = 32 * pp + k;
-      const uint32_t off = tc::sw_offset(r, k * 2, 64);
-      if (j < g.n16) {
-        const double v = (kk <= j && j < n) ? ldexp(Li[(size_t)j * n + kk], uL) : 0.0;
-        put(hi, hi + R * 64, off, v);
-      } else {
-        const int t = j - g.n16;
-        const double a = kk < n ? ldexp(alpha64[m.a_off + kk], uA) : 0.0;
-        const __half ah = __double2half(a);
-        __half vh = __double2half(0.0), vl = __double2half(0.0);
-        if (t == 0) vh = ah;
-        else if (t == 1) vh = __double2half(fabs(a));
-        else if (t == 2) vl = __double2half(ldexp(a - (double)__half2float(ah), 11));
-        *reinterpret_cast<__half *>(hi + off) = vh;
-        *reinterpret_cast<__half *>(hi + R * 64 + off) = vl;
-      }
+      put_l(hi, hi + R * 64, tc::sw_offset(r, k * 2, 64), 32 * pp + r, 32 * pp + k);
     }
   }
   float2 *ap = reinterpret_cast<float2 *>(img + g.off_a);

@@ -37,6 +37,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "score_common.cuh"
 #include "score_tc.cuh"
@@ -107,7 +108,13 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
   return s;
 }
 
-template <bool kMerged>
+// kPair: a cluster of two CTAs on one TPC scores 256-candidate pair tiles with M = 256 MMAs
+// (cta_group::2): each CTA holds its 128 rows (candidate tile, distances, K* stages, V) and half
+// of every B operand (the search's half image, score_pack.cuh); CTA 0 issues every MMA for both,
+// and every handoff, MMA issue and commit is paid once per 256 candidates.  The pair tile u of a
+// search covers its 128-row tiles 2u (CTA 0) and 2u + 1 (CTA 1); the host gives every search an
+// even tile count.
+template <bool kMerged, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, int kb_max, int d_max) {
   extern __shared__ unsigned char sm_raw[];
@@ -122,34 +129,52 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   auto bar = [&](int i) { return tc::smem_u32(bars + i); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // this launch covers tiles [tile_lo, tile_lo + total_tiles) of the call (chunked host feeds)
-  const int t0 = tile_lo + (int)((long long)total_tiles * blockIdx.x / gridDim.x);
-  const int t1 = tile_lo + (int)((long long)total_tiles * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t rank = kPair ? tc::cluster_rank() : 0u;  // CTA of the pair (0 issues the MMAs)
+  const bool leader = rank == 0u;
+  constexpr int kTs = kPair ? 2 : 1;  // 128-row tiles per (pair) tile
+  // this launch covers tiles [tile_lo, tile_lo + total_tiles) of the call (chunked host feeds);
+  // ta / tb below count (pair) tiles: units of kTs 128-row tiles
+  const int units = total_tiles / kTs, unit_lo = tile_lo / kTs;
+  const int gid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ngrp = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int t0 = unit_lo + (int)((long long)units * gid / ngrp);
+  const int t1 = unit_lo + (int)((long long)units * (gid + 1) / ngrp);
+  // an arrival on the issuing CTA's copy of a barrier (the pair's consumers of CTA 0's MMAs):
+  // relaxed -- the arriving threads' TMEM loads / stores have completed (tcgen05.wait::ld/st)
+  auto arrive_leader = [&](uint32_t b) {
+    if (kPair) tc::mbar_arrive_cluster_relaxed(tc::mapa(b, 0u));
+    else tc::mbar_arrive(b);
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(bar(B_AF0 + i), 64);
+      // (pair: one arrival per CTA's loader on CTA 0's barrier; else every loader thread)
+      tc::mbar_init(bar(B_AF0 + i), kPair ? 2 : 64);
       tc::mbar_init(bar(B_AE0 + i), 1);
 
       tc::mbar_init(bar(B_VF0 + i), 1);
-      tc::mbar_init(bar(B_VE0 + i), 4);
+      tc::mbar_init(bar(B_VE0 + i), 4 * kTs);
       tc::mbar_init(bar(B_SF0 + i), 1);
     }
     for (int i = 0; i < kDepth; ++i) {
       tc::mbar_init(bar(B_DF0 + i), 1);
-      tc::mbar_init(bar(B_DE0 + i), kKWarps);
+      tc::mbar_init(bar(B_DE0 + i), kKWarps * kTs);
     }
     for (int i = 0; i < kKStages; ++i) {
-      tc::mbar_init(bar(B_KF0 + i), kKWarps);
+      tc::mbar_init(bar(B_KF0 + i), kKWarps * kTs);
       tc::mbar_init(bar(B_KE0 + i), 1);
     }
     for (int i = 0; i < 4; ++i) tc::mbar_init(bar(B_VB0 + i), 1);
     tc::mbar_init(bar(B_IMG), 1);
     tc::fence_mbar_init();
   }
-  if (warp == kDistW) tc::tmem_alloc(tc::smem_u32(tmem_slot), kTmemCols);
+  if (warp == kDistW) {
+    if (kPair) tc::tmem_alloc2(tc::smem_u32(tmem_slot), kTmemCols);
+    else tc::tmem_alloc(tc::smem_u32(tmem_slot), kTmemCols);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if (kPair) tc::cluster_sync();  // both CTAs' barriers initialised before any remote arrival
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   // programmatic dependent launch: barrier init and TMEM allocation above overlapped the
@@ -172,14 +197,17 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
   uint32_t ve0 = 0, ve1 = 0, vb0c = 0, vb1c = 0;
 
   for (int ta = t0; ta < t1;) {
-    // ---------------- segment [ta, tb): consecutive tiles of one search
-    const int s = search_of(p.tile_first, p.S, ta);
-    const int tb = min(t1, p.tile_first[s + 1]);
+    // ---------------- segment [ta, tb): consecutive (pair) tiles of one search
+    const int s = search_of(p.tile_first, p.S, kTs * ta);
+    const int tb = min(t1, p.tile_first[s + 1] / kTs);
     const SearchMeta &m = p.meta[s];
-    __syncthreads();  // previous segment fully drained (epilogue consumed the last commit)
+    // previous segment fully drained (epilogue consumed the last commit; for the pair that
+    // commit followed every MMA reading this CTA's half image, so it may be replaced)
+    __syncthreads();
     if (threadIdx.x == 32 * kDistW) {
       tc::mbar_arrive_expect_tx(bar(B_IMG), (uint32_t)m.img_bytes);
-      tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off, (uint32_t)m.img_bytes, bar(B_IMG));
+      tc::bulk_g2s(tc::smem_u32(img), p.img + m.img_off + (int64_t)rank * m.img_bytes,
+                   (uint32_t)m.img_bytes, bar(B_IMG));
     }
     tc::mbar_wait(bar(B_IMG), img_phase);
     img_phase ^= 1u;
@@ -195,9 +223,13 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     const int P64 = (n16 + 63) / 64;  // 64-wide K* panels per tile
     const int P = T * P64;
     const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
-    const int tile0 = ta - p.tile_first[s];  // local index of the segment's first tile
+    // local 128-row tile index of this CTA's first tile of the segment (tile tl: tile0 + kTs tl)
+    const int tile0 = kTs * ta + (int)rank - p.tile_first[s];
 
-    if (warp == kDistW) {
+    if (warp == kDistW || warp == kVarW) {
+      // the pair's second CTA issues nothing: its operands are read by CTA 0's MMAs
+      if (!leader) {
+      } else if (warp == kDistW) {
       // ===================================================== distance MMA issuer
       // 64-wide chunks (one chunk feeds two K* panels; a tcgen05.mma costs max(40, N/2)
       // cycles, so N = 64 halves the issue cost of N = 32), issued as soon as a TMEM ring stage
@@ -217,32 +249,48 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         for (int q = 0; q < ndc; ++q) {
           tc::mbar_wait(bar(B_DE0 + d_st), d_ph ^ 1u);
           tc::tc_fence_after();
-          const uint32_t idn = tc::idesc_f16((uint32_t)min(64, n16 - 64 * q));
+          const uint32_t Nq = (uint32_t)min(64, n16 - 64 * q);
           const uint32_t dt = tbase + kScratch0 + 64u * (uint32_t)d_st;
           uint32_t a = abase + ab * (uint32_t)kb * 512u;  // 8192 B per K block
-          uint32_t bq = x0 + (uint32_t)q * 128u;          // rows 64 q (2048 B)
           if (lane == 0) trace_ev(p.trace, 24, 11, gc, trc);
-          for (int k = 0; k < kb; ++k) {
-            tc::mma_f16_split(dt, a, H32, bq, H32, idn, k > 0);
+          if constexpr (kPair) {
+            // this CTA's half of chunk q: K block k hi at +2048 k, lo at +1024 (score_pack.cuh)
+            const uint32_t idn = tc::idesc_f16_m256(Nq);
+            uint32_t bq = x0 + (uint32_t)(q * kb) * 128u;
+            for (int k = 0; k < kb; ++k) {
+              tc::mma2_f16_split(dt, a, H32, bq, H32, idn, k > 0);
+              tc::mma2_f16_split(dt, a, H32, bq + 64u, H32, idn, 1u);
+              tc::mma2_f16_split(dt, a + 256u, H32, bq, H32, idn, 1u);  // A lo: +4096 B
+              a += 512u;
+              bq += 128u;
+            }
+            tc::mma2_commit_warp(bar(B_DF0 + d_st));
+          } else {
+            const uint32_t idn = tc::idesc_f16(Nq);
+            uint32_t bq = x0 + (uint32_t)q * 128u;          // rows 64 q (2048 B)
+            for (int k = 0; k < kb; ++k) {
+              tc::mma_f16_split(dt, a, H32, bq, H32, idn, k > 0);
 #ifndef GPBO_EXP_NODIST  // timing experiment only: 1 of the 3 distance products
-            tc::mma_f16_split(dt, a, H32, bq + xlo, H32, idn, 1u);
-            tc::mma_f16_split(dt, a + 256u, H32, bq, H32, idn, 1u);  // A lo: +4096 B
+              tc::mma_f16_split(dt, a, H32, bq + xlo, H32, idn, 1u);
+              tc::mma_f16_split(dt, a + 256u, H32, bq, H32, idn, 1u);  // A lo: +4096 B
 #endif
-            a += 512u;
-            bq += 2u * xlo;
+              a += 512u;
+              bq += 2u * xlo;
+            }
+            tc::mma_commit_warp(bar(B_DF0 + d_st));
           }
-          tc::mma_commit_warp(bar(B_DF0 + d_st));
           if (lane == 0) trace_ev(p.trace, 4, 11, gc, trc);
           ++gc;
           if (++d_st == kDepth) { d_st = 0; d_ph ^= 1u; }
         }
-        tc::mma_commit_warp(bar(B_AE0 + ab));  // A tile consumed
+        if (kPair) tc::mma2_commit_warp(bar(B_AE0 + ab));  // A tiles of both CTAs consumed
+        else tc::mma_commit_warp(bar(B_AE0 + ab));         // A tile consumed
       }
       __syncwarp();
-    } else if (warp == kVarW) {
+      } else {
       // ===================================================== variance MMA issuer
       {
-        const uint32_t H64 = tc::sdesc_hi(64);
+        const uint32_t H64 = tc::sdesc_hi(64), H32v = tc::sdesc_hi(32);
         const uint32_t l0 = tc::sdesc_lo(tc::smem_u32(img + m.off_l));
         uint32_t gk = gk_seg;
         int v_tl = 0, v_pp = 0;
@@ -263,29 +311,48 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           for (int sk = 0; sk < 4; ++sk) {  // 16-wide k steps of the 64-wide panel
             const int j0 = 64 * v_pp + 16 * sk;
             if (j0 < n16) {
-              const int pp = 2 * v_pp + (sk >> 1), h = sk & 1;  // 32-wide L^-1 panel, its k step
-              const uint32_t R16 = (uint32_t)(nv16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
-              const uint32_t lp = l0 + (uint32_t)(pp * nv16 - 16 * pp * (pp - 1)) * 8u;
-              const uint32_t idn = tc::idesc_f16((uint32_t)(nv16 - j0));
               const uint32_t dt = tbase + 128u * vb + (uint32_t)j0;
               const uint32_t ka = kt + 8u * sk;       // k step sk: hi at +8 sk, lo at +32 + 8 sk
-              const uint32_t lb = lp + 66u * h;       // +1024 B rows, +32 B k-advance
-              tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | sk) ? 1u : 0u);
+              if constexpr (kPair) {
+                // k-step slab j0 / 16 of this CTA's half image: hi (N / 2 rows x 32 B), then lo
+                const uint32_t Nv = (uint32_t)(nv16 - j0);
+                const uint32_t lb = l0 + ((uint32_t)tc_pair_slab(nv16, j0 >> 4) >> 4);
+                const uint32_t idn = tc::idesc_f16_m256(Nv);
+                tc::mma2_f16_ts(dt, ka, lb, H32v, idn, (v_pp | sk) ? 1u : 0u);
+                tc::mma2_f16_ts(dt, ka, lb + Nv, H32v, idn, 1u);
+                tc::mma2_f16_ts(dt, ka + 32u, lb, H32v, idn, 1u);
+              } else {
+                const int pp = 2 * v_pp + (sk >> 1), h = sk & 1;  // 32-wide L^-1 panel, k step
+                const uint32_t R16 = (uint32_t)(nv16 - 32 * pp) * 4u;  // R * 64 B >> 4: hi -> lo
+                const uint32_t lp = l0 + (uint32_t)(pp * nv16 - 16 * pp * (pp - 1)) * 8u;
+                const uint32_t idn = tc::idesc_f16((uint32_t)(nv16 - j0));
+                const uint32_t lb = lp + 66u * h;       // +1024 B rows, +32 B k-advance
+                tc::mma_f16_ts(dt, ka, lb, H64, idn, (v_pp | sk) ? 1u : 0u);
 #ifndef GPBO_EXP_NOVMMA
-              tc::mma_f16_ts(dt, ka, lb + R16, H64, idn, 1u);
-              tc::mma_f16_ts(dt, ka + 32u, lb, H64, idn, 1u);
+                tc::mma_f16_ts(dt, ka, lb + R16, H64, idn, 1u);
+                tc::mma_f16_ts(dt, ka + 32u, lb, H64, idn, 1u);
 #endif
+              }
               if (lane == 0) trace_ev(p.trace, 20 + sk, 11, gk, trc);
             }
           }
-          tc::mma_commit_warp(bar(B_KE0 + ks));
-          // V columns [64 q, 64 q + 64) receive no later contribution: the drain may read them
-          tc::mma_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
+          // the K* stage is free; V columns [64 q, 64 q + 64) receive no later contribution (the
+          // drain may read them)
+          if (kPair) {
+            tc::mma2_commit_warp(bar(B_KE0 + ks));
+            tc::mma2_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
+          } else {
+            tc::mma_commit_warp(bar(B_KE0 + ks));
+            tc::mma_commit_warp(bar(B_VB0 + vbq * vb + v_pp));
+          }
           if (lane == 0) trace_ev(p.trace, 3, 11, gk, trc);
           ++gk;
           if (++v_pp == P64) {
             // the unused block barriers complete too: every B_VB completes once per tile
-            for (int q = P64; q < (int)vbq; ++q) tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
+            for (int q = P64; q < (int)vbq; ++q) {
+              if (kPair) tc::mma2_commit_warp(bar(B_VB0 + vbq * vb + q));
+              else tc::mma_commit_warp(bar(B_VB0 + vbq * vb + q));
+            }
             v_pp = 0;
             ++v_tl;
             if (vb) ++ve1; else ++ve0;
@@ -293,6 +360,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         }
       }
       __syncwarp();
+      }
     } else if (warp == kLoadW0 || warp == kLoadW0 + 1) {
       // ===================================================== candidate loader
       // Raw rows of tile t+1 are prefetched into the other staging buffer by one bulk copy
@@ -303,12 +371,13 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       const int stage_floats = ((128 * d_max * 4 + 127) & ~127) / 4;
       auto fetch = [&](int tl) {  // all 64 loader threads call it
         const uint32_t ti = gi + tl, sb = ti & 1u;
-        const int64_t row0 = (int64_t)(tile0 + tl) * 128;
-        const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);
-        const float *src = p.Xstar + p.x_off[s] + row0 * d;
+        const int64_t row0 = (int64_t)(tile0 + kTs * tl) * 128;
+        // (a pair tile's second half may lie past the search's rows: nothing to copy)
+        const int rows = (int)(Ms - row0 < 128 ? (Ms - row0 > 0 ? Ms - row0 : 0) : 128);
+        const float *src = p.Xstar + p.x_off[s] + (rows > 0 ? row0 * d : 0);
         float *dst = stage + sb * stage_floats;
         const uint32_t bytes = (uint32_t)(rows * d * 4);
-        if ((((uintptr_t)src) & 15u) == 0 && (bytes & 15u) == 0) {
+        if (rows > 0 && (((uintptr_t)src) & 15u) == 0 && (bytes & 15u) == 0) {
           if (lt == 0) {
             tc::mbar_arrive_expect_tx(bar(B_SF0 + sb), bytes);
             tc::bulk_g2s(tc::smem_u32(dst), src, bytes, bar(B_SF0 + sb));
@@ -322,13 +391,13 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       if (T > 0) fetch(0);
       for (int tl = 0; tl < T; ++tl) {
         const uint32_t ti = gi + tl, ab = ti & 1u, sb = ti & 1u;
-        const int64_t row0 = (int64_t)(tile0 + tl) * 128;
+        const int64_t row0 = (int64_t)(tile0 + kTs * tl) * 128;
         if (tl + 1 < T) fetch(tl + 1);
         if (lt == 0) trace_ev(p.trace, 9, 8, ti, trc);
         tc::mbar_wait(bar(B_SF0 + sb), (ti >> 1) & 1u);
         tc::mbar_wait(bar(B_AE0 + ab), ((ti >> 1) & 1u) ^ 1u);
         if (lt == 0) trace_ev(p.trace, 10, 8, ti, trc);
-        const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);
+        const int rows = (int)(Ms - row0 < 128 ? Ms - row0 : 128);  // (<= 0: all rows invalid)
         const float *stg = stage + sb * stage_floats;
         const uint32_t a0 = tc::smem_u32(Abuf) + ab * kb * 8192;
         for (int r = lt; r < 128; r += 64) {
@@ -388,7 +457,12 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         }
         tc::fence_proxy_async();
         tc::named_bar_sync(3, 64);  // staging buffer sb free, A tile complete
-        tc::mbar_arrive(bar(B_AF0 + ab));
+        if (kPair) {  // one arrival per CTA on the issuing CTA's barrier (release: the A tile's
+                      // shared-memory stores precede the MMA's reads)
+          if (lt == 0) tc::mbar_arrive_cluster(tc::mapa(bar(B_AF0 + ab), 0u));
+        } else {
+          tc::mbar_arrive(bar(B_AF0 + ab));
+        }
         if (lt == 0) trace_ev(p.trace, 11, 8, ti, trc);
       }
     } else if (warp >= kDrainW0 && warp < kDrainW0 + 4) {
@@ -462,7 +536,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_VE0 + vb));
+        if (lane == 0) arrive_leader(bar(B_VE0 + vb));
         if (trd) trace_ev(p.trace, 17, 9, ti, trc);
         if (!dbl || vb == 0) ++vb0c;
         if (!dbl || vb == 1) ++vb1c;
@@ -472,7 +546,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         if (trd) trace_ev(p.trace, 18, 9, ti, trc);
         const float2 ri = rowinfo[(ti & 7u) * 128 + row];
         const uint32_t flags = __float_as_uint(ri.y);
-        const int64_t rloc = (int64_t)(tile0 + tl) * 128 + row;
+        const int64_t rloc = (int64_t)(tile0 + kTs * tl) * 128 + row;
         const bool valid = (rloc < Ms) && !(flags & kFlagInvalid);
         const float u = 5.9604645e-8f;
         const float s2 = vv * vun2;
@@ -534,11 +608,12 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         } else {
           tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
+          if (trw) trace_ev(p.trace, 5, warp, gk, trc);
           tc::tc_fence_after();
           if (nv > 0) load_h();
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));  // the scratch stage is free
+          if (lane == 0) arrive_leader(bar(B_DE0 + st));  // the scratch stage is free
           ++ec;
           if (trw) trace_ev(p.trace, 6, warp, gk, trc);
           tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
@@ -594,9 +669,9 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar(B_KF0 + ks));
+        if (lane == 0) arrive_leader(bar(B_KF0 + ks));
         if (kMerged) {
-          if (lane == 0) tc::mbar_arrive(bar(B_DE0 + st));  // the scratch stage is free
+          if (lane == 0) arrive_leader(bar(B_DE0 + st));  // the scratch stage is free
           ++ec;
         }
         if (trw) trace_ev(p.trace, 8, warp, gk, trc);
@@ -610,7 +685,10 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     ta = tb;
   }
   tc::tc_fence_before();
-  __syncthreads();
+  // (pair: neither CTA leaves -- nor frees TMEM -- while the other may still arrive on its
+  // barriers or be read by the MMAs)
+  if (kPair) tc::cluster_sync();
+  else __syncthreads();
 #if defined(GPBO_TC_TRACE) || defined(GPBO_TC_CTATIME)  // per-CTA start / end (globaltimer, ns):
   // slice 5 of the trace buffer
   if (threadIdx.x == 0 && p.trace != nullptr && blockIdx.x < 8192) {
@@ -620,7 +698,10 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     p.trace[5 * 16384 + 2 * blockIdx.x + 1] = t1;
   }
 #endif
-  if (warp == kDistW) tc::tmem_dealloc(tbase, kTmemCols);
+  if (warp == kDistW) {
+    if (kPair) tc::tmem_dealloc2(tbase, kTmemCols);
+    else tc::tmem_dealloc(tbase, kTmemCols);
+  }
 }
 
 // ------------------------------------------------------------------ operand images (fit time)
@@ -655,6 +736,25 @@ static bool resident_fits(int n, int d) {
   return tc_smem(g.img, g.kb, d).total <= kMaxSmem;
 }
 
+// the CTA-pair kernel (default; GPBO_TC_PAIR=0 selects the one-CTA kernel for A/B runs)
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("GPBO_TC_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// (the pair pays off only for the single-buffered V accumulator, n16 + 16 > 128: measured at
+// config 2 fast phase 0.250 -> 0.244 ms, at config 3 -- two 64-wide panels per tile, double-
+// buffered V -- 2.62 -> 2.92 ms: there the cross-SM handoffs outweigh the halved MMA issues)
+bool tc_pair_fits(int n, int d) {
+  if (!pair_enabled() || !resident_fits(n, d)) return false;
+  const TcPairGeom g = tc_pair_geom(n, d);
+  if (g.n16 + kMeanRows <= 128) return false;
+  return tc_smem(g.half, g.kb, d).total <= kMaxSmem;
+}
+
 static bool stream_fits(int n, int d) {
   const TcsGeom g = tcs_geom(n, d);
   if (g.n16 > kTcsMaxN16 || d + 2 > 64) return false;
@@ -666,14 +766,26 @@ bool tcs_supported(const SearchMeta &m) { return m.tc_ok && m.tc_stream; }
 
 int64_t tc_image_bytes(const SearchMeta &m) {
   if (m.tc_stream) return stream_fits(m.n, m.d) ? tcs_geom(m.n, m.d).img : 0;
+  if (m.tc_pair) return 2 * (int64_t)tc_pair_geom(m.n, m.d).half;
   return resident_fits(m.n, m.d) ? tc_geom(m.n, m.d).img : 0;
 }
 
 // m.tc_stream on entry: 1 = streamed layout requested; it is also chosen when the resident
-// image does not fit.  (The caller makes the choice uniform over a model.)
+// image does not fit.  m.tc_pair on entry: 1 = CTA-pair layout requested (resident only).  (The
+// caller makes both choices uniform over a model.)
 void tc_fill_geometry(SearchMeta &m) {
   if (!resident_fits(m.n, m.d)) m.tc_stream = 1;
-  if (m.tc_stream) {
+  if (m.tc_stream || !tc_pair_fits(m.n, m.d)) m.tc_pair = 0;
+  if (m.tc_pair) {
+    const TcPairGeom g = tc_pair_geom(m.n, m.d);
+    m.n16 = g.n16;
+    m.kb = g.kb;
+    m.npan = (g.n16 + 31) / 32;
+    m.img_bytes = g.half;  // per CTA of the pair (the model holds two halves)
+    m.off_l = g.off_l;
+    m.off_a = g.off_w;  // (no alpha pairs: the mean is MMA-accumulated)
+    m.off_w = g.off_w;
+  } else if (m.tc_stream) {
     const TcsGeom g = tcs_geom(m.n, m.d);
     m.n16 = g.n16;
     m.kb = g.kb;
@@ -713,6 +825,7 @@ cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int 
                             cudaStream_t stream) {
   int img_max = 0, kb_max = 1, d_max = 1;
   bool merged = true;  // every search double-buffers V (n16 + 16 <= 128)
+  const bool pair = S > 0 && meta_h[0].tc_pair;  // (uniform over a model)
   for (int i = 0; i < S; ++i) {
     merged = merged && meta_h[i].n16 + kMeanRows <= 128;
     img_max = std::max(img_max, meta_h[i].img_bytes);
@@ -721,20 +834,28 @@ cudaError_t launch_score_tc(const ScoreLaunch &p, const SearchMeta *meta_h, int 
   }
   const int smem = tc_smem(img_max, kb_max, d_max).total;
   if (smem > kMaxSmem) return cudaErrorInvalidValue;
-  auto kern = merged ? score_tc_kernel<true> : score_tc_kernel<false>;
+  auto kern = pair ? (merged ? score_tc_kernel<true, true> : score_tc_kernel<false, true>)
+                   : (merged ? score_tc_kernel<true, false> : score_tc_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int grid = std::min(num_sms, total_tiles);
+  // pair: clusters of two CTAs (one per SM of a TPC), total_tiles even (the host pads each
+  // search to whole pair tiles)
+  const int grid = pair ? 2 * std::max(1, std::min(num_sms / 2, total_tiles / 2))
+                        : std::min(num_sms, total_tiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pair ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, p, tile_lo, total_tiles, img_max, kb_max, d_max);
 }
 

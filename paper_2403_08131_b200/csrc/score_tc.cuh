@@ -77,4 +77,6 @@ cudaError_t launch_score_tcs(const ScoreLaunch &p, const SearchMeta *meta_h, int
 int tcs_smem_bytes(int kb_max, int d_max);
 // true when the resident image of an (n, d) search does not fit in shared memory
 bool tc_needs_stream(int n, int d);
+// the CTA-pair resident layout (score_tc.cu kPair) covers an (n, d) search
+bool tc_pair_fits(int n, int d);
 }  // namespace gpbo

@@ -104,6 +104,7 @@ def load():
         "gpbo_last_bracket_violations": (i64, [vp]),
         "gpbo_debug_bound_scale": (C.c_int, [vp, C.c_float]),
         "gpbo_last_score_impl": (C.c_int, [vp]),
+        "gpbo_last_tc_pair": (C.c_int, [vp]),
         "gpbo_set_profiling": (C.c_int, [vp, C.c_int]),
         "gpbo_kernel_time": (C.c_int, [vp, C.c_int, vp, vp]),
         "gpbo_set_score_impl": (C.c_int, [vp, C.c_int]),
@@ -132,7 +133,7 @@ def exported_symbols():
             "gpbo_version", "gp_fit", "gp_fit_async", "gp_model_sync", "gp_model_free", "gp_model_lml", "gp_fit_append", "gpbo_last_append_refit", "gp_fit_ml2", "gpbo_last_ml2_evals", "gpbo_nm_selftest", "gpbo_influence", "gpbo_plan", "gp_model_stats", "gp_model_export",
             "gp_posterior", "ei_score_argmax", "gpbo_launch_count", "gpbo_collective_count", "gpbo_last_bracket_violations",
             "gpbo_debug_bound_scale", "gpbo_set_score_impl", "gpbo_last_refine_count", "gpbo_last_score_impl",
-            "gpbo_set_profiling", "gpbo_kernel_time",
+            "gpbo_last_tc_pair", "gpbo_set_profiling", "gpbo_kernel_time",
             "gpbo_debug_fast_phase", "gpbo_tc_selftest", "gpbo_debug_trace",
             "gpbo_tc_bench", "gpbo_space_create", "gpbo_space_free", "gpbo_space_dim",
             "gpbo_space_encode", "gpbo_space_sample", "bo_suggest_batch"]
@@ -294,6 +295,10 @@ class Context:
     @property
     def last_impl(self):
         return int(load().gpbo_last_score_impl(self.handle))
+
+    @property
+    def last_tc_pair(self):
+        return int(load().gpbo_last_tc_pair(self.handle))
 
     def debug_trace(self, buf):
         """buf: CUDA int64 tensor of >= 65536 entries, or None to disable."""

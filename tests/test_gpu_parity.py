@@ -169,6 +169,32 @@ def test_argmax_matches_oracle(G, name, make, impl):
         ctx.set_score_impl(0)
 
 
+@pytest.mark.parametrize("name,make", [
+    # every search n > 112: the CTA-pair kernel (n16 + 16 > 128); ragged sizes give odd tile
+    # counts (the pair tile's second half empty) and a 1-candidate search
+    ("pair_multi", lambda: gen.random_case(21, [130, 200, 113], [3, 20, 7], [1, 300, 4097])),
+    ("pair_cfg2", lambda: gen.make(2, M=65536 + 200)),
+], ids=["pair_multi", "pair_cfg2"])
+def test_pair_kernel_argmax_matches_oracle(G, name, make):
+    """The CTA-pair tcgen05 kernel (cta_group::2) against the oracle, with the pair asserted."""
+    gpbo, ctx = G
+    ctx.set_score_impl(2)
+    try:
+        w = make()
+        m = _fit(G, w)
+        Xs, off = H.pack_candidates(w)
+        idx, ei = ctx.score_argmax(m, Xs, off)
+        assert ctx.last_impl == 2 and ctx.last_tc_pair == 1
+        assert ctx.last_violations == 0
+        oms = H.oracle_fits(w)
+        for s in range(w.S):
+            res = gp.score(oms[s], w.Xstar[s])
+            H.check_argmax(res, int(idx[s]), f"{name}[{s}]")
+            assert abs(ei[s] / oms[s].std - res.ei) <= H.TOL * max(res.ei, 1e-30)
+    finally:
+        ctx.set_score_impl(0)
+
+
 def test_exact_tie_resolves_to_lowest_global_index(G):
     """R10 / S:L407: identical candidates tie bit-exactly; the lowest global index wins."""
     gpbo, ctx = G

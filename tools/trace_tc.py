@@ -31,7 +31,7 @@ n = len(ev)
 ev.sort()
 t0 = ev[0][0] if ev else 0
 names = {1: "mma:wait_kf", 2: "mma:kf_ok", 3: "mma:V_issued", 4: "mma:dist_issued",
-         5: "epi:wait_df", 6: "epi:df_ok", 7: "epi:ke_ok", 8: "epi:kf_arrive",
+         5: "epi:df_arrived", 6: "epi:df_ok", 7: "epi:ke_ok", 8: "epi:kf_arrive",
          9: "ld:wait", 10: "ld:go", 11: "ld:A_full", 12: "mma:wait_de", 13: "mma:de_ok",
          14: "mma:V_mmas_done", 15: "mma:V_start",
          16: "drn:start", 17: "drn:v_done", 18: "drn:pf_ok", 19: "drn:finished",
