@@ -174,27 +174,32 @@ __device__ __forceinline__ void pack_body(SearchMeta *meta_s, SearchMeta m, cons
   if (m.tc_pair) {
     const TcPairGeom pg = tc_pair_geom(n, d);
     const int nv16 = pg.n16 + kMeanRows;
-    for (int r = 0; r < 2; ++r) {
-      unsigned char *base = img + r * pg.half;
-      for (int idx = t0; idx < pg.nchunk * pg.kb * 32 * 16; idx += tstep) {
-        const int k = idx & 15, rr = (idx >> 4) & 31, cb = idx >> 9;  // cb = q kb + kblk
-        const int q = cb / pg.kb, kblk = cb - q * pg.kb;
-        const int h = min(64, pg.n16 - 64 * q) / 2;
-        const double v = rr < h ? xval(64 * q + r * h + rr, 16 * kblk + k) : 0.0;
-        unsigned char *hi = base + cb * 2048;
-        put(hi, hi + 1024, tc::sw_offset(rr, k * 2, 32), v);
-      }
-      for (int s = 0; s < pg.nks; ++s) {
-        const int h = (nv16 - 16 * s) / 2;
-        unsigned char *hi = base + pg.off_l + tc_pair_slab(nv16, s);
-        for (int idx = t0; idx < h * 16; idx += tstep) {
-          const int rr = idx >> 4, kk = idx & 15;
-          put_l(hi, hi + h * 32, tc::sw_offset(rr, kk * 2, 32), 16 * s + r * h + rr, 16 * s + kk);
-        }
-      }
-      float *wp = reinterpret_cast<float *>(base + pg.off_w);
-      for (int c = t0; c < GPBO_MAX_D; c += tstep)
-        wp[c] = c < d ? (float)(xs / (double)ls32[m.ls_off + c]) : 0.f;
+    // flat loops over both halves (every thread of the grid busy; per-slab loops left most of
+    // them idle and serialised 2 x nks short passes)
+    const int xe = pg.nchunk * pg.kb * 32 * 16;          // X elements per half
+    for (int idx = t0; idx < 2 * xe; idx += tstep) {
+      const int r = idx >= xe, e = idx - r * xe;
+      const int k = e & 15, rr = (e >> 4) & 31, cb = e >> 9;  // cb = q kb + kblk
+      const int q = cb / pg.kb, kblk = cb - q * pg.kb;
+      const int h = min(64, pg.n16 - 64 * q) / 2;
+      const double v = rr < h ? xval(64 * q + r * h + rr, 16 * kblk + k) : 0.0;
+      unsigned char *hi = img + r * pg.half + cb * 2048;
+      put(hi, hi + 1024, tc::sw_offset(rr, k * 2, 32), v);
+    }
+    const int le = tc_pair_slab(nv16, pg.nks) / 4;      // L elements per half (16 per row)
+    for (int idx = t0; idx < 2 * le; idx += tstep) {
+      const int r = idx >= le, e = idx - r * le;
+      int s = 0;
+      while (s + 1 < pg.nks && tc_pair_slab(nv16, s + 1) / 4 <= e) ++s;
+      const int h = (nv16 - 16 * s) / 2, o = e - tc_pair_slab(nv16, s) / 4;
+      const int rr = o >> 4, kk = o & 15;
+      unsigned char *hi = img + r * pg.half + pg.off_l + tc_pair_slab(nv16, s);
+      put_l(hi, hi + h * 32, tc::sw_offset(rr, kk * 2, 32), 16 * s + r * h + rr, 16 * s + kk);
+    }
+    for (int c = t0; c < 2 * GPBO_MAX_D; c += tstep) {
+      const int r = c >= GPBO_MAX_D, cc = c - r * GPBO_MAX_D;
+      float *wp = reinterpret_cast<float *>(img + r * pg.half + pg.off_w);
+      wp[cc] = cc < d ? (float)(xs / (double)ls32[m.ls_off + cc]) : 0.f;
     }
     return;
   }
