@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "score_common.cuh"
 #include "score_tc.cuh"
@@ -594,8 +595,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         const uint32_t ks = gk % kKStages;
         const uint32_t da = tl_addr + kScratch0 + 64u * st + (uint32_t)(kCW * part);
         uint32_t hr[kCW];
-        auto load_h = [&]() {
-          if constexpr (kCW == 32) tc::tmem_ld32(da, hr);
+        auto load_h = [&]() {  // (a 16-point remainder: only its 16 columns)
+          if (kCW == 32 && nv == 32) tc::tmem_ld32(da, hr);
           else tc::tmem_ld16(da, *reinterpret_cast<uint32_t(*)[16]>(hr));
           tc::tmem_wait_ld();
         };
@@ -620,43 +621,43 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           tc::tc_fence_after();  // the V MMAs that read this K* stage have completed
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         }
-        if (nv > 0) {
-          float kv[kCW];
+        // K* = k(h) for NE points, the float16 hi / lo split, and the stores of the NE / 16 k
+        // steps (the 16-point remainder of a ragged last panel evaluates and stores only its own
+        // 16 points: config 2 / 3 waste 7 / 12 % of the MUFU work otherwise)
+        auto eval = [&](auto ne_tag) {
+          constexpr int NE = decltype(ne_tag)::value;
+          float kv[NE];
 #ifdef GPBO_EXP_NOKSTAR  // timing experiment only: no kernel evaluation (wrong results)
           if (true) {
 #pragma unroll
-            for (int q = 0; q < kCW; ++q) kv[q] = __uint_as_float(hr[q]);
+            for (int q = 0; q < NE; ++q) kv[q] = __uint_as_float(hr[q]);
           } else
 #endif
           // |h| (a free source modifier) rather than max(h, 0): the GEMM-form h can be a few ulps
           // negative; |h| stays within the same error bound of the true h >= 0
           if (kind == GPBO_RBF) {
 #pragma unroll
-            for (int q = 0; q < kCW; ++q)
+            for (int q = 0; q < NE; ++q)
               kv[q] = ex2_approx(fmaf(fabsf(__uint_as_float(hr[q])), c1, c0));
           } else {
 #pragma unroll
-            for (int q = 0; q < kCW; ++q) {
+            for (int q = 0; q < NE; ++q) {
               const float tq = sqrt_approx(fabsf(__uint_as_float(hr[q])));
               kv[q] = fmaf(tq, fmaf(tq, c3, c2), c0) * ex2_approx(tq * c1);
             }
           }
-          if (nv < kCW) {  // points beyond n16: scratch columns the distance MMA did not write
+          uint32_t hw[NE / 2], lw[NE / 2];
 #pragma unroll
-            for (int q = 16; q < kCW; ++q) kv[q] = 0.f;
-          }
-          uint32_t hw[kCW / 2], lw[kCW / 2];
-#pragma unroll
-          for (int q = 0; q < kCW / 2; ++q) {
+          for (int q = 0; q < NE / 2; ++q) {
             const float h0 = __uint_as_float(__float_as_uint(kv[2 * q]) & 0xFFFFE000u);
             const float h1 = __uint_as_float(__float_as_uint(kv[2 * q + 1]) & 0xFFFFE000u);
             hw[q] = tc::pack_f16x2(h0, h1);
             lw[q] = tc::pack_f16x2(kv[2 * q] - h0, kv[2 * q + 1] - h1);
           }
-          // this warp's kCW k values are k steps (kCW / 16) part .. of the panel: hi at +8 per
-          // k step, lo at +32
+          // this warp's k values are k steps (kCW / 16) part .. of the panel: hi at +8 per k
+          // step, lo at +32
           const uint32_t kt = tl_addr + kKstar0 + 64u * ks + (uint32_t)(kCW / 2 * part);
-          if constexpr (kCW == 32) {
+          if constexpr (NE == 32) {
             tc::tmem_st16(kt, *reinterpret_cast<const uint32_t(*)[16]>(hw));
             tc::tmem_st16(kt + 32u, *reinterpret_cast<const uint32_t(*)[16]>(lw));
           } else {
@@ -666,6 +667,10 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
 #ifndef GPBO_EXP_NOWAITST  // timing experiment only (races with the MMA)
           tc::tmem_wait_st();
 #endif
+        };
+        if (nv > 0) {
+          if (kCW == 32 && nv == 32) eval(std::integral_constant<int, kCW>());
+          else eval(std::integral_constant<int, 16>());
         }
         tc::tc_fence_before();
         __syncwarp();
