@@ -369,81 +369,212 @@ direct_kernel(const RefineLaunch p, int S, int64_t rows) {
   }
 }
 
-// gp_posterior's dense path: every row of search dense_s in float64 (the refine's arithmetic:
-// direct differences of x / l, the float64 kernel, mu~ = k*^T alpha, v = L^-1 k*, tau), but
-// candidate-TILED: a CTA scores kPostTile candidates together, so each row of L^-1 is read once
-// per tile (a broadcast load shared by the tile's lanes) instead of once per candidate -- the
-// per-candidate refine streams n^2 / 2 float64 per candidate from L2 (56x the argmax path's time
-// at config 2).  Thread (c, g): candidate c of the tile, rows j = g (mod groups) of v.
+// gp_posterior's dense path: every row of search dense_s in float64 (the refine's arithmetic up
+// to summation order: the float64 kernel, mu~ = k*^T alpha, s2~ = sf2 - |L^-1 k*|^2, tau), on the
+// FP64 tensor cores, kPostTile = 32 candidates per CTA iteration:
+//   1. x* / l of the tile and q* = |x* / l|^2 into shared memory;
+//   2. K* from GEMM-form squared distances r^2 = q* + q - 2 (x* / l) . (x / l) on DMMA m8n8k4
+//      (float64: the form's cancellation error ~ u q is ~1e-15 sf2 in k*, far inside T1, whose
+//      variance term is relative to sf2 -- tests/helpers.py check_T1), clamped at 0; the kernel
+//      in float64 on the fragments; K*^T into shared memory and the mean partials k* alpha;
+//   3. V^T = L^-1 K*^T on DMMA: 8-row blocks J of L^-1 (2J + 2 k-steps of 4 each) dealt to the
+//      warps by longest-processing-time (deterministic, near-equal k-step totals); A fragments
+//      straight from L2 (row-major L^-1, lower part; four k-steps of loads in flight), B
+//      fragments from the K*^T tile, four 8-candidate accumulators; |v|^2 accumulates per
+//      candidate as each row block completes (V is never stored);
+//   4. fixed-order reductions (deterministic), EI, raw outputs.
+// Per candidate ~2 n d + n (n + 8) tensor flops plus the n kernel evaluations -- the
+// per-candidate refine streams n^2 / 2 float64 of L^-1 per candidate instead.
 constexpr int kPostTile = 32;
+#ifndef GPBO_POST_PF
+#define GPBO_POST_PF 8      // distance-stage B fragments in flight (k-steps of 4 dims)
+#endif
+#ifndef GPBO_POST_MINB
+#define GPBO_POST_MINB 3    // resident CTAs per SM the 8-warp variant is compiled for
+#endif
+#ifndef GPBO_POST_PF8
+#define GPBO_POST_PF8 4     // the same for the 8-warp variant
+#endif
+#ifndef GPBO_POST_ACC8
+#define GPBO_POST_ACC8 1    // V accumulator sets (k-step parity) of the 8-warp variant (16 warps: 2)
+#endif
+#ifndef GPBO_POST_WSMALL
+#define GPBO_POST_WSMALL 8  // warps per CTA for n <= 256
+#endif
+constexpr int kPostLd = kPostTile + 4;  // K*^T row stride (doubles): conflict-free B fragments
 
-// groups per tile = blockDim.x / 32 (8, 16 or 32: more row groups for larger n)
-__global__ void __launch_bounds__(1024)
-posterior64_kernel(const RefineLaunch p, int nmax, int dmax) {
-  const int kPostGroups = blockDim.x / kPostTile;
+__device__ __forceinline__ void dmma64(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// kPostWarps: 8 (up to 3 CTAs per SM) or 16 when the K*^T tile limits the SM to one CTA (n > 256)
+template <int kPostWarps>
+__global__ void __launch_bounds__(32 * kPostWarps, kPostWarps == 8 ? GPBO_POST_MINB : 1)
+posterior64_kernel(const RefineLaunch p, int dmax) {
+  constexpr int kPostThreads = 32 * kPostWarps;
+  constexpr int kGroups = kPostWarps / 4;  // point-block groups of the distance stage
+  constexpr int kPF = kPostWarps == 8 ? GPBO_POST_PF8 : GPBO_POST_PF;
+  constexpr int kAcc = kPostWarps == 8 ? GPBO_POST_ACC8 : 2;
   extern __shared__ __align__(16) double psm[];
-  double *ks = psm;                                  // [n][kPostTile]  k*(c, j) at j * 32 + c
-  double *xs = ks + (size_t)nmax * kPostTile;        // [kPostTile][dmax] x* / l
-  double *red = xs + (size_t)kPostTile * dmax;       // [kPostGroups][kPostTile] x 2
-  const int tid = threadIdx.x, c = tid % kPostTile, g = tid / kPostTile;
   const int s = p.dense_s;
   const SearchMeta &m = p.meta[s];
-  const int n = m.n, d = m.d;
+  const int n = m.n, d = m.d, nt = (n + 7) / 8, n8 = 8 * nt, d4 = (d + 3) / 4 * 4;
+  const int xld = (dmax + 3) / 4 * 4 + 1;
+  double *ks = psm;                                  // [n8][kPostLd]: K*^T(j, c)
+  double *xs = ks + (size_t)n8 * kPostLd;            // [kPostTile][xld]: x* / l (0 beyond d)
+  double *qj = xs + (size_t)kPostTile * xld;         // [n8]: |x_j / l|^2
+  double *qc = qj + n8;                              // [kPostTile]: |x* / l|^2
+  double *red = qc + kPostTile;                      // [2][kPostWarps][kPostTile]
+  int *owner = reinterpret_cast<int *>(red + 2 * kPostWarps * kPostTile);  // [nt]: warp of J
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
   const double *Xj = p.Xs64 + m.x_off;      // column-major d x n
   const double *alpha = p.alpha64 + m.a_off;
   const double *Li = p.Linv64 + m.mat_off;  // row-major, lower part
   const float *ls = p.ls32 + m.ls_off;
   const double sf2 = (double)m.sf2;
+  const double best = resolve_best(p.best[s], m);
+  // per-CTA setup: q_j, and the row-block -> warp deal (longest first to the least loaded)
+  for (int j = tid; j < n8; j += kPostThreads) {
+    double q = 0.0;
+    if (j < n)
+      for (int dim = 0; dim < d; ++dim) { const double v = Xj[(size_t)dim * n + j]; q = fma(v, v, q); }
+    qj[j] = q;
+  }
+  if (tid == 0) {
+    int load[kPostWarps];
+    for (int q = 0; q < kPostWarps; ++q) load[q] = 0;
+    for (int J = nt - 1; J >= 0; --J) {
+      int w = 0;
+      for (int q = 1; q < kPostWarps; ++q) w = load[q] < load[w] ? q : w;
+      owner[J] = w;
+      load[w] += 2 * J + 2;
+    }
+  }
   const int64_t ntile = (p.dense_rows + kPostTile - 1) / kPostTile;
   for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
     const int64_t row0 = t * kPostTile;
     const int cnt = (int)min((int64_t)kPostTile, p.dense_rows - row0);
-    __syncthreads();  // the previous tile is done with ks / xs / red
-    for (int e = tid; e < kPostTile * d; e += blockDim.x) {
-      const int cc = e / d, dim = e - cc * d;
-      xs[cc * dmax + dim] =
-          cc < cnt ? (double)p.Xstar[p.x_off[s] + (row0 + cc) * d + dim] / (double)ls[dim] : 0.0;
+    __syncthreads();  // the previous tile is done with ks / xs / red (and the setup is visible)
+    for (int e = tid; e < kPostTile * d4; e += kPostThreads) {
+      const int cc = e / d4, dim = e - cc * d4;
+      xs[cc * xld + dim] = cc < cnt && dim < d
+          ? (double)p.Xstar[p.x_off[s] + (row0 + cc) * d + dim] / (double)ls[dim] : 0.0;
     }
     __syncthreads();
-    double mu = 0.0;
-    for (int j = g; j < n; j += kPostGroups) {  // k* and the mean partials
-      double r2 = 0.0;
-      for (int dim = 0; dim < d; ++dim) {
-        const double t2 = xs[c * dmax + dim] - Xj[(size_t)dim * n + j];
-        r2 = fma(t2, t2, r2);
+    if (tid < kPostTile) {
+      double q = 0.0;
+      for (int dim = 0; dim < d; ++dim) q = fma(xs[tid * xld + dim], xs[tid * xld + dim], q);
+      qc[tid] = q;
+    }
+    __syncthreads();
+    // 2. K* on DMMA: warp w -> candidate block cb = w & 3, point blocks J = (w >> 2) mod kGroups
+    {
+      const int cb = warp & 3;
+      const double *xa = xs + (8 * cb + gid) * xld + tig;
+      const double qa = qc[8 * cb + gid];
+      double mu = 0.0;  // candidate 8 cb + gid, points 2 tig + {0, 1} of this warp's blocks
+      for (int J = warp >> 2; J < nt; J += kGroups) {
+        const int jb = 8 * J + gid;  // B column (point) of this lane's fragment loads
+        const double *xb = Xj + min(jb, n - 1);
+        // GPBO_POST_PF k-steps' B fragments in flight at once, then their DMMAs
+        double d0 = 0.0, d1 = 0.0;
+        for (int kb = 0; kb < d4; kb += 4 * kPF) {
+          double bv[kPF];
+#pragma unroll
+          for (int u = 0; u < kPF; ++u) {
+            const int dim = kb + 4 * u + tig;
+            bv[u] = dim < d ? __ldg(xb + (size_t)dim * n) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kPF; ++u)
+            if (kb + 4 * u < d4) dmma64(d0, d1, xa[kb + 4 * u], bv[u]);
+        }
+        const int j0 = 8 * J + 2 * tig;
+        double k0v = 0.0, k1v = 0.0;
+        if (j0 < n) {
+          k0v = kernel64(fmax(qa + qj[j0] - 2.0 * d0, 0.0), sf2, m.kernel);
+          mu = fma(k0v, __ldg(alpha + j0), mu);
+        }
+        if (j0 + 1 < n) {
+          k1v = kernel64(fmax(qa + qj[j0 + 1] - 2.0 * d1, 0.0), sf2, m.kernel);
+          mu = fma(k1v, __ldg(alpha + j0 + 1), mu);
+        }
+        ks[j0 * kPostLd + 8 * cb + gid] = k0v;
+        ks[(j0 + 1) * kPostLd + 8 * cb + gid] = k1v;
       }
-      const double k = kernel64(r2, sf2, m.kernel);
-      ks[j * kPostTile + c] = k;
-      mu = fma(k, alpha[j], mu);
+      mu += __shfl_xor_sync(0xffffffffu, mu, 1);
+      mu += __shfl_xor_sync(0xffffffffu, mu, 2);
+      if (tig == 0) red[(warp >> 2) * kPostTile + 8 * cb + gid] = mu;  // [kGroups][kPostTile]
     }
     __syncthreads();  // ks complete
-    double vv = 0.0;
-    for (int j = g; j < n; j += kPostGroups) {  // v_j = sum_{k <= j} L^-1_jk k*_k
-      const double *row = Li + (size_t)j * n;
-      double a0 = 0.0, a1 = 0.0;
-      int k = 0;
-      for (; k + 1 <= j; k += 2) {
-        a0 = fma(row[k], ks[k * kPostTile + c], a0);
-        a1 = fma(row[k + 1], ks[(k + 1) * kPostTile + c], a1);
+    // 3. v = L^-1 k* on DMMA, |v|^2 per candidate
+    double vv[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int J = nt - 1; J >= 0; --J) {
+      if (owner[J] != warp) continue;
+      const int j = 8 * J + gid;
+      const double *Lrow = Li + (size_t)min(j, n - 1) * n;
+      const int nks = 2 * J + 2;  // k-steps of 4 covering k < 8 J + 8
+      // kAcc accumulator sets (k-step parity): 4 kAcc independent DMMA chains per warp
+      double acc[kAcc][4][2] = {};
+      double an[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * u + tig;
+        an[u] = (u < nks && k <= j && j < n) ? __ldg(Lrow + k) : 0.0;
       }
-      if (k == j) a0 = fma(row[k], ks[k * kPostTile + c], a0);
-      const double v = a0 + a1;
-      vv = fma(v, v, vv);
+      for (int k0 = 0; k0 < nks; k0 += 4) {
+        double ac[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ac[u] = an[u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = k0 + 4 + u, k = 4 * kk + tig;
+          an[u] = (kk < nks && k <= j && j < n) ? __ldg(Lrow + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = k0 + u;
+          if (kk < nks) {
+            const double *brow = ks + (4 * kk + tig) * kPostLd + gid;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dmma64(acc[u % kAcc][q][0], acc[u % kAcc][q][1], ac[u], brow[8 * q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double v0 = acc[0][q][0], v1 = acc[0][q][1];
+#pragma unroll
+        for (int h = 1; h < kAcc; ++h) { v0 += acc[h][q][0]; v1 += acc[h][q][1]; }
+        vv[q][0] = fma(v0, v0, vv[q][0]);
+        vv[q][1] = fma(v1, v1, vv[q][1]);
+      }
     }
-    red[g * kPostTile + c] = mu;
-    red[(kPostGroups + g) * kPostTile + c] = vv;
-    __syncthreads();
-    if (g == 0 && c < cnt) {
-      double mu_s = 0.0, vv_s = 0.0;
-      for (int q = 0; q < kPostGroups; ++q) {  // fixed order: deterministic
-        mu_s += red[q * kPostTile + c];
-        vv_s += red[(kPostGroups + q) * kPostTile + c];
+    // rows gid -> one partial per (warp, candidate 8 q + 2 tig + h), fixed shuffle order
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = vv[q][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (gid == 0) red[(kPostWarps + warp) * kPostTile + 8 * q + 2 * tig + h] = v;
       }
+    __syncthreads();
+    if (tid < cnt) {
+      const int c = tid;
+      double mu_s = 0.0, vv_s = 0.0;
+      for (int q = 0; q < kGroups; ++q) mu_s += red[q * kPostTile + c];
+      for (int q = 0; q < kPostWarps; ++q) vv_s += red[(kPostWarps + q) * kPostTile + c];
       const int64_t e = row0 + c;
       const bool fin = isfinite(mu_s) && isfinite(vv_s);  // NaN rows: NaN outputs
       const double var64 = fmax(sf2 - vv_s, 0.0);
       const double sig = sqrt(var64);
-      const double imp = resolve_best(p.best[s], m) - mu_s;
+      const double imp = best - mu_s;
       const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
       if (p.out_mu) p.out_mu[e] = fin ? (float)(m.mean + m.std * mu_s) : NAN;
       if (p.out_var) p.out_var[e] = fin ? (float)(m.std * m.std * var64) : NAN;
@@ -454,21 +585,31 @@ posterior64_kernel(const RefineLaunch p, int nmax, int dmax) {
 
 }  // namespace
 
-cudaError_t launch_posterior64(const RefineLaunch &p, int nmax, int dmax, int num_sms,
+template <int W>
+static cudaError_t launch_post(const RefineLaunch &p, int n8, int dmax, int num_sms,
                                cudaStream_t stream) {
-  if (p.dense_rows <= 0) return cudaSuccess;
-  const int groups = nmax <= 128 ? 8 : nmax <= 256 ? 16 : 32;
-  const size_t smem = ((size_t)nmax * kPostTile + (size_t)kPostTile * dmax +
-                       2 * groups * kPostTile) * sizeof(double);
+  const int xld = (dmax + 3) / 4 * 4 + 1;
+  const size_t smem = ((size_t)n8 * kPostLd + (size_t)kPostTile * xld + n8 + kPostTile +
+                       2 * W * kPostTile) * sizeof(double) + (size_t)(n8 / 8) * sizeof(int);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(posterior64_kernel,
+    cudaError_t e = cudaFuncSetAttribute(posterior64_kernel<W>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, posterior64_kernel<W>, 32 * W, smem);
   const int64_t tiles = (p.dense_rows + kPostTile - 1) / kPostTile;
-  const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms * 8);
-  posterior64_kernel<<<grid, kPostTile * groups, smem, stream>>>(p, nmax, dmax);
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms * std::max(per_sm, 1));
+  posterior64_kernel<W><<<grid, 32 * W, smem, stream>>>(p, dmax);
   return cudaGetLastError();
+}
+
+cudaError_t launch_posterior64(const RefineLaunch &p, int nmax, int dmax, int num_sms,
+                               cudaStream_t stream) {
+  if (p.dense_rows <= 0) return cudaSuccess;
+  const int n8 = (nmax + 7) / 8 * 8;
+  return n8 > 256 ? launch_post<16>(p, n8, dmax, num_sms, stream)
+                  : launch_post<GPBO_POST_WSMALL>(p, n8, dmax, num_sms, stream);
 }
 
 cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sms, int nmax,
