@@ -41,6 +41,9 @@ constexpr int kWarps = kFitThreads / 32;
 #define GPBO_FIT_QW 4
 #endif
 constexpr int kQ = GPBO_FIT_QW;  // tiles of one tile row per trailing-update work item (<= kQ)
+#ifndef GPBO_FIT_STATIC
+#define GPBO_FIT_STATIC 1  // T work list: static 4-aligned quads (1) or per-row items (0)
+#endif
 static_assert(kFitB == 8, "the DMMA tiling of fit.cu assumes 8-step panels");
 
 #ifdef GPBO_FIT_TIMING  // phase clocks of CTA 0 printed at exit (tools/fit_phases.py)
@@ -293,6 +296,19 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   int jk = -1;
   double jit = 0.0;
   double p10 = 1.0;
+#if GPBO_FIT_STATIC
+  // the trailing update's quad list: (R, Q) for rows R = nt - 1 .. 1, Q = 0 .. R / kQ;
+  // qabove[J] = number of quads of rows > J
+  __shared__ int qtab[(kFitSmemMaxN / 8) * (kFitSmemMaxN / 8 / kQ + 1)];
+  __shared__ int qabove[kFitSmemMaxN / 8 + 1];
+  if (kSmem && tid == 0) {
+    int k = 0;
+    for (int R = nt - 1; R >= 1; --R) {
+      for (int Q = 0; Q <= R / kQ; ++Q) qtab[k++] = R << 8 | Q;
+      qabove[R - 1] = k;
+    }
+  }
+#endif
   FIT_T(0);
   for (int k = 0; k < 7 && jk < 0; ++k, p10 *= 10.0) {
     jit = 1e-8 * p10 * sf2;
@@ -405,6 +421,45 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
       for (int q = 0; q < kQ; ++q)
         if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
     };
+    // quad() for one G buffer and a full quad (kQ tiles): no per-tile predicates (a predicated
+    // mma.sync costs a WARPSYNC + NOP pair per DMMA) and one base address per operand stream
+    // (the predicated form rematerialised every address: ~3x the instructions per tile)
+    auto quad_full = [&](const double *__restrict__ Ga, int R, int C0) {
+      double *Wt = W + tb(R, C0) + 2 * lane;
+      const double *ga = Ga + tig * gs + 8 * R + gid;
+      const double *gb = Ga + tig * gs + 8 * C0 + gid;
+      double2 c[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
+      const double a0 = -ga[0], a1 = -ga[4 * gs];
+      double b0[kQ], b1[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) { b0[q] = gb[8 * q]; b1[q] = gb[4 * gs + 8 * q]; }
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) dmma(c[q].x, c[q].y, a0, b0[q]);
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) dmma(c[q].x, c[q].y, a1, b1[q]);
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
+    };
+    // quad() over the tiles of a 4-aligned quad selected by `mask` (one G buffer)
+    auto quad_mask = [&](const double *Ga, int R, int C0, unsigned mask) {
+      double *Wt = W + tb(R, C0) + 2 * lane;
+      const double *ga = Ga + tig * gs + 8 * R + gid;
+      const double *gb = Ga + tig * gs + 8 * C0 + gid;
+      double2 c[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        if (mask >> q & 1) c[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
+      const double a0 = -ga[0], a1 = -ga[4 * gs];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        if (mask >> q & 1) {
+          dmma(c[q].x, c[q].y, a0, gb[8 * q]);
+          dmma(c[q].x, c[q].y, a1, gb[4 * gs + 8 * q]);
+          *reinterpret_cast<double2 *>(Wt + 64 * q) = c[q];
+        }
+    };
     constexpr int kT = kWarps - 1;  // T warps (the highest warp is the D warp)
     // The working matrix in shared memory: one panel per step, the trailing update overlapping
     // the next block's D (D's latency is hidden behind a full T pass; measured faster than
@@ -420,19 +475,42 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
         __syncwarp();
         diag_block(8 * (JT + 1));
       } else {
+#if GPBO_FIT_STATIC
+        // 4-aligned quads (R, Q) of the rows below the panel, rows descending (qtab): the quads
+        // of rows > JT are the first qabove[JT] entries, dealt round robin; a quad's tiles at
+        // the panel column JT, past the diagonal, or on the D warp's diagonal tile are masked
+        const int nq = qabove[JT];
+        for (int k = warp; k < nq; k += kT) {
+          const int v = qtab[k], R = v >> 8, C0 = kQ * (v & 255);
+          unsigned mask = 0;
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            const int C = C0 + q;
+            mask |= (C <= R && C != JT && !(R == JT + 1 && C == R)) ? 1u << q : 0u;
+          }
+          if (mask == (1u << kQ) - 1) quad_full(G1, R, C0);
+          else if (mask) quad_mask(G1, R, C0, mask);
+        }
+#else
         // items of tile row r (R = JT + 1 + r): nlq left quads, then r / 4 + 1 right quads
         // (row 0's right quad is the diagonal tile -- the D warp's), round robin, rotated
         for (int r = 0, w0 = 0; r < nrt; ++r, w0 = (w0 + 5) % kT) {
           const int R = JT + 1 + r, len = nlq + (r > 0 ? r / kQ + 1 : 0);
           for (int q = (warp - w0 + kT) % kT; q < len; q += kT) {
+            int C0, cnt;
             if (q < nlq) {
-              quad(G1, nullptr, R, kQ * q, min(kQ, JT - kQ * q));
+              C0 = kQ * q;
+              cnt = min(kQ, JT - kQ * q);
             } else {
               const int c0 = kQ * (q - nlq);
-              quad(G1, nullptr, R, JT + 1 + c0, min(kQ, r + 1 - c0));
+              C0 = JT + 1 + c0;
+              cnt = min(kQ, r + 1 - c0);
             }
+            if (cnt == kQ) quad_full(G1, R, C0);
+            else quad(G1, nullptr, R, C0, cnt);
           }
         }
+#endif
       }
       __syncthreads();
       FIT_T(4);

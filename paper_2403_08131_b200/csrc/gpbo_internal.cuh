@@ -22,8 +22,14 @@ constexpr int kFitB = 8;
 constexpr int kFitSmemMaxN = 216;
 constexpr int kFitSmemBudget = 227 * 1024 - 512;  // dynamic shared memory of the fit kernel
 __host__ __device__ constexpr int fit_nr8(int n) { return (n + 7) & ~7; }
-// G row stride: = 8 (mod 16) doubles, so DMMA fragment loads of 4 rows hit distinct banks
-__host__ __device__ constexpr int fit_gstride(int n) { return ((n + 15) & ~15) + 8; }
+// G row stride (doubles) = GPBO_GS_MOD (mod 16).  A DMMA fragment load of G reads rows tig = 0..3
+// at columns gid; 64-bit loads are served per half-warp (lanes 4 gid + tig, gid < 4), so the
+// rows must land in distinct 4-double bank groups: 4 (mod 16) does that, 8 (mod 16) pairs rows
+// 0 / 2 and 1 / 3 on the same banks (2-way conflicts)
+#ifndef GPBO_GS_MOD
+#define GPBO_GS_MOD 4
+#endif
+__host__ __device__ constexpr int fit_gstride(int n) { return ((n + 15) & ~15) + GPBO_GS_MOD; }
 __host__ __device__ constexpr int fit_tile_doubles(int n) {
   return ((n + 7) / 8) * ((n + 7) / 8 + 1) / 2 * 64;
 }
