@@ -431,9 +431,34 @@ def main():
     _, _, kt, _ = timed(step_device, args.steps, args.warmup, profile=True)
     # ---- end-to-end through the C ABI with host buffers
     T_e2e, _, _, _ = timed(step_host, args.steps, args.warmup)
+    # ---- end to end through bo_suggest_batch (the BO user's call): per step the observations
+    # (host) go in, the suggestion comes out; the M candidates of each search are drawn on the
+    # device from the search's parameter box (d REAL parameters in [0, 1], the workload's
+    # uniform candidates; H5) -- no candidate crosses PCIe
+    T_sug = None
+    if world == 1 and args.layout == "uniform":
+        spaces = [gpbo.Space(ctx, [{"kind": 0, "lo": 0.0, "hi": 1.0}] * dd) for dd in d]
+        Msug = np.diff(m_off).astype(np.int64)
+        it_ctr = [0]
+
+        def step_suggest():
+            m = ctx.fit(n, d, Xh, yh, lsh, sf2h, sn2h, kernel=w.kernel, wait=False)
+            it_ctr[0] += 1
+            out = gpbo.suggest(ctx, m, spaces, Msug, 1234, it_ctr[0], dedup=True)
+            m.free()
+            return out
+
+        T_sug, _, _, _ = timed(step_suggest, args.steps, args.warmup)
+        del spaces
     # ---- score-only (model resident, fit outside the timed region): H6-H10 alone
     m_res = ctx.fit(n, d, Xd, yd, lsd, sf2d, sn2d, kernel=w.kernel)
     T_score, _, _, _ = timed(lambda: step_score(m_res), args.steps, args.warmup)
+    # ---- gp_posterior (H6-H8 raw mu / var / EI of every candidate, float64 on DMMA) of search 0
+    T_post, M_post = None, 0
+    if world == 1:
+        M_post = int(m_off[1])
+        Xs0 = Xsd[: M_post * d[0]].view(M_post, d[0])
+        T_post, _, _, _ = timed(lambda: ctx.posterior(m_res, 0, Xs0), args.steps, args.warmup)
     m_res.free()
 
     def vmax(x):
@@ -473,7 +498,13 @@ def main():
             tr = profiled_traffic("score_tcs" if impl_used == "tcgen05-stream" else "score_tc",
                                   args.config)
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": tr[0] if tr else None,
+                    "frac": achieved / peak,
+                    "fp16x3_ceiling": {"peak": peak / 3, "frac": achieved / (peak / 3),
+                                       "why": "every contraction runs as 3 fp16 MMAs (hi.hi + "
+                                              "hi.lo + lo.hi: float32-level products for the "
+                                              "1e-4 parity), so the algorithmic flops can reach "
+                                              "at most 1/3 of the fp16 peak"},
+                    "traffic": tr[0] if tr else None,
                     "traffic_src": tr[1] if tr else None,
                     "algorithmic_bytes": int(sum(4 * dd * x.shape[0] for dd, x in zip(d, w.Xstar))),
                     "peak_src": f"{peaks['src']} bf16 dense "
@@ -539,6 +570,23 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
+            "e2e_suggest": None if T_sug is None else {
+                "value": total_cands / (T_sug / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes + lsh.nbytes + sf2h.nbytes +
+                                          sn2h.nbytes),
+                "d2h_bytes_per_step": int(8 * S + 4 * S + 8 * sum(d)),
+                "what": "gp_fit (host observations) + bo_suggest_batch (candidates drawn on the "
+                        "device from the parameter box, H5) -> suggestion read back"},
+            "posterior": None if T_post is None else {
+                "value": M_post * args.steps / (T_post / 1e3), "unit": UNIT,
+                "ms_per_call": T_post / args.steps, "candidates": M_post,
+                "what": "gp_posterior of search 0 on a resident model: raw mu, var, EI of every "
+                        "candidate in float64 (K* and V = L^-1 K*^T on the FP64 tensor cores)",
+                "roofline": {"bound": "tensor-fp64",
+                             "achieved": (n[0] * (n[0] + 1) + 2 * n[0] * d[0] + 2 * n[0]) *
+                                         M_post * args.steps / (T_post / 1e3) / 1e12,
+                             "peak": 45.0, "unit": "TFLOP/s",
+                             "peak_src": "B200 FP64 tensor nominal (blackwell_cuda_programming.md)"}},
             "score_only": {"value": score_value, "unit": UNIT,
                            "ms_per_step": T_score / args.steps,
                            "what": "ei_score_argmax alone on a resident model (H6-H10)"},
@@ -552,6 +600,9 @@ def main():
             "oracle_check": oracle_check,
             "collectives": ctx.collectives,
         }
+        if line["posterior"]:
+            pr = line["posterior"]["roofline"]
+            pr["frac"] = pr["achieved"] / pr["peak"]
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

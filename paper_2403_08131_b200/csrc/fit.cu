@@ -354,16 +354,25 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
     auto cphase = [&](int JT, double *Gc) {
       const int J = 8 * JT, bb = min(kFitB, n - J);
       const int nrt = nt - JT - 1;
+      // the maps' fragments are the same for every item of the panel: loaded once
+      double nf[2], mf[2], rf[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kk = 4 * h;
+        nf[h] = Nm[(kk + tig) * 8 + gid];
+        mf[h] = Mm[(kk + tig) * 8 + gid];
+        rf[h] = Rm[gid * 8 + kk + tig];
+      }
       for (int it = warp; it < nrt + JT; it += kWarps) {
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
         if (it < nrt) {
           const int R = JT + 1 + it, i = 8 * R + gid;
           double *Wt = W + tb(R, JT);
 #pragma unroll
-          for (int kk = 0; kk < 8; kk += 4) {
-            const double a = Wt[8 * gid + kk + tig];
-            dmma(d0, d1, a, Nm[(kk + tig) * 8 + gid]);
-            dmma(e0, e1, a, Mm[(kk + tig) * 8 + gid]);
+          for (int h = 0; h < 2; ++h) {
+            const double a = Wt[8 * gid + 4 * h + tig];
+            dmma(d0, d1, a, nf[h]);
+            dmma(e0, e1, a, mf[h]);
           }
           const int u = 2 * tig;
           Gc[u * gs + i] = d0;
@@ -378,10 +387,10 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
           const int C = it - nrt;
           double *Wt = W + tb(JT, C);
 #pragma unroll
-          for (int kk = 0; kk < 8; kk += 4) {
-            const int mrow = kk + tig;
+          for (int h = 0; h < 2; ++h) {
+            const int mrow = 4 * h + tig;
             const double b = mrow < bb ? Wt[8 * mrow + gid] : 0.0;
-            dmma(d0, d1, Rm[gid * 8 + mrow], b);
+            dmma(d0, d1, rf[h], b);
           }
           const int kc = 8 * C + 2 * tig;
           Gc[gid * gs + kc] = d0;

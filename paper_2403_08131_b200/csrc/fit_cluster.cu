@@ -91,8 +91,8 @@ __host__ __device__ __forceinline__ int own_rowoff(int lr, int c, int Cc) {
 }
 
 // shared-memory plan (doubles): yt | w | flags (24) | maps M N R (192) | L11 stash (64) |
-// GT (2 x 9 nr8) | W (own tiles).  The GT area is reused by CTA 0 in the tail for the Cc partial
-// alpha vectors (Cc x nr8 <= 18 nr8).
+// GT (2 x 8 nr8) | W (own tiles).  The GT area is reused by CTA 0 in the tail for the Cc partial
+// alpha vectors (Cc x nr8 <= 16 nr8).
 __host__ __device__ __forceinline__ int own_tiles(int nt, int c, int Cc) {
   const int rows = c < nt ? (nt - 1 - c) / Cc + 1 : 0;
   return own_rowoff(rows, c, Cc);
@@ -120,11 +120,13 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   double *Nm = Mm + 64;
   double *Rm = Nm + 64;
   double *l11s = Rm + 64;         // L11 of the latest D, written to global memory later
-  // the panel's G transposed, double-buffered by panel parity: GT[b][i * 9 + u] (row i of the
-  // matrix, u = 0..7 the panel's columns; 9 = 8 + 1 pad: a tile row is one contiguous 576-byte
-  // block -- the unit of the DSMEM bulk copies -- and the DMMA fragment loads are 2-way at most)
+  // the panel's G transposed, double-buffered by panel parity: element (i, u) (row i of the
+  // matrix, u = 0..7 the panel's columns) at gx(i, u) = 64 (i / 8) + 32 (u / 4) + 4 (i % 8) + u % 4:
+  // a tile row is one contiguous 512-byte block (the unit of the DSMEM bulk copies) and a DMMA
+  // fragment (rows gid, columns tig of one half) is 32 consecutive doubles -- conflict-free
   double *GT0 = l11s + 64;
-  double *W = GT0 + 2 * 9 * nr8;
+  double *W = GT0 + 2 * 8 * nr8;
+  auto gx = [](int i, int u) { return ((i >> 3) << 6) + ((u >> 2) << 5) + ((i & 7) << 2) + (u & 3); };
   double *G = GT0;  // (the tail reuses the GT area for CTA 0's partial alpha vectors)
   __shared__ __align__(8) uint64_t mbars[3];  // maps | G buffer 0 | G buffer 1
   // (DSMEM: every CTA's G, maps and flags sit at the same offsets; remote addresses are formed
@@ -298,12 +300,14 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
 #pragma unroll
     for (int q = 0; q < kQ; ++q)
       if (q < cnt) cc[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
-    const double a0 = -GT[i * 9 + tig], a1 = -GT[i * 9 + 4 + tig];
-    const double *g = GT + (8 * C0 + gid) * 9 + tig;
+    (void)i;
+    const double *ga = GT + R * 64 + gid * 4 + tig;
+    const double a0 = -ga[0], a1 = -ga[32];
+    const double *g = GT + C0 * 64 + gid * 4 + tig;
     double b0[kQ], b1[kQ];
 #pragma unroll
     for (int q = 0; q < kQ; ++q)
-      if (q < cnt) { b0[q] = g[72 * q]; b1[q] = g[72 * q + 4]; }
+      if (q < cnt) { b0[q] = g[64 * q]; b1[q] = g[64 * q + 32]; }
 #pragma unroll
     for (int q = 0; q < kQ; ++q)
       if (q < cnt) dmma(cc[q].x, cc[q].y, a0, b0[q]);
@@ -313,6 +317,27 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
 #pragma unroll
     for (int q = 0; q < kQ; ++q)
       if (q < cnt) *reinterpret_cast<double2 *>(Wt + 64 * q) = cc[q];
+  };
+
+  // quad() for a full quad: no per-tile predicates (a predicated mma.sync costs a WARPSYNC + NOP
+  // pair per DMMA), one base address per operand stream
+  auto quad_full = [&](const double *__restrict__ GT, int R, int C0) {
+    double *Wt = at(R, C0) + 2 * lane;
+    double2 cc[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) cc[q] = *reinterpret_cast<const double2 *>(Wt + 64 * q);
+    const double *ga = GT + R * 64 + gid * 4 + tig;
+    const double a0 = -ga[0], a1 = -ga[32];
+    const double *g = GT + C0 * 64 + gid * 4 + tig;
+    double b0[kQ], b1[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) { b0[q] = g[64 * q]; b1[q] = g[64 * q + 32]; }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) dmma(cc[q].x, cc[q].y, a0, b0[q]);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) dmma(cc[q].x, cc[q].y, a1, b1[q]);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) *reinterpret_cast<double2 *>(Wt + 64 * q) = cc[q];
   };
 
   const int nown = c < nt ? (nt - 1 - c) / Cc + 1 : 0;  // own tile rows
@@ -364,7 +389,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
     for (int JT = 0; JT < nt && ok; ++JT) {
       const int J = 8 * JT, bb = min(kFitB, n - J);
       const int par = JT & 1;
-      double *GT = GT0 + par * 9 * nr8;
+      double *GT = GT0 + par * 8 * nr8;
       const int r0 = JT + 1 + ((c - (JT + 1) % Cc) + Cc) % Cc;  // first own row > JT
       const int nrows = r0 < nt ? (nt - 1 - r0) / Cc + 1 : 0;
       // ---- C: own rows below the panel; the owner of row JT also the block row left of it
@@ -381,11 +406,10 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
               dmma(d0, d1, a, Nm[(kk + tig) * 8 + gid]);
               dmma(e0, e1, a, Mm[(kk + tig) * 8 + gid]);
             }
-            GT[i * 9 + 2 * tig] = d0;      // (the L panel goes to global memory in T)
-            GT[i * 9 + 2 * tig + 1] = d1;
+            // (the L panel goes to global memory in T); u = 2 tig, 2 tig + 1: one 16-byte store
+            *reinterpret_cast<double2 *>(GT + gx(i, 2 * tig)) = make_double2(d0, d1);
             __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
-            __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
-          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
+            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
           } else {
             const int C = it - nrows;
             double *Wt = at(JT, C);
@@ -396,11 +420,10 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
               dmma(d0, d1, Rm[gid * 8 + mrow], b);
             }
             const int kc = 8 * C + 2 * tig;
-            GT[kc * 9 + gid] = d0;
-            GT[(kc + 1) * 9 + gid] = d1;
+            GT[gx(kc, gid)] = d0;
+            GT[gx(kc + 1, gid)] = d1;
             __syncwarp();
-            __syncwarp();
-          *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
+            *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
           }
         }
       }
@@ -416,7 +439,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
         break;
       }
       // ---- send this CTA's part of G (its rows below the block; the owner also the block row
-      // left of it) to every other CTA: 576-byte tile-row blocks, warp 0 issuing
+      // left of it) to every other CTA: 512-byte tile-row blocks, warp 0 issuing
       const uint32_t mb_g = tc::smem_u32(&mbars[1 + par]);
       if (warp == 0) {
         const int nl = owner(JT) == c && JT > 0 ? 1 : 0;
@@ -424,15 +447,15 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
         for (int it = lane; it < items; it += 32) {
           const int dst = it % (Cc - 1), q = it / (Cc - 1);
           const int r = dst < c ? dst : dst + 1;
-          const uint32_t off = q < nrows ? (uint32_t)(r0 + q * Cc) * 576u : 0u;
-          const uint32_t bytes = q < nrows ? 576u : 576u * (uint32_t)JT;
+          const uint32_t off = q < nrows ? (uint32_t)(r0 + q * Cc) * 512u : 0u;
+          const uint32_t bytes = q < nrows ? 512u : 512u * (uint32_t)JT;
           const uint32_t src = tc::smem_u32(GT) + off;
           bulk_s2s(mapa(src, r), src, bytes, mapa(mb_g, r));
         }
         if (lane == 0) {  // this CTA's own arrival, expecting what the others send it
-          uint32_t expect = owner(JT) != c ? 576u * (uint32_t)JT : 0u;
+          uint32_t expect = owner(JT) != c ? 512u * (uint32_t)JT : 0u;
           for (int R = JT + 1; R < nt; ++R)
-            if (owner(R) != c) expect += 576u;
+            if (owner(R) != c) expect += 512u;
           tc::mbar_arrive_expect_tx(mb_g, expect);
         }
       }
@@ -441,7 +464,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       for (int R = r0; R < nt; R += Cc)
         for (int e = tid; e < 64; e += kFitThreads) {
           const int u = e >> 3, i = 8 * R + (e & 7);
-          if (i < n) Lg[(size_t)(J + u) * n + i] = GT[i * 9 + u];
+          if (i < n) Lg[(size_t)(J + u) * n + i] = GT[gx(i, u)];
         }
       if (owner(JT) == c)
         for (int e = tid; e < 64; e += kFitThreads) {
@@ -479,12 +502,17 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
             const int len = nlq + (r > 0 ? r / kQ + 1 : 0);
             for (int q = 0; q < len; ++q, ++item) {
               if (item % kT != warp) continue;
+              int C0, cnt;
               if (q < nlq) {
-                quad(GT, R, kQ * q, min(kQ, JT - kQ * q));
+                C0 = kQ * q;
+                cnt = min(kQ, JT - kQ * q);
               } else {
                 const int c0 = kQ * (q - nlq);
-                quad(GT, R, JT + 1 + c0, min(kQ, r + 1 - c0));
+                C0 = JT + 1 + c0;
+                cnt = min(kQ, r + 1 - c0);
               }
+              if (cnt == kQ) quad_full(GT, R, C0);
+              else quad(GT, R, C0, cnt);
             }
           }
         }
@@ -618,7 +646,7 @@ int fit_cluster_smem(int n, int Cc) {
   const int nt = (n + 7) / 8;
   int tiles = 0;
   for (int c = 0; c < Cc; ++c) tiles = std::max(tiles, own_tiles(nt, c, Cc));
-  return (2 * fit_nr8(n) + 24 + 4 * 64 + 2 * 9 * fit_nr8(n) + tiles * 64) * 8;
+  return (2 * fit_nr8(n) + 24 + 4 * 64 + 2 * 8 * fit_nr8(n) + tiles * 64) * 8;
 }
 
 cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem_bytes,

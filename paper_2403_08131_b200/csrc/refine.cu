@@ -375,7 +375,8 @@ direct_kernel(const RefineLaunch p, int S, int64_t rows) {
 //   1. x* / l of the tile and q* = |x* / l|^2 into shared memory;
 //   2. K* from GEMM-form squared distances r^2 = q* + q - 2 (x* / l) . (x / l) on DMMA m8n8k4
 //      (float64: the form's cancellation error ~ u q is ~1e-15 sf2 in k*, far inside T1, whose
-//      variance term is relative to sf2 -- tests/helpers.py check_T1), clamped at 0; the kernel
+//      variance term is relative to sf2 -- tests/helpers.py check_T1), clamped at 0 (NaN kept:
+//      a non-finite candidate row yields NaN outputs); the kernel
 //      in float64 on the fragments; K*^T into shared memory and the mean partials k* alpha;
 //   3. V^T = L^-1 K*^T on DMMA: 8-row blocks J of L^-1 (2J + 2 k-steps of 4 each) dealt to the
 //      warps by longest-processing-time (deterministic, near-equal k-step totals); A fragments
@@ -493,12 +494,15 @@ posterior64_kernel(const RefineLaunch p, int dmax) {
         }
         const int j0 = 8 * J + 2 * tig;
         double k0v = 0.0, k1v = 0.0;
+        // r^2 clamped at 0 by a compare that keeps NaN (fmax(NaN, 0) = 0 would turn a NaN
+        // candidate row into a finite one at distance 0)
+        auto clamp0 = [](double r2) { return r2 < 0.0 ? 0.0 : r2; };
         if (j0 < n) {
-          k0v = kernel64(fmax(qa + qj[j0] - 2.0 * d0, 0.0), sf2, m.kernel);
+          k0v = kernel64(clamp0(qa + qj[j0] - 2.0 * d0), sf2, m.kernel);
           mu = fma(k0v, __ldg(alpha + j0), mu);
         }
         if (j0 + 1 < n) {
-          k1v = kernel64(fmax(qa + qj[j0 + 1] - 2.0 * d1, 0.0), sf2, m.kernel);
+          k1v = kernel64(clamp0(qa + qj[j0 + 1] - 2.0 * d1), sf2, m.kernel);
           mu = fma(k1v, __ldg(alpha + j0 + 1), mu);
         }
         ks[j0 * kPostLd + 8 * cb + gid] = k0v;

@@ -81,22 +81,90 @@ __host__ __device__ inline void sample_candidate(const SpaceView &sp, uint64_t s
 
 namespace {
 
-__global__ void __launch_bounds__(128)
-gen_kernel(const SpaceView sp, uint64_t seed, uint32_t search, uint32_t iter, int64_t first,
+constexpr int kGenThreads = 128;
+constexpr int kHashSlots = 1024;  // >= 2 GPBO_MAX_N: open addressing stays short
+
+// 64-bit hash of an encoded row (FNV-1a style over the columns' bits, then a final mix); +0 and
+// -0 hash alike (they compare equal).  Training rows and candidates are hashed the same way.
+__device__ __forceinline__ uint64_t row_hash(const float *r, int d) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (int c = 0; c < d; ++c) {
+    const float v = r[c] == 0.f ? 0.f : r[c];
+    h = (h ^ __float_as_uint(v)) * 0x100000001B3ull;
+  }
+  h ^= h >> 29;
+  h *= 0xBF58476D1CE4E5B9ull;
+  return h ^ (h >> 32);
+}
+
+// One candidate per thread, 128 per CTA: drawn into a shared-memory tile (row stride d | 1:
+// conflict-free), deduplicated against the training rows through a shared-memory hash table of
+// their encodings (reading R14: a candidate equal to an observed configuration is masked with
+// NaN; equality is exact, the hash only selects which rows to compare), then written to HBM as
+// one contiguous, coalesced block.
+__global__ void __launch_bounds__(kGenThreads)
+gen_kernel(const SpaceView sp_g, uint64_t seed, uint32_t search, uint32_t iter, int64_t first,
            int64_t count, float *out, const float *__restrict__ Xtrain, int n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  float enc[GPBO_MAX_D];
-  sample_candidate(sp, seed, search, iter, (uint32_t)(first + i), enc, nullptr);
-  const int d = sp.d;
-  if (Xtrain) {  // reading R14: a candidate equal to an observed configuration is masked
-    for (int j = 0; j < n; ++j) {
-      bool eq = true;
-      for (int c = 0; c < d && eq; ++c) eq = Xtrain[j * d + c] == enc[c];
-      if (eq) { enc[0] = NAN; break; }
+  extern __shared__ float tile[];
+  __shared__ unsigned long long hkey[kHashSlots];
+  __shared__ int hrow[kHashSlots];
+  // the per-parameter tables (P <= GPBO_MAX_D) in shared memory: sample_candidate reads them
+  // once per parameter and candidate
+  __shared__ int32_t s_kind[GPBO_MAX_D], s_nv[GPBO_MAX_D], s_col[GPBO_MAX_D], s_free[GPBO_MAX_D];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < sp_g.P; i += kGenThreads) {
+    s_kind[i] = sp_g.kind[i]; s_nv[i] = sp_g.nv[i]; s_col[i] = sp_g.col[i];
+  }
+  for (int i = tid; i < sp_g.nfree; i += kGenThreads) s_free[i] = sp_g.free_list[i];
+  SpaceView sp = sp_g;
+  sp.kind = s_kind; sp.nv = s_nv; sp.col = s_col; sp.free_list = s_free;
+  __syncthreads();
+  const int d = sp.d, ld = d | 1;
+  if (Xtrain) {
+    for (int e = tid; e < kHashSlots; e += kGenThreads) { hkey[e] = 0ull; hrow[e] = -1; }
+    __syncthreads();
+    for (int j = tid; j < n; j += kGenThreads) {
+      const uint64_t h = row_hash(Xtrain + (size_t)j * d, d) | 1ull;  // 0 marks an empty slot
+      for (int sl = (int)(h & (kHashSlots - 1));; sl = (sl + 1) & (kHashSlots - 1)) {
+        if (atomicCAS(&hkey[sl], 0ull, (unsigned long long)h) == 0ull) { hrow[sl] = j; break; }
+      }
+    }
+    __syncthreads();
+  }
+  float *enc = tile + tid * ld;
+  const int64_t ntile = (count + kGenThreads - 1) / kGenThreads;
+  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {  // persistent: one table build per CTA
+    const int64_t i0 = t * kGenThreads;
+    const int cnt = (int)min((int64_t)kGenThreads, count - i0);
+    __syncthreads();  // the previous tile's rows are written out
+    if (tid < cnt) {
+      sample_candidate(sp, seed, search, iter, (uint32_t)(first + i0 + tid), enc, nullptr);
+      if (Xtrain) {
+        const uint64_t h = row_hash(enc, d) | 1ull;
+        bool dup = false;
+        for (int sl = (int)(h & (kHashSlots - 1)); !dup && hkey[sl] != 0ull;
+             sl = (sl + 1) & (kHashSlots - 1)) {
+          if (hkey[sl] != h) continue;
+          const float *xr = Xtrain + (size_t)hrow[sl] * d;
+          bool eq = true;
+          for (int c = 0; c < d && eq; ++c) eq = xr[c] == enc[c];
+          dup = eq;
+        }
+        if (dup) enc[0] = NAN;
+      }
+    }
+    __syncthreads();
+    // coalesced write-out: element e = r d + c of the tile, (r, c) advanced incrementally
+    float *dst = out + i0 * d;
+    const int step_r = kGenThreads / d, step_c = kGenThreads - step_r * d;
+    int r = tid / d, c = tid - r * d;
+    for (int e = tid; e < cnt * d; e += kGenThreads) {
+      dst[e] = tile[r * ld + c];
+      r += step_r;
+      c += step_c;
+      if (c >= d) { c -= d; ++r; }
     }
   }
-  for (int c = 0; c < d; ++c) out[i * d + c] = enc[c];
 }
 
 }  // namespace
@@ -105,8 +173,18 @@ cudaError_t launch_gen(const SpaceView &sp_dev, uint64_t seed, uint32_t search, 
                        int64_t first, int64_t count, float *out, const float *Xtrain, int n,
                        cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  gen_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(sp_dev, seed, search, iter, first,
-                                                             count, out, Xtrain, n);
+  if (n > kHashSlots / 2) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)kGenThreads * (sp_dev.d | 1) * sizeof(float);
+  static int sms = 0;  // (a benign race: every thread computes the same value)
+  if (sms == 0) {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      sms = v;
+  }
+  const int64_t tiles = (count + kGenThreads - 1) / kGenThreads;
+  gen_kernel<<<(unsigned)std::min<int64_t>(tiles, (int64_t)std::max(sms, 1) * 8), kGenThreads, smem, st>>>(
+      sp_dev, seed, search, iter, first, count, out, Xtrain, n);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,8 @@ for c in 2 4; do
 done
 timeout 900 python bench.py --config 5 --steps 200 --warmup 3 > $o/${tag}_bench_cfg5.json 2> $o/${tag}_bench_cfg5.err
 timeout 600 python tools/replay_bench.py > $o/${tag}_replay_cfg5.json 2>&1
+rm -f $o/${tag}_posterior_bench.jsonl
+for c in 2 3 4; do timeout 300 python tools/posterior_bench.py $c >> $o/${tag}_posterior_bench.jsonl 2>&1; done
 # launch list of the default step (cold-cache, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $o/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
@@ -37,4 +39,6 @@ cap refine 'refine'
 cap gram 'gram_kernel'
 cap pack 'pack_tc'
 cap mean64 'mean64' --layout bo
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:posterior64 -s 2 -c 1 \
+    -o $o/${tag}_posterior64 python tools/posterior_bench.py 2 65536 > $o/${tag}_posterior64.log 2>&1
 ls -la $o/${tag}_*
