@@ -297,6 +297,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   double jit = 0.0;
   double p10 = 1.0;
 #if GPBO_FIT_STATIC
+  static_assert(kQ == 4, "the static quad list assumes 4-tile quads");
   // the trailing update's quad list: (R, Q) for rows R = nt - 1 .. 1, Q = 0 .. R / kQ;
   // qabove[J] = number of quads of rows > J
   __shared__ int qtab[(kFitSmemMaxN / 8) * (kFitSmemMaxN / 8 / kQ + 1)];
@@ -489,15 +490,19 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
         // of rows > JT are the first qabove[JT] entries, dealt round robin; a quad's tiles at
         // the panel column JT, past the diagonal, or on the D warp's diagonal tile are masked
         const int nq = qabove[JT];
+        // tiles of quad (R, C0) to update: C <= R, not the panel column JT, not the D warp's
+        // diagonal tile (R = JT + 1)
+        auto qmask = [&](int R, int C0) -> unsigned {
+          unsigned mk = 0xFu;
+          if (C0 + 3 > R) mk &= (1u << (R - C0 + 1)) - 1u;
+          if (JT >= C0 && JT < C0 + 4) mk &= ~(1u << (JT - C0));
+          if (R == JT + 1 && R < C0 + 4) mk &= ~(1u << (R - C0));
+          return mk;
+        };
         for (int k = warp; k < nq; k += kT) {
           const int v = qtab[k], R = v >> 8, C0 = kQ * (v & 255);
-          unsigned mask = 0;
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) {
-            const int C = C0 + q;
-            mask |= (C <= R && C != JT && !(R == JT + 1 && C == R)) ? 1u << q : 0u;
-          }
-          if (mask == (1u << kQ) - 1) quad_full(G1, R, C0);
+          const unsigned mask = qmask(R, C0);
+          if (mask == 0xFu) quad_full(G1, R, C0);
           else if (mask) quad_mask(G1, R, C0, mask);
         }
 #else
