@@ -131,9 +131,11 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   __shared__ __align__(8) uint64_t mbars[3];  // maps | G buffer 0 | G buffer 1
   // (DSMEM: every CTA's G, maps and flags sit at the same offsets; remote addresses are formed
   // with cluster.map_shared_rank where they are written)
-  auto owner = [&](int R) { return R % Cc; };
+  // Cc is a power of two (1, 2, 4, 8: api.cu fit_cluster_size): shifts instead of divisions
+  const int lcc = __ffs(Cc) - 1;
+  auto owner = [&](int R) { return R & (Cc - 1); };
   auto at = [&](int R, int C) -> double * {  // own tile (R, C), R = c (mod Cc)
-    return W + (own_rowoff(R / Cc, c, Cc) + C) * 64;
+    return W + (own_rowoff(R >> lcc, c, Cc) + C) * 64;
   };
   double *Lg = io.L64 + m.mat_off;
   const float *X = io.X_src + m.x_off;
@@ -390,8 +392,8 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       const int J = 8 * JT, bb = min(kFitB, n - J);
       const int par = JT & 1;
       double *GT = GT0 + par * 8 * nr8;
-      const int r0 = JT + 1 + ((c - (JT + 1) % Cc) + Cc) % Cc;  // first own row > JT
-      const int nrows = r0 < nt ? (nt - 1 - r0) / Cc + 1 : 0;
+      const int r0 = JT + 1 + ((c - (JT + 1)) & (Cc - 1));  // first own row > JT
+      const int nrows = r0 < nt ? ((nt - 1 - r0) >> lcc) + 1 : 0;
       // ---- C: own rows below the panel; the owner of row JT also the block row left of it
       {
         const int nleft = owner(JT) == c ? JT : 0;
@@ -496,12 +498,16 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
           FCT(4);
           // items of own row R (r = R - JT - 1): nlq left quads (C < JT), then right quads of
           // columns JT + 1 .. R (row JT + 1's right quad is the diagonal tile: the D warp's)
-          int item = 0;
+          // (items are numbered row after row and dealt round robin: this warp's first item of
+          // a row follows from the row's base number -- one modulo per row, not per item: the
+          // per-item test was ~37 % of the kernel's instructions)
+          int base = 0;
           for (int lr = 0; lr < nrows; ++lr) {
             const int R = r0 + lr * Cc, r = R - JT - 1;
             const int len = nlq + (r > 0 ? r / kQ + 1 : 0);
-            for (int q = 0; q < len; ++q, ++item) {
-              if (item % kT != warp) continue;
+            const int q0 = (warp - base % kT + kT) % kT;
+            base += len;
+            for (int q = q0; q < len; q += kT) {
               int C0, cnt;
               if (q < nlq) {
                 C0 = kQ * q;
