@@ -749,7 +749,7 @@ namespace {
 // offsets, tcgen05 geometry) and one stream-ordered device block holding every array.
 struct ModelScratch {
   SearchMeta *meta_in = nullptr;  // device staging of the input meta records
-  double *Wscr64 = nullptr, *Kt64 = nullptr, *pm_part = nullptr;
+  double *Wscr64 = nullptr, *Kt64 = nullptr, *pm_part = nullptr, *G64 = nullptr;
   int smem_max = 0;
 };
 
@@ -763,7 +763,7 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
   m->stream = ctx->stream;
   m->meta.resize(S);
   int64_t nx = 0, nls = 0, ny = 0, nmat = 0, nxs = 0, nlt = 0, na = 0, nimg = 0, nscr = 0;
-  int64_t nkt = 0;
+  int64_t nkt = 0, nstg = 0;
   int smem_max = 0;
   // tcgen05 image layout, uniform over the model: streamed (score_tcs.cu) when any search's
   // resident image would not fit in shared memory, or when the ctx forces it (impl 3)
@@ -806,6 +806,7 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
     q.use_smem = n <= gpbo::kFitSmemMaxN;
     if (!q.use_smem) { q.scr_off = nscr; nscr += gpbo::fit_tile_doubles(n); }
     q.kt_off = nkt; nkt += gpbo::fit_tile_doubles(n);
+    q.stg_off = nstg; nstg += 16 * gpbo::fit_nr8(n);
     const int smem = gpbo::fit_smem_doubles(n, q.use_smem) * 8;
     q.xs_smem = 0;
     smem_max = std::max(smem_max, smem);
@@ -821,6 +822,7 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
   const size_t o_Li = take(nmat * 8), o_a = take(na * 8), o_img = take(nimg);
   const size_t o_x64 = take(nx * 8), o_scr = take(nscr * 8), o_kt = take(nkt * 8);
   const size_t o_pm = take((size_t)S * 16 * 8);
+  const size_t o_stg = take((size_t)nstg * 8);
   cudaError_t e = cudaMallocAsync((void **)&m->block, off, ctx->stream);
   if (e != cudaSuccess) { delete m; return fail(ctx, GPBO_ENOMEM, "model allocation failed"); }
   m->meta_d = (SearchMeta *)(m->block + o_meta);
@@ -838,6 +840,7 @@ gpbo_status alloc_model(gpbo_ctx *ctx, int S, const int32_t *n_in, const int32_t
   sc->Wscr64 = (double *)(m->block + o_scr);
   sc->Kt64 = (double *)(m->block + o_kt);
   sc->pm_part = (double *)(m->block + o_pm);
+  sc->G64 = (double *)(m->block + o_stg);
   sc->smem_max = smem_max;
   m->img_bytes = nimg;
   m->nx_total = nx; m->nls_total = nls; m->ny_total = ny;
@@ -909,6 +912,7 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   io.Wscr64 = Wscr64;
   io.Kt64 = Kt64;
   io.pm_part = sc.pm_part;
+  io.G64 = sc.G64;
   if (a->mem == GPBO_HOST) {  // stage into the model's arrays
     CKM(cudaMemcpyAsync(m->X32, a->X, nx * 4, kind, ctx->stream));
     CKM(cudaMemcpyAsync(m->ls32, a->lengthscale, nls * 4, kind, ctx->stream));

@@ -59,6 +59,20 @@ __device__ __forceinline__ void bulk_s2s(uint32_t dst, uint32_t src, uint32_t by
       ::"r"(dst), "r"(src), "r"(bytes), "r"(mbar) : "memory");
 }
 
+// bulk copy (TMA) global -> the same shared-memory offset in every CTA of `mask`, completing
+// `bytes` of transaction count on each destination's mbarrier at the offset of `mbar`
+__device__ __forceinline__ void bulk_g2s_mc(uint32_t dst, const void *src, uint32_t bytes,
+                                            uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "h"(mask) : "memory");
+}
+
+#ifndef GPBO_FITC_MCAST
+#define GPBO_FITC_MCAST 1  // G rows via global staging + multicast (1) or DSMEM pushes (0)
+#endif
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
@@ -351,6 +365,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   uint32_t mp = 0, gp[2] = {0u, 0u};  // completed phases: maps barrier, G barriers
 #ifdef GPBO_FIT_TIMING
   long long ft[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long wgs[3] = {0, 0, 0};
   long long ft0 = clock64();
   __shared__ long long dclk;
   if (tid == 0) dclk = 0;
@@ -392,6 +407,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       const int J = 8 * JT, bb = min(kFitB, n - J);
       const int par = JT & 1;
       double *GT = GT0 + par * 8 * nr8;
+      double *GS = io.G64 + m.stg_off + par * 8 * nr8;  // the same layout in global memory
       const int r0 = JT + 1 + ((c - (JT + 1)) & (Cc - 1));  // first own row > JT
       const int nrows = r0 < nt ? ((nt - 1 - r0) >> lcc) + 1 : 0;
       // ---- C: own rows below the panel; the owner of row JT also the block row left of it
@@ -410,6 +426,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
             }
             // (the L panel goes to global memory in T); u = 2 tig, 2 tig + 1: one 16-byte store
             *reinterpret_cast<double2 *>(GT + gx(i, 2 * tig)) = make_double2(d0, d1);
+            if (GPBO_FITC_MCAST) *reinterpret_cast<double2 *>(GS + gx(i, 2 * tig)) = make_double2(d0, d1);
             __syncwarp();  // every lane's tile reads precede the write-back (racecheck-clean)
             *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(e0, e1);
           } else {
@@ -424,12 +441,14 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
             const int kc = 8 * C + 2 * tig;
             GT[gx(kc, gid)] = d0;
             GT[gx(kc + 1, gid)] = d1;
+            if (GPBO_FITC_MCAST) { GS[gx(kc, gid)] = d0; GS[gx(kc + 1, gid)] = d1; }
             __syncwarp();
             *reinterpret_cast<double2 *>(Wt + 2 * lane) = make_double2(d0, d1);
           }
         }
       }
       tc::fence_proxy_async();  // GT writes -> visible to the bulk copies below
+      if (GPBO_FITC_MCAST) asm volatile("fence.proxy.async.global;" ::: "memory");  // GS too
       __syncthreads();
       FCT(3);
       if (JT + 1 == nt) {  // the last block: its L11 (no rows below, no trailing update)
@@ -443,7 +462,22 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       // ---- send this CTA's part of G (its rows below the block; the owner also the block row
       // left of it) to every other CTA: 512-byte tile-row blocks, warp 0 issuing
       const uint32_t mb_g = tc::smem_u32(&mbars[1 + par]);
-      if (warp == 0) {
+      if (warp == 0 && GPBO_FITC_MCAST) {
+        // one multicast bulk copy per own tile row (and the block row left of the panel at its
+        // owner) from the global staging into every other CTA: the DSMEM pushes took 7 copies
+        // per block, issued by one warp, and the owner's left block (up to 32 KB x 7) left its
+        // SM serially; the multicast reads L2 once and fans out
+        const uint16_t others = (uint16_t)(((1u << Cc) - 1u) & ~(1u << c));
+        const int nl = owner(JT) == c && JT > 0 ? 1 : 0;
+        for (int q = lane; q < nrows + nl; q += 32) {
+          const uint32_t off = q < nrows ? (uint32_t)(r0 + q * Cc) * 512u : 0u;
+          const uint32_t bytes = q < nrows ? 512u : 512u * (uint32_t)JT;
+          if (others)
+            bulk_g2s_mc(tc::smem_u32(GT) + off, reinterpret_cast<const char *>(GS) + off, bytes,
+                        mb_g, others);
+        }
+      }
+      if (warp == 0 && !GPBO_FITC_MCAST) {
         const int nl = owner(JT) == c && JT > 0 ? 1 : 0;
         const int items = (nrows + nl) * (Cc - 1);
         for (int it = lane; it < items; it += 32) {
@@ -454,12 +488,12 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
           const uint32_t src = tc::smem_u32(GT) + off;
           bulk_s2s(mapa(src, r), src, bytes, mapa(mb_g, r));
         }
-        if (lane == 0) {  // this CTA's own arrival, expecting what the others send it
-          uint32_t expect = owner(JT) != c ? 512u * (uint32_t)JT : 0u;
-          for (int R = JT + 1; R < nt; ++R)
-            if (owner(R) != c) expect += 512u;
-          tc::mbar_arrive_expect_tx(mb_g, expect);
-        }
+      }
+      if (warp == 0 && lane == 0) {  // this CTA's own arrival, expecting what the others send it
+        uint32_t expect = owner(JT) != c ? 512u * (uint32_t)JT : 0u;
+        for (int R = JT + 1; R < nt; ++R)
+          if (owner(R) != c) expect += 512u;
+        tc::mbar_arrive_expect_tx(mb_g, expect);
       }
       // ---- deferred global writes of panel JT (their latency overlaps T): the L panel of the
       // own rows below the block (= their G entries) and, at the block's owner, the L11 of D(JT)
@@ -494,7 +528,13 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
           if (lane == 0) dclk += clock64() - td0;
 #endif
         } else {
+#ifdef GPBO_FIT_TIMING
+          const long long tw0 = clock64();
+#endif
           tc::mbar_wait(mb_g, gp[par] & 1u);
+#ifdef GPBO_FIT_TIMING
+          if (tid == 0) wgs[(3 * JT) / nt] += clock64() - tw0;
+#endif
           FCT(4);
           // items of own row R (r = R - JT - 1): nlq left quads (C < JT), then right quads of
           // columns JT + 1 .. R (row JT + 1's right quad is the diagonal tile: the D warp's)
@@ -611,8 +651,9 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   FCT(7);
 #ifdef GPBO_FIT_TIMING
   if (tid == 0 && s == 0 && (c == 0 || c == 1))
-    printf("FITC n=%d Cc=%d c=%d load=%lld D0=%lld maps0=%lld C=%lld waitG=%lld T=%lld maps=%lld tail=%lld Dlook=%lld\n",
-           n, Cc, c, ft[0], ft[1], ft[2], ft[3], ft[4], ft[5], ft[6], ft[7], dclk);
+    printf("FITC n=%d Cc=%d c=%d load=%lld D0=%lld maps0=%lld C=%lld waitG=%lld T=%lld maps=%lld tail=%lld Dlook=%lld"
+           " [G wait by panel third: %lld %lld %lld]\n",
+           n, Cc, c, ft[0], ft[1], ft[2], ft[3], ft[4], ft[5], ft[6], ft[7], dclk, wgs[0], wgs[1], wgs[2]);
 #endif
   if (c != 0) return;
   double l1 = 0.0, amx = 0.0;

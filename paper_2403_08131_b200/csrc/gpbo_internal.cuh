@@ -80,6 +80,8 @@ struct SearchMeta {
   int32_t xs_smem;      // fit stages x / l (n x d float64) in shared memory for the Gram
   int64_t scr_off;      // else: its tile-packed working matrix (fit_tile_doubles) in model.Wscr64
   int64_t kt_off;       // kernel matrix k(X, X) without noise / jitter, tile-packed, in model.Kt64
+  int64_t stg_off;      // cluster fit: the panel's G rows staged in global memory for the
+                        // multicast bulk copies (2 x 8 fit_nr8(n) doubles) in model's G64
 };
 
 // Candidate flagged by the fast phase for the float64 refine phase.  The refine re-scores it in
@@ -168,6 +170,7 @@ struct FitIO {
   double *y64, *L64, *Linv64, *Xs64, *alpha64, *Wscr64;
   double *Kt64;                  // the Gram pre-pass output (tile-packed, no noise / jitter)
   double *pm_part;               // [16 S] per-CTA max |x / l|^2 of the pre-pass
+  double *G64;                   // cluster fit staging (SearchMeta::stg_off)
   unsigned char *img;            // non-NULL: the one-CTA fit packs the tcgen05 operand image of
                                  // searches with n > kDirectMaxN in its tail (score_pack.cuh)
 };
