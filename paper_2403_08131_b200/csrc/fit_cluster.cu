@@ -489,10 +489,10 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
           bulk_s2s(mapa(src, r), src, bytes, mapa(mb_g, r));
         }
       }
-      if (warp == 0 && lane == 0) {  // this CTA's own arrival, expecting what the others send it
-        uint32_t expect = owner(JT) != c ? 512u * (uint32_t)JT : 0u;
-        for (int R = JT + 1; R < nt; ++R)
-          if (owner(R) != c) expect += 512u;
+      if (warp == 0 && lane == 0) {  // this CTA's own arrival, expecting what the others send it:
+        // the rows JT + 1 .. nt - 1 it does not own, and the left block unless it owns row JT
+        const uint32_t expect = 512u * (uint32_t)(nt - 1 - JT - nrows) +
+                                (owner(JT) != c ? 512u * (uint32_t)JT : 0u);
         tc::mbar_arrive_expect_tx(mb_g, expect);
       }
       // ---- deferred global writes of panel JT (their latency overlaps T): the L panel of the
