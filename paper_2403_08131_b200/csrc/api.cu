@@ -854,11 +854,15 @@ int fit_cluster_size(const gpbo_ctx *ctx, int S, int nmax) {
     const char *e = getenv("GPBO_FIT");
     return e && !strcmp(e, "single");
   }();
+  static const bool force_cluster = [] {  // A/B: the cluster fit for every n
+    const char *e = getenv("GPBO_FIT");
+    return e && !strcmp(e, "cluster");
+  }();
   // measured (profiles/r02): for n <= 216 the one-CTA kernel keeps its working matrix in shared
   // memory and the cluster's DSMEM hops (~2.5 k cycles per panel) cost as much as the split
   // trailing update saves (n = 200: 0.139 vs 0.140 ms; 64 x n = 100: 0.056 vs 0.084 ms); for
   // n > 216 the one-CTA kernel streams W through L2 and the cluster wins (n = 500: 1.27 -> 0.68 ms)
-  if (single || nmax <= gpbo::kFitSmemMaxN) return 0;
+  if (single || (nmax <= gpbo::kFitSmemMaxN && !force_cluster)) return 0;
   const int per = ctx->num_sms / std::max(S, 1);
   int Cc = per >= 8 ? 8 : per >= 4 ? 4 : per >= 2 ? 2 : 1;
   while (Cc < 8 && gpbo::fit_cluster_smem(nmax, Cc) > gpbo::kFitSmemBudget) Cc *= 2;
