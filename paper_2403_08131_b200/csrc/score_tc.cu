@@ -78,11 +78,16 @@ constexpr int kKStages = 2;         // K* operand stages (TMEM), one 64-wide pan
 // MUFU or tensor pipes, bound the kernel (timing experiments without MUFU work / without 2/3
 // of the MMAs: -7 % / -4 %).
 constexpr uint32_t kScratch0 = 256;
+// GPBO_RING4: kMerged launches (every n16 + 16 <= 128) trade the second V accumulator for a
+// 4-deep distance ring: V [0, 128), ring [128, 384), K* stages [384, 512)
+#ifndef GPBO_RING4
+#define GPBO_RING4 1  // measured: config 3 fast phase 2.689 -> 2.653 ms (config 2: not kMerged, unaffected)
+#endif
 constexpr uint32_t kKstar0 = 384;
 
 enum {
   B_AF0 = 0, B_AF1, B_AE0, B_AE1,           // candidate A tile (double buffer)
-  B_DF0, B_DF1, B_DE0, B_DE1,               // distance scratch ring
+  B_DF0, B_DF1, B_DF2, B_DF3, B_DE0, B_DE1, B_DE2, B_DE3,  // distance scratch ring (<= 4)
   B_KF0, B_KF1, B_KF2, B_KF3, B_KE0, B_KE1, B_KE2, B_KE3,  // K* panel stages
   B_VF0, B_VF1, B_VE0, B_VE1,               // V accumulators
   B_SF0, B_SF1,                             // raw candidate rows landed in staging (TMA)
@@ -118,6 +123,8 @@ __host__ __device__ inline TcSmem tc_smem(int img_max, int kb_max, int d_max) {
 template <bool kMerged, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, int kb_max, int d_max) {
+  constexpr int kDep = (kMerged && GPBO_RING4) ? 4 : kDepth;                 // distance ring depth
+  constexpr uint32_t kScr = (kMerged && GPBO_RING4) ? 128u : kScratch0;     // its first column
   extern __shared__ unsigned char sm_raw[];
   unsigned char *sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
   const TcSmem L = tc_smem(img_max, kb_max, d_max);
@@ -157,7 +164,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       tc::mbar_init(bar(B_VE0 + i), 4 * kTs);
       tc::mbar_init(bar(B_SF0 + i), 1);
     }
-    for (int i = 0; i < kDepth; ++i) {
+    for (int i = 0; i < 4; ++i) {
       tc::mbar_init(bar(B_DF0 + i), 1);
       tc::mbar_init(bar(B_DE0 + i), kKWarps * kTs);
     }
@@ -218,7 +225,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
     // B_VB0..1 / B_VB2..3 per buffer.  Otherwise one accumulator and 4 block barriers (one per
     // 64-wide column block: one commit per panel besides the K* stage release).
     const int nv16 = n16 + kMeanRows;  // V accumulator columns (L^-1 rows + mean rows)
-    const bool dbl = nv16 <= 128;
+    const bool dbl = nv16 <= 128 && !(kMerged && GPBO_RING4);
     const uint32_t vbq = dbl ? 2u : 4u;
     const int T = tb - ta;
     const int P64 = (n16 + 63) / 64;  // 64-wide K* panels per tile
@@ -241,8 +248,8 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       const uint32_t xlo = (uint32_t)(n16 * 32) >> 4;  // hi -> lo block of the X^ operand
       const int ndc = (npan + 1) >> 1;                 // distance chunks per tile
       uint32_t gc = gc_seg;
-      int d_st = (int)(gc % kDepth);
-      uint32_t d_ph = (gc / kDepth) & 1u;
+      int d_st = (int)(gc % kDep);
+      uint32_t d_ph = (gc / kDep) & 1u;
       for (int tl = 0; tl < T; ++tl) {
         const uint32_t ti = gi + tl, ab = ti & 1u;
         tc::mbar_wait(bar(B_AF0 + ab), (ti >> 1) & 1u);
@@ -251,7 +258,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           tc::mbar_wait(bar(B_DE0 + d_st), d_ph ^ 1u);
           tc::tc_fence_after();
           const uint32_t Nq = (uint32_t)min(64, n16 - 64 * q);
-          const uint32_t dt = tbase + kScratch0 + 64u * (uint32_t)d_st;
+          const uint32_t dt = tbase + kScr + 64u * (uint32_t)d_st;
           uint32_t a = abase + ab * (uint32_t)kb * 512u;  // 8192 B per K block
           if (lane == 0) trace_ev(p.trace, 24, 11, gc, trc);
           if constexpr (kPair) {
@@ -282,7 +289,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           }
           if (lane == 0) trace_ev(p.trace, 4, 11, gc, trc);
           ++gc;
-          if (++d_st == kDepth) { d_st = 0; d_ph ^= 1u; }
+          if (++d_st == kDep) { d_st = 0; d_ph ^= 1u; }
         }
         if (kPair) tc::mma2_commit_warp(bar(B_AE0 + ab));  // A tiles of both CTAs consumed
         else tc::mma_commit_warp(bar(B_AE0 + ab));         // A tile consumed
@@ -583,7 +590,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
       uint32_t ec = gc_seg;  // distance chunk counter (= panel counter)
       int pp = 0;
       for (int g = 0; g < P; ++g) {
-        const uint32_t st = ec % kDepth;
+        const uint32_t st = ec % kDep;
         const int jb = 64 * pp + kCW * part;
         const int nv = min(kCW, n16 - jb);  // valid points of this warp (kCW, 16 or <= 0)
         const bool trw = (warp == 0 || warp == kKWarps - 1) && lane == 0;
@@ -593,7 +600,7 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
         // separate acquires (the early DE release keeps the distance ring ahead).
         // A compile-time choice: the run-time branch cost registers and was slower in both cases.
         const uint32_t ks = gk % kKStages;
-        const uint32_t da = tl_addr + kScratch0 + 64u * st + (uint32_t)(kCW * part);
+        const uint32_t da = tl_addr + kScr + 64u * st + (uint32_t)(kCW * part);
         uint32_t hr[kCW];
         auto load_h = [&]() {  // (a 16-point remainder: only its 16 columns)
           if (kCW == 32 && nv == 32) tc::tmem_ld32(da, hr);
@@ -601,14 +608,14 @@ score_tc_kernel(const ScoreLaunch p, int tile_lo, int total_tiles, int img_max, 
           tc::tmem_wait_ld();
         };
         if (kMerged) {
-          tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
+          tc::mbar_wait(bar(B_DF0 + st), (ec / kDep) & 1u);
           tc::mbar_wait(bar(B_KE0 + ks), ((gk / kKStages) & 1u) ^ 1u);
           tc::tc_fence_after();
           if (nv > 0) load_h();
           if (trw) trace_ev(p.trace, 6, warp, gk, trc);
           if (trw) trace_ev(p.trace, 7, warp, gk, trc);
         } else {
-          tc::mbar_wait(bar(B_DF0 + st), (ec / kDepth) & 1u);
+          tc::mbar_wait(bar(B_DF0 + st), (ec / kDep) & 1u);
           if (trw) trace_ev(p.trace, 5, warp, gk, trc);
           tc::tc_fence_after();
           if (nv > 0) load_h();
