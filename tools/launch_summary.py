@@ -34,3 +34,22 @@ for k, (c, t) in sorted(agg.items(), key=lambda a: -a[1][1]):
 print("\n# per launch (us)")
 for i, k, t in lst:
     print(f"{i:>4s} {k:44s} {t:9.1f}")
+
+# one timed step of bench.py (the launches between the first two L2 flushes: the value's pass --
+# gp_fit + ei_score_argmax; the later passes of the same run time e2e, e2e_suggest, score-only and
+# gp_posterior, whose kernels appear in the totals above)
+groups, cur, seen = [], [], False
+for i, k, t in lst:
+    if k.startswith("[torch]"):
+        if seen:
+            groups.append(cur)
+        cur, seen = [], True
+    elif seen:
+        cur.append((k, t))
+if groups:
+    g = groups[0]
+    st = sum(t for _, t in g)
+    print("\n# one timed step (first flush-delimited group): kernel, us, share of the step")
+    for k, t in g:
+        print(f"  {k:44s} {t:9.1f} {100 * t / st:6.1f}%")
+    print(f"  {'total':44s} {st:9.1f}")
