@@ -137,3 +137,38 @@ def test_replay_teacher_forced(G):
         v = ref.sample_values(seed, 0, it, [int(idx[0])]).astype(np.int64)
         X = np.concatenate([X, ref.encode_values(v.astype(float))])
         y = np.concatenate([y, rttddft.objective(v, params)])
+
+
+@pytest.mark.parametrize("n_dup", [1, 400])
+def test_dedup_with_a_full_hash_table(G, n_dup):
+    """The generator's dedup (space.cu: a shared-memory hash table of the training encodings,
+    exact comparison on hash hits) with up to 500 training rows, n_dup of them equal to
+    candidates of this call: no masked candidate is suggested, and the suggestion is the oracle's
+    argmax over the unmasked candidates (R14 / S:L432; R11 where the gap is decisive)."""
+    gpbo, ctx = G
+    sp = gpbo.Space(ctx, MIXED, MIXED_BLOCKS)
+    ref = osp.Space(MIXED, MIXED_BLOCKS)
+    seed, it, M = 5, 3, 4096
+    cand = ref.sample(seed, 0, it, np.arange(M))
+    g = np.random.default_rng(n_dup)
+    dup = np.sort(g.choice(M, n_dup, replace=False))
+    X = np.concatenate([g.random((500 - n_dup, ref.dim)).astype(np.float32), cand[dup]])
+    y = g.standard_normal(500)
+    y[500 - n_dup:] -= 1.0  # the duplicated configurations are among the best observations
+    ls = np.full(ref.dim, 0.5, np.float32)
+    m = ctx.fit([500], [ref.dim], np.ascontiguousarray(X.ravel()), y, ls, np.ones(1, np.float32),
+                np.full(1, 1e-4, np.float32))
+    idx, _, _ = gpbo.suggest(ctx, m, [sp], [M], seed, it, dedup=True)
+    om = gp.fit(X, y, ls, 1.0, 1e-4)
+    mu, var = gp.posterior(om, cand)
+    ei = gp.expected_improvement(mu, var, om.best)
+    masked = np.zeros(M, bool)
+    for r in X:  # the oracle's definition: exact equality with any observed configuration
+        masked |= np.all(cand == r, axis=1)
+    assert masked.sum() == n_dup
+    ei[masked] = -1.0
+    assert not masked[int(idx[0])]
+    srt = np.sort(ei)[::-1]
+    if (srt[0] - srt[1]) > 1e-3 * srt[0]:
+        assert int(idx[0]) == int(np.argmax(ei))
+    m.free()
