@@ -293,6 +293,8 @@ def main():
                     help="candidates the CPU oracle scores for cpu_baseline (~10-15 s at config 2)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: fixed candidates per GPU; strong: the config's M split over N")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the configs 1/3/4/5 sub-runs summarised in the config-2 line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -603,10 +605,46 @@ def main():
         if line["posterior"]:
             pr = line["posterior"]["roofline"]
             pr["frac"] = pr["achieved"] / pr["peak"]
+        if (args.config == 2 and world == 1 and args.layout == "uniform" and
+                args.scaling == "weak" and not args.no_other_configs):
+            line["other_configs"] = other_configs(args)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs(args):
+    """The other BASELINE configs measured in the same run (sub-processes of this script on the
+    same GPU, after this run's own timing): per config the bench line's value, step time,
+    breakdown, roofline fraction and clocks -- so the driver-run line covers configs 1-5."""
+    import subprocess
+    out = {}
+    for c, extra in ((1, []), (3, []), (4, []), (5, ["--steps", "100"])):
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", str(c), "--warmup", "3",
+               "--no-cpu-baseline", "--no-other-configs"]
+        cmd += extra if extra else ["--steps", str(min(args.steps, 20))]
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+            j = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+        except Exception as e:  # a failed sub-run is reported, not fatal
+            out[f"cfg{c}"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+            continue
+        roof = j.get("roofline") or {}
+        out[f"cfg{c}"] = {
+            "workload": (j.get("config") or {}).get("workload"),
+            "value": j.get("value"), "unit": j.get("unit"), "ms_per_step": j.get("ms_per_step"),
+            "steps": j.get("steps"),
+            "breakdown_ms_per_step": j.get("breakdown_ms_per_step"),
+            "roofline_frac": roof.get("frac"), "roofline_bound": roof.get("bound"),
+            "score_only": (j.get("score_only") or {}).get("value"),
+            "e2e": (j.get("e2e") or {}).get("value"),
+            "e2e_suggest": (j.get("e2e_suggest") or {}).get("value"),
+            "refined_per_step": j.get("refined_per_step"),
+            "clocks": j.get("clocks"), "gpu_launches": j.get("gpu_launches")}
+    return out
 
 
 def main_replay(args, world, rank, local):
