@@ -161,3 +161,33 @@ def test_precise_mean_tier_bo_layout(G):
     assert ctx.last_refine_count < 4096 and ctx.last_violations == 0, ctx.last_refine_count
     H.check_argmax(gp.score(om, w.Xstar[0]), int(idx[0]), "bo-tier")
     m.free()
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_full_bench_shape_sampled_oracle(G, cfg):
+    """The bench's exact shapes (config 2: 2^20 candidates, config 3: 64 searches x 2^18 -- the
+    4-deep-ring kMerged kernel --, config 4: the 2^19 per-GPU shard), checked against the oracle
+    on outputs it can compute one by one: every search's returned EI equals the oracle's EI of the
+    returned candidate (T1), no candidate of a 2,048-row random sample (plus its index neighbours)
+    has a larger oracle EI beyond T1, and no bracket violation occurred."""
+    gpbo, ctx = G
+    w = gen.make(cfg, M=(1 << 19) if cfg == 4 else None)  # config 4: bench's per-GPU shard
+    m = ctx.fit(*H.pack(w), kernel=w.kernel)
+    Xs, off = H.pack_candidates(w)
+    idx, ei = ctx.score_argmax(m, Xs, off)
+    assert ctx.last_violations == 0
+    oms = H.oracle_fits(w)
+    g = np.random.default_rng(cfg)
+    for s in range(w.S):
+        om, X = oms[s], w.Xstar[s]
+        i = int(idx[s])
+        assert 0 <= i < X.shape[0], (cfg, s, i)
+        mu, var = gp.posterior(om, X[i:i + 1])
+        e_win = float(gp.expected_improvement(mu, var, om.best)[0]) * om.std  # raw units
+        assert abs(float(ei[s]) - e_win) <= 1e-4 * abs(e_win) + 1e-30, (cfg, s, float(ei[s]), e_win)
+        smp = np.unique(np.concatenate([g.choice(X.shape[0], 2048, replace=False),
+                                        np.clip([i - 1, i + 1], 0, X.shape[0] - 1)]))
+        mu, var = gp.posterior(om, X[smp])
+        e_smp = gp.expected_improvement(mu, var, om.best) * om.std
+        assert float(e_smp.max()) <= e_win * (1 + 1e-4) + 1e-30, (cfg, s, float(e_smp.max()), e_win)
+    m.free()
