@@ -293,6 +293,10 @@ def main():
                     help="candidates the CPU oracle scores for cpu_baseline (~10-15 s at config 2)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: fixed candidates per GPU; strong: the config's M split over N")
+    ap.add_argument("--shard", default="candidates", choices=["candidates", "searches"],
+                    help="candidates: every rank scores a slice of every search, one all-reduce "
+                         "of the keys (H10); searches: rank r takes searches r, r + N, ... whole "
+                         "(no collective; the SURVEY.md §8(e) ablation for config 3)")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip the configs 1/3/4/5 sub-runs summarised in the config-2 line")
     args = ap.parse_args()
@@ -352,17 +356,26 @@ def main():
     from paper_2403_08131_b200 import gpbo
 
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.shard == "candidates":
         obj = [gpbo.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
-    ctx = gpbo.Context(device=local, stream=stream, nranks=world, rank=rank, nccl_id=nccl_id)
+    shard_s = args.shard == "searches"
+    ctx = gpbo.Context(device=local, stream=stream, nranks=1 if shard_s else world,
+                       rank=0 if shard_s else rank, nccl_id=nccl_id)
     ctx.set_score_impl(args.score_impl)
 
     # ---- inputs (seeded, host -> HBM once, untimed)
     M_total = M0 if args.scaling == "strong" else per_gpu * world
-    w = gen.make(args.config, M=M_total, rank=rank, world=world, layout=args.layout)
+    if shard_s:  # whole searches per rank: the config's full pool of each of its searches
+        M_total = M0
+        ids = list(range(rank, S0, world))
+        if not ids:
+            raise SystemExit(f"--shard searches: rank {rank} has no search (S = {S0} < N)")
+        w = gen.make(args.config, M=M0, layout=args.layout, search_ids=ids)
+    else:
+        w = gen.make(args.config, M=M_total, rank=rank, world=world, layout=args.layout)
     S = w.S
     n = [s.X.shape[0] for s in w.searches]
     d = [s.X.shape[1] for s in w.searches]
@@ -559,12 +572,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": T_dev / args.steps,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "higher_is_better": True,
+            "scaling": "strong" if shard_s else args.scaling, "vs_baseline": None,
             "dtype": ("f16x3+f32+f64" if impl_used.startswith("tcgen05") else
                       "f64" if impl_used == "fp64-direct" else "f32+f64"),
             "data": "synthetic",
             "config": {"workload": gen.CONFIG_NAMES[args.config], "S": S, "n": n0, "d": d0,
-                       "M_per_gpu": per_gpu, "M_global": M_total,
+                       "M_per_gpu": per_gpu, "M_global": M_total, "shard": args.shard,
                        "candidates_per_step": global_cands,
                        "kernel": "matern52" if w.kernel == 1 else "rbf",
                        "layout": args.layout, "l2": "flushed between steps (256 MiB write)",

@@ -70,3 +70,15 @@ def test_sharding_reproduces_global_rows():
             assert w.m_global_base[0] == min(1000, r * -(-1000 // world))
             rows.append(w.Xstar[0])
         assert np.array_equal(np.concatenate(rows), full.Xstar[0])
+
+
+def test_search_subset_is_identical_to_the_full_draw():
+    """Search-sharded runs (bench.py --shard searches) draw searches r, r + N, ... with the same
+    training sets and candidates as the full workload."""
+    full = gen.make(3, M=256)
+    sub = gen.make(3, M=256, search_ids=[1, 5, 9])
+    for k, s in enumerate([1, 5, 9]):
+        a, b = full.searches[s], sub.searches[k]
+        assert np.array_equal(a.X, b.X) and np.array_equal(a.y, b.y)
+        assert np.array_equal(a.lengthscale, b.lengthscale) and a.sf2 == b.sf2 and a.sn2 == b.sn2
+        assert np.array_equal(full.Xstar[s], sub.Xstar[k])

@@ -119,13 +119,15 @@ def lattice64():
 
 
 def make(cfg, n=None, d=None, M=None, S=None, layout="uniform", kernel=MATERN52,
-         with_candidates=True, rank=0, world=1):
+         with_candidates=True, rank=0, world=1, search_ids=None):
     """Generate config ``cfg`` (optionally shrunk for parity tests).
 
     Candidates are sharded contiguously: rank r of ``world`` gets global rows
     [r*ceil(M/world), min(M, (r+1)*ceil(M/world))) of every search.  The rows
     are drawn from the search's X* stream in global order, so every sharding sees the same
-    candidates.
+    candidates.  ``search_ids`` selects a subset of the searches (search-sharded runs: rank r
+    takes searches r, r + world, ...); each search is drawn from its own streams, identical to
+    its draw in the full workload.
     """
     S0, n0, d0, M0 = CONFIG_SHAPES[cfg]
     S = S0 if S is None else S
@@ -133,7 +135,7 @@ def make(cfg, n=None, d=None, M=None, S=None, layout="uniform", kernel=MATERN52,
     d = d0 if d is None else d
     M = M0 if M is None else M
     searches, Xs, bases, Mg = [], [], [], []
-    for s in range(S):
+    for s in (range(S) if search_ids is None else search_ids):
         g = rng(cfg, 0, s)
         if cfg == 3 and s % 4 == 3:
             X = g.random((n, d), dtype=np.float32)
