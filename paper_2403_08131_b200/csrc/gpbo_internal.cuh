@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/gpbo.h"
+#include "../../include/gpbo_test.h"
 
 namespace gpbo {
 

@@ -1,5 +1,6 @@
 """CPU checks of the boundary: libgpbo.so loads and exports every entry point include/gpbo.h
-declares (no compute calls -- there is no GPU here)."""
+and include/gpbo_test.h (the test / diagnostic hooks) declare (no compute calls -- there is no
+GPU here)."""
 import ctypes
 import os
 import re
@@ -10,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "gpbo.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("gpbo.h", "gpbo_test.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, re.M))
 
