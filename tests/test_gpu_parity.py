@@ -53,6 +53,26 @@ def test_fit_matches_oracle(G, n, d, kernel):
     np.testing.assert_allclose(a, om.alpha, rtol=0, atol=1e-7 * np.abs(om.alpha).max())
 
 
+@pytest.mark.parametrize("ns", [[230, 17, 400], [217, 8, 1, 300, 64]])
+def test_mixed_fit_batch_on_the_cluster_kernel(G, ns):
+    """A batch whose largest search has n > 216 runs every search on the cluster fit (multicast G
+    rows, per-search staging, CTAs that own no row of a small search): each search matches the
+    oracle as in test_fit_matches_oracle, and its LML the oracle's."""
+    w = gen.random_case(77 + len(ns), ns, [5 + (i % 3) for i in range(len(ns))], 4)
+    m = _fit(G, w)
+    oms = H.oracle_fits(w)
+    lml = m.lml()
+    for s, om in enumerate(oms):
+        assert m.status[s] in (0, 3) and m.jitter_k[s] == om.jitter_k, s
+        L, Li, a = m.export(s)
+        np.testing.assert_allclose(L, om.L, rtol=0, atol=1e-12 * np.abs(om.L).max())
+        Li_ref = np.linalg.inv(om.L)
+        np.testing.assert_allclose(Li, Li_ref, rtol=0, atol=1e-9 * np.abs(Li_ref).max())
+        np.testing.assert_allclose(a, om.alpha, rtol=0, atol=1e-7 * np.abs(om.alpha).max())
+        from oracle import ml2 as oml2
+        assert abs(lml[s] - oml2.lml(om)) <= 1e-9 * max(1.0, abs(lml[s])), s
+
+
 def test_fit_jitter_escalation_and_failures(G):
     gpbo, ctx = G
     rng = np.random.default_rng(0)
