@@ -65,6 +65,10 @@ struct gpbo_ctx {
   // copy_stream while the tcgen05 kernel scores the previous chunk on `stream`
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t feed_ev[8] = {};
+  // bo_suggest_batch draws its candidates on gen_stream, overlapping a pending fit on `stream`:
+  // xready_ev marks the latest Gram pre-pass (which copies X into the model, the dedup's input)
+  cudaStream_t gen_stream = nullptr;
+  cudaEvent_t gen_ev = nullptr, xready_ev = nullptr;
   int score_impl = 0;       // 0 = auto (tcgen05 where supported), 1 = SIMT, 2 = tcgen05,
                             // 3 = tcgen05 with the streamed image layout forced at fit time,
                             // 4 = float64 direct kernel (n <= 64)
@@ -668,6 +672,12 @@ gpbo_status gpbo_ctx_destroy(gpbo_ctx *ctx) {
   }
   for (auto &e : ctx->feed_ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->gen_stream) {
+    cudaStreamSynchronize(ctx->gen_stream);
+    cudaStreamDestroy(ctx->gen_stream);
+  }
+  if (ctx->gen_ev) cudaEventDestroy(ctx->gen_ev);
+  if (ctx->xready_ev) cudaEventDestroy(ctx->xready_ev);
   if (ctx->stage_d) cudaFree(ctx->stage_d);
   if (ctx->aux_d) cudaFree(ctx->aux_d);
   if (ctx->aux_h) cudaFreeHost(ctx->aux_h);
@@ -938,6 +948,9 @@ gpbo_status fit_impl(gpbo_ctx *ctx, const gpbo_fit_args *a, gpbo_model **out, bo
   {
     KernTimer t(ctx, kKernFit);
     CKM(gpbo::launch_gram(meta_in, S, m->nmax, m->dmax, io, ctx->stream));
+    // the model's X32 is complete once the pre-pass has run (bo_suggest_batch's dedup reads it)
+    if (!ctx->xready_ev) CKM(cudaEventCreateWithFlags(&ctx->xready_ev, cudaEventDisableTiming));
+    CKM(cudaEventRecord(ctx->xready_ev, ctx->stream));
     // the factorisation: a cluster of Cc CTAs per search (fit_cluster.cu) -- as many CTAs per
     // search as the SMs allow (~148 / S), and enough that the distributed working matrix fits in
     // their shared memory; GPBO_FIT=single selects the one-CTA kernel (fit.cu) for A/B runs
@@ -1467,13 +1480,23 @@ gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
   gpbo_status st = ensure_stage(ctx, (size_t)xoff[S] * 4 + 16);
   if (st) return st;
   float *X = (float *)ctx->stage_d;
+  // H5 on a side stream: the generator needs only the space and (for the dedup) the model's
+  // training rows, ready after the Gram pre-pass -- so it runs on the SMs the (one-CTA per
+  // search) fit leaves idle, and the scoring waits for both
+  if (!ctx->gen_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->gen_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->gen_ev, cudaEventDisableTiming));
+  }
+  if (ctx->xready_ev) CK(cudaStreamWaitEvent(ctx->gen_stream, ctx->xready_ev, 0));
   for (int s = 0; s < S; ++s) {
     const SearchMeta &q = model->meta[s];
     CK(gpbo::launch_gen(gpbo::space_dev(spaces[s]), seed, (uint32_t)s, (uint32_t)iteration,
                         base[s], off[s + 1] - off[s], X + xoff[s],
-                        dedup ? model->X32 + q.x_off : nullptr, q.n, ctx->stream));
+                        dedup ? model->X32 + q.x_off : nullptr, q.n, ctx->gen_stream));
     ctx->launches += 1;
   }
+  CK(cudaEventRecord(ctx->gen_ev, ctx->gen_stream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->gen_ev, 0));
   std::vector<float> eiv(S);
   st = argmax_tail(ctx, model, X, off.data(), base.data(), best_std.data(), idx, eiv.data());
   if (st) return st;

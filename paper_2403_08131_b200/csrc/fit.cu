@@ -162,10 +162,7 @@ __device__ __forceinline__ void fit_body(double *sm, double *red,
   // inputs into the model when they come from the caller's device arrays
   const bool copy = io.X_src != io.X32;
   int bad = 0;
-  for (int i = tid; i < n * d; i += kFitThreads) {
-    bad |= !isfinite(X[i]);
-    if (copy) io.X32[m.x_off + i] = X[i];
-  }
+  for (int i = tid; i < n * d; i += kFitThreads) bad |= !isfinite(X[i]);  // (copied by the pre-pass)
   for (int i = tid; i < n; i += kFitThreads) {
     bad |= !isfinite(y[i]);
     if (copy) io.y64[m.y_off + i] = y[i];
@@ -762,10 +759,16 @@ gram_kernel(const SearchMeta *__restrict__ meta, const FitIO io) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if ((int)blockIdx.x * 128 < n) {
     const int i = blockIdx.x * 128 + threadIdx.x;
+    // the caller's device X is copied into the model here (not in the fit kernel): X32 is then
+    // complete when this grid is, and bo_suggest_batch's generator can start on another stream
+    // while the factorisation runs (api.cu xready_ev)
+    const bool copy = io.X_src != io.X32;
     double q = 0.0;
     if (i < n)
       for (int c = 0; c < d; ++c) {
-        const double v = (double)X[i * d + c] / (double)ls[c];
+        const float xv = X[i * d + c];
+        if (copy) io.X32[m.x_off + i * d + c] = xv;
+        const double v = (double)xv / (double)ls[c];
         io.Xs64[m.x_off + (size_t)c * n + i] = v;
         q += v * v;
       }

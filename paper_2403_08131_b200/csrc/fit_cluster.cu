@@ -159,10 +159,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   // ---- validation (every CTA; CTA 0 copies the caller's device inputs into the model)
   const bool copy = io.X_src != io.X32 && c == 0;
   int bad = 0;
-  for (int i = tid; i < n * d; i += kFitThreads) {
-    bad |= !isfinite(X[i]);
-    if (copy) io.X32[m.x_off + i] = X[i];
-  }
+  for (int i = tid; i < n * d; i += kFitThreads) bad |= !isfinite(X[i]);  // (X: copied by the pre-pass)
   for (int i = tid; i < n; i += kFitThreads) {
     bad |= !isfinite(y[i]);
     if (copy) io.y64[m.y_off + i] = y[i];
