@@ -26,6 +26,9 @@ namespace gpbo {
 namespace {
 
 constexpr int kChunk = 64;
+#ifndef GPBO_M64_RSQ32  // float32-seeded sqrt in kval64: measured slower (1.28 -> 1.35 ms), off
+#define GPBO_M64_RSQ32 0
+#endif
 constexpr int kExpTab = 1024;  // e^{-k/16}, k < 1024 (arguments >= 64: e^-64 ~ 1.6e-28 -> 0)
 
 // e^{-s} for s >= 0 in float64: s = k/16 + f, f in [0, 1/16): e^{-k/16} from the table times a
@@ -52,7 +55,18 @@ __device__ __forceinline__ double exp_neg(double s, const double *tab) {
 __device__ __forceinline__ double sqrt_nr(double r2) {
   if (!(r2 > 0.0)) return r2 == 0.0 ? 0.0 : r2;  // 0 -> 0, NaN -> NaN
   double y;
+#if GPBO_M64_RSQ32
+  // float32 MUFU estimate (~2^-22; the float64 MUFU path is slower) when r2 is in float range
+  if (r2 > 1e-30 && r2 < 1e30) {
+    float yf;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"((float)r2));
+    y = (double)yf;
+  } else {
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  }
+#else
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#endif
 #pragma unroll
   for (int i = 0; i < 2; ++i) y = fma(0.5 * y, fma(-r2, y * y, 1.0), y);
   const double r = r2 * y;
@@ -135,12 +149,153 @@ mean64_kernel(const ScoreLaunch p, const double *__restrict__ Xs64, const double
   }
 }
 
+// The same precise mean with the GEMM-form distances on the FP64 tensor cores (measured: config 2
+// BO layout 1.50 -> 1.28 ms, config 4 BO 4.60 -> 3.22 ms; the kernel values on the FP64 pipe,
+// latency-bound chains, are the rest): a CTA (8 warps)
+// per scoring tile of <= 128 candidates, the training points in chunks of 64 staged in shared
+// memory (x_j / l, |x_j / l|^2, alpha_j); warp w owns candidate blocks w and w + 8 (8 rows each):
+// per 8-point block one DMMA m8n8k4 chain over the dimensions (the point block's B fragments
+// shared by both candidate blocks) gives x* . x_j, then each lane evaluates the kernel for its
+// (candidate, 2 points) and accumulates k alpha; lanes of a candidate reduce in a fixed order.
+// The O(n d) distance work leaves the FP64 (DFMA) pipe for the tensor pipe; the kernel values
+// stay on the FP64 pipe.
+constexpr int kM64Warps = 8;
+
+__device__ __forceinline__ void dmma64(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// row stride (doubles) >= d4 with stride = 4 (mod 8): a fragment load (rows gid < 4 of a
+// half-warp, columns tig) hits distinct banks
+__host__ __device__ __forceinline__ int m64_ld(int d4) { return (d4 % 8 == 4) ? d4 : d4 + 4; }
+
+__global__ void __launch_bounds__(32 * kM64Warps)
+mean64_dmma_kernel(const ScoreLaunch p, const double *__restrict__ Xs64,
+                   const double *__restrict__ etab, int tile, int tile_lo, int tiles, int dmax,
+                   double *mean64) {
+  extern __shared__ __align__(16) double msm[];
+  const int d4max = (dmax + 3) / 4 * 4, ld = m64_ld(d4max);
+  double *tab = msm;                         // [kExpTab]
+  double *xa = tab + kExpTab;                // [128][ld]   candidates x* / l
+  double *xb = xa + 128 * ld;                // [kChunk][ld] training points x_j / l
+  double *qb = xb + kChunk * ld;             // [kChunk]    |x_j / l|^2
+  double *ab = qb + kChunk;                  // [kChunk]    alpha_j
+  double *qa = ab + kChunk;                  // [128]       |x* / l|^2
+  bool any = false;
+  for (int i = 0; i < p.S && !any; ++i)
+    any = p.meta[i].mean_tier && (p.meta[i].status == GPBO_OK || p.meta[i].status == GPBO_WDEGENERATE);
+  if (!any) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int e = tid; e < kExpTab; e += 32 * kM64Warps) tab[e] = etab[e];
+  for (int t = tile_lo + (int)blockIdx.x; t < tile_lo + tiles; t += gridDim.x) {
+    const int s = search_of(p.tile_first, p.S, t);
+    const SearchMeta &m = p.meta[s];
+    if (!m.mean_tier || (m.status != GPBO_OK && m.status != GPBO_WDEGENERATE)) continue;
+    const int n = m.n, d = m.d, d4 = (d + 3) / 4 * 4;
+    const int64_t Ms = p.m_off[s + 1] - p.m_off[s];
+    const int64_t row0 = (int64_t)(t - p.tile_first[s]) * tile;
+    const int rows = (int)min((int64_t)tile, Ms - row0);
+    const float *ls = p.ls32 + m.ls_off;
+    const double *Xj = Xs64 + m.x_off;  // column-major d x n
+    const double *alpha = p.alpha64 + m.a_off;
+    const double sf2 = m.sf2;
+    __syncthreads();  // the previous tile is done with xa / qa
+    for (int e = tid; e < 128 * d4; e += 32 * kM64Warps) {
+      const int r = e / d4, c = e - r * d4;
+      xa[r * ld + c] = (r < rows && c < d)
+          ? (double)p.Xstar[p.x_off[s] + (row0 + r) * d + c] / (double)ls[c] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 128) {
+      double q = 0.0;
+      for (int c = 0; c < d; ++c) q = fma(xa[tid * ld + c], xa[tid * ld + c], q);
+      qa[tid] = q;  // (NaN inputs stay NaN through q, the distance and mu)
+    }
+    double mu[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [candidate block][point of the lane's pair]
+    for (int j0 = 0; j0 < n; j0 += kChunk) {
+      const int cnt = min(kChunk, n - j0);
+      __syncthreads();  // qa written; the previous chunk is consumed
+      for (int e = tid; e < kChunk * d4; e += 32 * kM64Warps) {
+        const int j = e / d4, c = e - j * d4;
+        xb[j * ld + c] = (j < cnt && c < d) ? Xj[(int64_t)c * n + j0 + j] : 0.0;
+      }
+      for (int j = tid; j < kChunk; j += 32 * kM64Warps) {
+        double qj = 0.0;
+        if (j < cnt)
+          for (int c = 0; c < d; ++c) {
+            const double v = Xj[(int64_t)c * n + j0 + j];
+            qj = fma(v, v, qj);
+          }
+        qb[j] = qj;
+        ab[j] = j < cnt ? alpha[j0 + j] : 0.0;
+      }
+      __syncthreads();
+      for (int J = 0; 8 * J < cnt; ++J) {
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const double *bp = xb + (8 * J + gid) * ld + tig;
+        for (int k0 = 0; k0 < d4; k0 += 4) {
+          const double b = bp[k0];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cb = warp + kM64Warps * h;
+            dmma64(acc[h][0], acc[h][1], xa[(8 * cb + gid) * ld + k0 + tig], b);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cb = warp + kM64Warps * h;
+          const double q = qa[8 * cb + gid];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = 8 * J + 2 * tig + u;
+            if (j < cnt) {
+              double r2 = q + qb[j] - 2.0 * acc[h][u];
+              r2 = r2 < 0.0 ? 0.0 : r2;  // (NaN propagates)
+              mu[h][u] = fma(kval64(r2, sf2, m.kernel, tab), ab[j], mu[h][u]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = mu[h][0] + mu[h][1];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      const int r = 8 * (warp + kM64Warps * h) + gid;
+      if (tig == 0 && r < rows) mean64[p.m_off[s] + row0 + r] = v;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, int tile_lo,
                           int tiles, int dmax, double *mean64, const double *etab, int num_sms,
                           cudaStream_t stream) {
   if (tiles <= 0) return cudaSuccess;
+#ifndef GPBO_MEAN64_DMMA
+#define GPBO_MEAN64_DMMA 1
+#endif
+  if (GPBO_MEAN64_DMMA && tile <= 128) {
+    const int d4max = (dmax + 3) / 4 * 4, ld = m64_ld(d4max);
+    const size_t smem = ((size_t)kExpTab + 128 * ld + kChunk * ld + 2 * kChunk + 128) * sizeof(double);
+    static int attr_done = 0;  // (per process; the attribute is set at the largest size once)
+    if (smem > 48 * 1024 && attr_done < (int)smem) {
+      cudaError_t e = cudaFuncSetAttribute(mean64_dmma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr_done = 227 * 1024;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mean64_dmma_kernel, 32 * kM64Warps, smem);
+    const int grid = std::min(tiles, num_sms * std::max(per_sm, 1));
+    mean64_dmma_kernel<<<grid, 32 * kM64Warps, smem, stream>>>(p, Xs64, etab, tile, tile_lo, tiles,
+                                                               dmax, mean64);
+    return cudaGetLastError();
+  }
   const int thr = tile <= 64 ? 64 : 128;
   const int grid = std::min(tiles, num_sms * 8);
 #define GPBO_MEAN64(D)                                                                          \
