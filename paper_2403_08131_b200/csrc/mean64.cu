@@ -17,6 +17,7 @@
 // the training points x_j / l (float64), |x_j / l|^2 and alpha_j are staged through shared
 // memory in chunks of kChunk points (broadcast reads).  Searches of the fast tier exit at once.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "gpbo_internal.cuh"
@@ -282,12 +283,17 @@ cudaError_t launch_mean64(const ScoreLaunch &p, const double *Xs64, int tile, in
   if (GPBO_MEAN64_DMMA && tile <= 128) {
     const int d4max = (dmax + 3) / 4 * 4, ld = m64_ld(d4max);
     const size_t smem = ((size_t)kExpTab + 128 * ld + kChunk * ld + 2 * kChunk + 128) * sizeof(double);
-    static int attr_done = 0;  // (per process; the attribute is set at the largest size once)
-    if (smem > 48 * 1024 && attr_done < (int)smem) {
+    // the attribute is per device (one ctx per device may run in one process, on different
+    // threads): a per-device flag, set once at the largest size
+    static std::atomic<int> attr_done[64];
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    if (smem > 48 * 1024 && (dev < 0 || dev >= 64 || !attr_done[dev].load())) {
       cudaError_t e = cudaFuncSetAttribute(mean64_dmma_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
-      attr_done = 227 * 1024;
+      if (dev >= 0 && dev < 64) attr_done[dev].store(1);
     }
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mean64_dmma_kernel, 32 * kM64Warps, smem);
