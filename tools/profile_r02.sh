@@ -7,7 +7,7 @@ o=gpurun_out
 mkdir -p $o
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,noheader > $o/${tag}_gpu.txt
 # bench lines first (clean clocks, no profiler)
-timeout 600 python bench.py > $o/${tag}_bench_cfg2.json 2> $o/${tag}_bench_cfg2.err
+timeout 600 python bench.py --no-other-configs > $o/${tag}_bench_cfg2.json 2> $o/${tag}_bench_cfg2.err
 timeout 900 python bench.py --impl reference > $o/${tag}_reference_cfg2.json 2>&1
 for c in 1 3 4; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > $o/${tag}_bench_cfg$c.json 2> $o/${tag}_bench_cfg$c.err
@@ -22,12 +22,12 @@ rm -f $o/${tag}_posterior_bench.jsonl
 for c in 2 3 4; do timeout 300 python tools/posterior_bench.py $c >> $o/${tag}_posterior_bench.jsonl 2>&1; done
 # launch list of the default step (cold-cache, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $o/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
+    --log-file $o/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs \
     > $o/${tag}_launches_bench.log 2>&1
 cap() {  # name regex args...
   local name=$1 re=$2; shift 2
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$re -s 3 -c 1 \
-      -o $o/${tag}_$name python bench.py --steps 1 --warmup 3 --no-cpu-baseline "$@" \
+      -o $o/${tag}_$name python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-other-configs "$@" \
       > $o/${tag}_$name.log 2>&1
 }
 cap score_tc 'score_tc_kernel'
