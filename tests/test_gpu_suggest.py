@@ -172,3 +172,39 @@ def test_dedup_with_a_full_hash_table(G, n_dup):
     if (srt[0] - srt[1]) > 1e-3 * srt[0]:
         assert int(idx[0]) == int(np.argmax(ei))
     m.free()
+
+
+def test_suggest_right_after_an_async_device_fit(G):
+    """bo_suggest_batch draws its candidates on a side stream that waits only for the latest Gram
+    pre-pass (which copies the caller's device X into the model -- the dedup's input): after an
+    asynchronous fit from device arrays, with training rows that equal candidates of the call,
+    the masked set and the suggestion must still be the oracle's, on every one of several
+    back-to-back fits (a stale or unfinished X copy would leak a duplicate or mask a wrong row)."""
+    import torch
+    gpbo, ctx = G
+    sp = gpbo.Space(ctx, MIXED, MIXED_BLOCKS)
+    ref = osp.Space(MIXED, MIXED_BLOCKS)
+    M = 4096
+    dev = torch.device("cuda", 0)
+    for rep in range(4):
+        seed, it = 21 + rep, rep
+        cand = ref.sample(seed, 0, it, np.arange(M))
+        g = np.random.default_rng(100 + rep)
+        dup = np.sort(g.choice(M, 150, replace=False))
+        X = np.concatenate([g.random((50, ref.dim)).astype(np.float32), cand[dup]])
+        y = g.standard_normal(200)
+        y[50:] -= 1.5
+        ls = np.full(ref.dim, 0.5, np.float32)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        m = ctx.fit([200], [ref.dim], t(X.ravel()), t(y), t(ls), t(np.ones(1, np.float32)),
+                    t(np.full(1, 1e-4, np.float32)), wait=False)
+        idx, _, _ = gpbo.suggest(ctx, m, [sp], [M], seed, it, dedup=True)
+        om = gp.fit(X, y, ls, 1.0, 1e-4)
+        mu, var = gp.posterior(om, cand)
+        ei = gp.expected_improvement(mu, var, om.best)
+        ei[dup] = -1.0
+        assert int(idx[0]) not in set(dup.tolist()), rep
+        srt = np.sort(ei)[::-1]
+        if (srt[0] - srt[1]) > 1e-3 * srt[0]:
+            assert int(idx[0]) == int(np.argmax(ei)), rep
+        m.free()
