@@ -875,7 +875,14 @@ int fit_cluster_size(const gpbo_ctx *ctx, int S, int nmax) {
   // n > 216 the one-CTA kernel streams W through L2 and the cluster wins (n = 500: 1.27 -> 0.68 ms)
   if (single || (nmax <= gpbo::kFitSmemMaxN && !force_cluster)) return 0;
   const int per = ctx->num_sms / std::max(S, 1);
-  int Cc = per >= 8 ? 8 : per >= 4 ? 4 : per >= 2 ? 2 : 1;
+  int Cc = per >= 16 ? 16 : per >= 8 ? 8 : per >= 4 ? 4 : per >= 2 ? 2 : 1;
+  static const int cc_cap = [] {  // A/B: cap the cluster size (GPBO_FIT_CC=1|2|4|8|16)
+    const char *e = getenv("GPBO_FIT_CC");
+    return e ? atoi(e) : 16;
+  }();
+  if (cc_cap >= 1 && cc_cap < Cc) Cc = cc_cap;
+  // 16-CTA (non-portable) clusters: only where the device can hold one at this size
+  if (Cc == 16 && !gpbo::fit_cluster16_ok(gpbo::fit_cluster_smem(nmax, 16))) Cc = 8;
   while (Cc < 8 && gpbo::fit_cluster_smem(nmax, Cc) > gpbo::kFitSmemBudget) Cc *= 2;
   return gpbo::fit_cluster_smem(nmax, Cc) <= gpbo::kFitSmemBudget ? Cc : 0;
 }

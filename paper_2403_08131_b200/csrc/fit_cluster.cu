@@ -1,4 +1,4 @@
-// H2-H4 on a thread-block cluster: the fit of one sub-search spread over Cc CTAs (Cc <= 8, one
+// H2-H4 on a thread-block cluster: the fit of one sub-search spread over Cc CTAs (Cc <= 16, one
 // cluster per search), float64 throughout.  PAPER.md L249/L256 (§IV.D): the GP's O(N^3) training.
 //
 // Same blocked elimination as fit.cu ([K | I] -> [L^T | L^-1] on 8 x 8 tiles, DMMA m8n8k4; the
@@ -37,7 +37,7 @@ namespace {
 namespace cg = cooperative_groups;
 constexpr int kWarps = kFitThreads / 32;
 constexpr int kQ = 4;       // tiles of one tile row per trailing-update item
-constexpr int kMaxCc = 8;   // portable cluster size
+constexpr int kMaxCc = 16;  // 8 portable, 16 with the non-portable attribute
 
 #ifdef GPBO_FIT_TIMING  // phase clocks of CTA (0, owner) printed at exit (tools/fit_phases.py)
 #define FCT(slot) do { if (tid == 0) { const long long t_ = clock64(); ft[slot] += t_ - ft0; ft0 = t_; } } while (0)
@@ -693,6 +693,34 @@ int fit_cluster_smem(int n, int Cc) {
   return (2 * fit_nr8(n) + 24 + 4 * 64 + 2 * 8 * fit_nr8(n) + tiles * 64) * 8;
 }
 
+// whether clusters of 16 CTAs with `smem_bytes` each can be resident on this device
+bool fit_cluster16_ok(int smem_bytes) {
+  if (cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16);
+  cfg.blockDim = dim3(kFitThreads);
+  cfg.dynamicSmemBytes = (size_t)smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, fit_cluster_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return nclusters > 0;
+}
+
 cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem_bytes,
                                const FitIO &io, SearchMeta *meta_out, cudaStream_t stream) {
   static std::atomic<int> smem_set[64];
@@ -708,6 +736,10 @@ cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem
       while (smem_bytes > cur && !smem_set[dev].compare_exchange_weak(cur, smem_bytes)) {
       }
     }
+  }
+  if (Cc > 8) {  // 16-CTA clusters are non-portable: opt in (once per device, like the smem)
+    e = cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S * Cc);

@@ -182,6 +182,7 @@ cudaError_t launch_fit(const SearchMeta *meta_d, int S, int smem_bytes, const Fi
                        SearchMeta *meta_out, cudaStream_t stream, bool pdl);
 // Cluster fit (fit_cluster.cu): Cc CTAs per search, the working matrix in their shared memory.
 int fit_cluster_smem(int n, int Cc);
+bool fit_cluster16_ok(int smem_bytes);
 cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem_bytes,
                                const FitIO &io, SearchMeta *meta_out, cudaStream_t stream);
 cudaError_t launch_simt_operands(const SearchMeta *meta_d, int S, const float *X32,
