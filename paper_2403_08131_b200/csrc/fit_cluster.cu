@@ -378,6 +378,9 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   double jit = 0.0, p10 = 1.0;
   for (int k = 0; k < 7 && jk < 0; ++k, p10 *= 10.0) {
     jit = 1e-8 * p10 * sf2;
+    // a restart of the ladder: every CTA has read the failing D's flag (and left the failed
+    // sweep) before CTA 0's new maps(0) can overwrite its maps block
+    if (k > 0) cluster.sync();
     __syncthreads();
     // H2: own rows' kernel tiles from the pre-pass, + sn2 + jitter on the diagonal
     for (int lr = 0; lr < nown; ++lr) {
