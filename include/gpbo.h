@@ -231,14 +231,19 @@ gpbo_status ei_score_argmax(gpbo_ctx *ctx, const gpbo_model *model, const float 
  *   GPBO_P_INT         lo..hi (step 1)     encoded (v - lo)/(hi - lo)
  *   GPBO_P_ORDINAL     K numeric values    encoded rank/(K-1) (K = 1 -> 0)
  *   GPBO_P_CATEGORICAL K labels 0..K-1     encoded one-hot (K columns)
+ *   GPBO_P_FIXED       the value lo        no encoded column, draws nothing (a parameter the
+ *                                          interdependence plan does not tune in this search:
+ *                                          fixed at its default / an earlier stage's value;
+ *                                          SPEC.md L243, L290) -- decoded as lo
  * (reading R8), plus constrained blocks: a block names >= 1 discrete parameters and lists its
  * valid value-index tuples; the generator draws one tuple uniformly (no rejection), so every
  * candidate satisfies the caller's constraints.  Encoded dimension d = number of
- * non-categorical parameters + sum of categorical K (<= GPBO_MAX_D).
+ * non-fixed, non-categorical parameters + sum of categorical K (<= GPBO_MAX_D).
  * Generator: Philox4x32-10, key = seed, word u of global candidate i of search s at iteration t
  * = output[u % 4] of Philox(ctr = (i, s, t, u / 4)), u over free parameters (declaration order)
  * then blocks; real: (w >> 8) 2^-24, K values: (u64(w >> 8) K) >> 24. */
-typedef enum { GPBO_P_REAL = 0, GPBO_P_INT = 1, GPBO_P_ORDINAL = 2, GPBO_P_CATEGORICAL = 3 }
+typedef enum { GPBO_P_REAL = 0, GPBO_P_INT = 1, GPBO_P_ORDINAL = 2, GPBO_P_CATEGORICAL = 3,
+               GPBO_P_FIXED = 4 }
     gpbo_param_kind;
 typedef struct gpbo_space gpbo_space;
 typedef struct {

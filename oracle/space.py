@@ -13,12 +13,15 @@ path (no shared code, tables or constants; only the documented algorithm):
 * Encoding (H0, S:L378, reading R8): real/int (v - lo)/(hi - lo); ordinal rank/(K - 1);
   categorical one-hot; K = 1 -> 0.  Each encoded value is computed in float64 and rounded once to
   float32.
+* Fixed parameters (SURVEY.md §8(a) H0 "fixed params dropped"; parameters a
+  search does not tune keep their default or an earlier stage's value): no encoded column, no
+  Philox word (they are not free parameters); their raw value is the given constant.
 """
 from __future__ import annotations
 
 import numpy as np
 
-REAL, INT, ORDINAL, CATEGORICAL = 0, 1, 2, 3
+REAL, INT, ORDINAL, CATEGORICAL, FIXED = 0, 1, 2, 3, 4
 
 M0, M1 = 0xD2511F53, 0xCD9E8D57
 W0, W1 = 0x9E3779B9, 0xBB67AE85
@@ -61,11 +64,12 @@ class Space:
 
     def __init__(self, params, blocks=()):
         # params: list of dicts {kind, lo, hi} (REAL/INT) or {kind, values} (ORDINAL) or
-        #         {kind, K} (CATEGORICAL)
+        #         {kind, K} (CATEGORICAL) or {kind, lo} (FIXED: the constant)
         self.params = params
         self.blocks = [(list(b["params"]), np.asarray(b["tuples"], dtype=np.int64)) for b in blocks]
         inblock = {p for ps, _ in self.blocks for p in ps}
-        self.free = [i for i in range(len(params)) if i not in inblock]
+        self.free = [i for i in range(len(params))
+                     if i not in inblock and params[i]["kind"] != FIXED]
         self.units = len(self.free) + len(self.blocks)
 
     def nvals(self, i):
@@ -80,7 +84,7 @@ class Space:
 
     @property
     def dim(self):
-        return sum(self.nvals(i) if p["kind"] == CATEGORICAL else 1
+        return sum(self.nvals(i) if p["kind"] == CATEGORICAL else 0 if p["kind"] == FIXED else 1
                    for i, p in enumerate(self.params))
 
     def words(self, seed, search, iteration, idx):
@@ -118,6 +122,8 @@ class Space:
         cols = []
         for i, p in enumerate(self.params):
             v = vals[:, i]
+            if p["kind"] == FIXED:
+                continue
             if p["kind"] == REAL:
                 cols.append(v.astype(np.float32))
             elif p["kind"] == CATEGORICAL:
@@ -141,6 +147,8 @@ class Space:
                 out[:, i] = p["lo"] + v
             elif p["kind"] == ORDINAL:
                 out[:, i] = np.asarray(p["values"], dtype=np.float64)[v.astype(np.int64)]
+            elif p["kind"] == FIXED:
+                out[:, i] = float(p["lo"])
             else:
                 out[:, i] = v
         return out

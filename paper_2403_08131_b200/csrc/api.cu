@@ -1523,6 +1523,7 @@ gpbo_status bo_suggest_batch(gpbo_ctx *ctx, const gpbo_model *model,
           if (k == GPBO_P_REAL) r = v.lo[i] + (v.hi[i] - v.lo[i]) * vals[i];
           else if (k == GPBO_P_INT) r = v.lo[i] + vals[i];
           else if (k == GPBO_P_ORDINAL) r = v.values[v.val_off[i] + (int)vals[i]];
+          else if (k == GPBO_P_FIXED) r = v.lo[i];
           x_raw[po + i] = r;
         }
       } else {

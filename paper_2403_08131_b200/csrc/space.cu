@@ -8,7 +8,7 @@
 // uniformly, free parameters are drawn independently -- no rejection loop.
 //
 // Counter-based generator: Philox4x32-10, key = (seed lo, seed hi);
-// word u (free parameters in declaration order, then blocks) of global candidate i of search s
+// word u (free parameters in declaration order -- fixed ones draw nothing --, then blocks) of global candidate i of search s
 // at iteration t = output[u % 4] of Philox(ctr = (i, s, t, u / 4)).  Real: u = (w >> 8) 2^-24;
 // K values: index (u64(w >> 8) K) >> 24; block with T tuples: tuple (u64(w >> 8) T) >> 24.
 // Encoding (H0, reading R8): real/int (v - lo)/(hi - lo), ordinal rank/(K-1),
@@ -234,7 +234,13 @@ gpbo_status gpbo_space_create(gpbo_ctx *ctx, const gpbo_space_desc *s, gpbo_spac
   int d = 0;
   for (int i = 0; i < P; ++i) {
     const int k = kind[i];
-    if (k < 0 || k > 3) return GPBO_EINVAL;
+    if (k < 0 || k > 4) return GPBO_EINVAL;
+    if (k == GPBO_P_FIXED) {  // no column, no draw: its value is lo
+      if (!std::isfinite(s->lo[i])) return GPBO_EINVAL;
+      nv[i] = 0;
+      col[i] = d;
+      continue;
+    }
     if (k == GPBO_P_REAL) {
       if (!(s->hi[i] > s->lo[i])) return GPBO_EINVAL;
       nv[i] = 0;
@@ -256,7 +262,8 @@ gpbo_status gpbo_space_create(gpbo_ctx *ctx, const gpbo_space_desc *s, gpbo_spac
     if (e <= a) return GPBO_EINVAL;
     for (int j = a; j < e; ++j) {
       const int i = s->block_params[j];
-      if (i < 0 || i >= P || kind[i] == GPBO_P_REAL || inblock[i]) return GPBO_EINVAL;
+      if (i < 0 || i >= P || kind[i] == GPBO_P_REAL || kind[i] == GPBO_P_FIXED || inblock[i])
+        return GPBO_EINVAL;
       inblock[i] = 1;
       bpar.push_back(i);
     }
@@ -284,7 +291,7 @@ gpbo_status gpbo_space_create(gpbo_ctx *ctx, const gpbo_space_desc *s, gpbo_spac
   }
   std::vector<int32_t> freel;
   for (int i = 0; i < P; ++i)
-    if (!inblock[i]) freel.push_back(i);
+    if (!inblock[i] && kind[i] != GPBO_P_FIXED) freel.push_back(i);
   std::vector<int32_t> voff(P, 0);
   std::vector<double> vals;
   for (int i = 0; i < P; ++i) {
@@ -336,6 +343,7 @@ gpbo_status gpbo_space_encode(const gpbo_space *sp, const double *raw, float *en
     const int k = v.kind[i], col = v.col[i], K = v.nv[i];
     const double x = raw[i];
     if (!std::isfinite(x)) return GPBO_EINVAL;
+    if (k == GPBO_P_FIXED) continue;  // no encoded column
     if (k == GPBO_P_REAL || k == GPBO_P_INT) {
       enc[col] = (float)((x - v.lo[i]) / (v.hi[i] - v.lo[i]));
     } else if (k == GPBO_P_ORDINAL) {

@@ -7,7 +7,7 @@
 namespace gpbo {
 
 enum { kReal = GPBO_P_REAL, kInt = GPBO_P_INT, kOrdinal = GPBO_P_ORDINAL,
-       kCategorical = GPBO_P_CATEGORICAL };
+       kCategorical = GPBO_P_CATEGORICAL, kFixed = GPBO_P_FIXED };
 
 struct SpaceView {
   int32_t P, d, nfree, nblocks;

@@ -517,7 +517,8 @@ def tc_selftest(A, B, row_bytes, b_row_off=0):
 
 class Space:
     """gpbo_space from a parameter list (dicts with kind REAL/INT {lo, hi}, ORDINAL {values},
-    CATEGORICAL {K}) and constrained blocks ({params: [...], tuples: [[value indices]...]})."""
+    CATEGORICAL {K}, FIXED {lo}: a constant, no encoded column) and constrained blocks
+    ({params: [...], tuples: [[value indices]...]})."""
 
     def __init__(self, ctx, params, blocks=()):
         P = len(params)

@@ -208,3 +208,34 @@ def test_suggest_right_after_an_async_device_fit(G):
         if (srt[0] - srt[1]) > 1e-3 * srt[0]:
             assert int(idx[0]) == int(np.argmax(ei)), rep
         m.free()
+
+
+def test_fixed_parameters_in_generation_encoding_and_decode(G):
+    """GPBO_P_FIXED: no encoded column and no Philox word (bit-exact against the oracle's space
+    with the same fixed parameters), gpbo_space_encode drops them, and bo_suggest_batch decodes
+    them to their constant."""
+    gpbo, ctx = G
+    params = [MIXED[0], {"kind": 4, "lo": 64.0}] + MIXED[1:] + [{"kind": 4, "lo": -1.25}]
+    nfix = len(MIXED) + 1  # index of the second fixed parameter
+    shift = lambda b: {"params": [p + 1 for p in b["params"]], "tuples": b["tuples"]}
+    blocks = [shift(b) for b in MIXED_BLOCKS]
+    sp = gpbo.Space(ctx, params, blocks)
+    ref = osp.Space(params, blocks)
+    ref0 = osp.Space(MIXED, MIXED_BLOCKS)
+    assert sp.dim == ref.dim == ref0.dim
+    got = sp.sample(99, 0, 4, 0, 2048)
+    assert np.array_equal(got.view(np.uint32), ref.sample(99, 0, 4, np.arange(2048)).view(np.uint32))
+    assert np.array_equal(got.view(np.uint32), ref0.sample(99, 0, 4, np.arange(2048)).view(np.uint32))
+    raw = ref.raw_values(ref.sample_values(99, 0, 4, np.arange(3)))
+    assert np.array_equal(sp.encode(raw), got[:3])
+    g = np.random.default_rng(5)
+    X = g.random((30, ref.dim)).astype(np.float32)
+    y = g.standard_normal(30)
+    ls = np.full(ref.dim, 0.5, np.float32)
+    m = ctx.fit([30], [ref.dim], np.ascontiguousarray(X.ravel()), y, ls, np.ones(1, np.float32),
+                np.full(1, 1e-4, np.float32))
+    idx, xr, _ = gpbo.suggest(ctx, m, [sp], [4096], 99, 4, dedup=True)
+    assert xr[0][1] == 64.0 and xr[0][nfix] == -1.25
+    exp = ref.raw_values(ref.sample_values(99, 0, 4, np.array([int(idx[0])])))[0]
+    assert np.array_equal(xr[0], exp)
+    m.free()

@@ -75,3 +75,23 @@ def test_value_mappings_and_encoding():
     # counters: word u of block b is output[u % 4] of Philox(ctr = (i, s, t, u // 4))
     ref = sp.philox4x32_10((5, 2, 5, 0), (99, 0))
     assert int(W[1][5]) == ref[1]
+
+
+def test_fixed_parameters_draw_nothing_and_encode_nothing():
+    """H0 'fixed params dropped': inserting FIXED parameters
+    anywhere leaves every other parameter's draw and encoding unchanged (they take no Philox word
+    and no column), and their raw value is the given constant."""
+    base = [{"kind": sp.REAL, "lo": -50.0, "hi": 50.0}, {"kind": sp.INT, "lo": 1, "hi": 32},
+            {"kind": sp.CATEGORICAL, "K": 4}, {"kind": sp.ORDINAL, "values": [1, 2, 4, 8]}]
+    fixed = [base[0], {"kind": sp.FIXED, "lo": 64.0}, base[1], base[2],
+             {"kind": sp.FIXED, "lo": -3.5}, base[3]]
+    a, b = sp.Space(base), sp.Space(fixed)
+    assert b.dim == a.dim == 1 + 1 + 4 + 1
+    idx = np.arange(2000)
+    for seed, s, t in ((7, 0, 0), (2 ** 40 + 5, 3, 11)):
+        ea, eb = a.sample(seed, s, t, idx), b.sample(seed, s, t, idx)
+        assert np.array_equal(ea.view(np.uint32), eb.view(np.uint32))
+        ra = a.raw_values(a.sample_values(seed, s, t, idx))
+        rb = b.raw_values(b.sample_values(seed, s, t, idx))
+        assert np.array_equal(rb[:, [0, 2, 3, 5]], ra)
+        assert np.all(rb[:, 1] == 64.0) and np.all(rb[:, 4] == -3.5)
