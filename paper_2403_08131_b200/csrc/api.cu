@@ -609,7 +609,7 @@ gpbo_status argmax_tail(gpbo_ctx *ctx, const gpbo_model *model, const float *xd,
 extern "C" {
 
 const char *gpbo_version(void) {
-  return "libgpbo 0.5 (sm_100a; fit fp64 1 CTA or 8-CTA cluster/search (multicast G) + O(n^2) "
+  return "libgpbo 0.5 (sm_100a; fit fp64 1 CTA or 8/16-CTA cluster/search (multicast G) + O(n^2) "
          "append + ML-II; score: tcgen05 fp16x3 resident (CTA pairs, cta_group::2, for n > 112; "
          "4-deep distance ring for n16 + 16 <= 128) / TMA-streamed, mean on the tensor cores, fp64 "
          "precise-mean tier, fp64 direct for small problems, CUDA-core fallback; fp64 refine with "
