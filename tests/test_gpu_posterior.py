@@ -92,3 +92,23 @@ def test_posterior_is_deterministic(G):
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
     m.free()
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_posterior_full_shape_sampled(G, cfg):
+    """gp_posterior at the bench's shapes (config 2: 2^20 candidates, the posterior pass of
+    bench.py; config 4: 2^18 of the n = 500, d = 60 search -- the 16-warp variant): T1 on 4,096
+    sampled rows the oracle computes one by one, and every row finite."""
+    gpbo, ctx = G
+    w = gen.make(cfg, M=(1 << 20) if cfg == 2 else (1 << 18))
+    m = ctx.fit(*H.pack(w), kernel=w.kernel)
+    om = H.oracle_fits(w)[0]
+    X = w.Xstar[0]
+    mu, var, ei = ctx.posterior(m, 0, X)
+    assert ctx.last_impl == 5
+    assert np.all(np.isfinite(mu)) and np.all(np.isfinite(var)) and np.all(np.isfinite(ei))
+    smp = np.sort(np.random.default_rng(cfg).choice(X.shape[0], 4096, replace=False))
+    res = gp.score(om, X[smp])
+    # T1's EI term is relative to the maximum EI; over a sample use the sample's maximum
+    H.check_T1(om, res, mu[smp], var[smp], ei[smp], f"cfg{cfg}-sampled")
+    m.free()
