@@ -26,6 +26,18 @@
 namespace gpbo {
 namespace {
 
+// whether a search of the launch is in the precise tier (decided by the fit, possibly still
+// pending on the host): the block's threads check the S records in parallel (a serial scan by
+// every thread cost ~17 us per launch at S = 64 -- one dependent L2 round trip per search)
+__device__ __forceinline__ bool any_mean_tier(const ScoreLaunch &p) {
+  int any = 0;
+  for (int i = threadIdx.x; i < p.S; i += blockDim.x) {
+    const SearchMeta &m = p.meta[i];
+    any |= m.mean_tier && (m.status == GPBO_OK || m.status == GPBO_WDEGENERATE);
+  }
+  return __syncthreads_or(any) != 0;
+}
+
 constexpr int kChunk = 64;
 #ifndef GPBO_M64_RSQ32  // float32-seeded sqrt in kval64: measured slower (1.28 -> 1.35 ms), off
 #define GPBO_M64_RSQ32 0
@@ -89,10 +101,7 @@ mean64_kernel(const ScoreLaunch p, const double *__restrict__ Xs64, const double
   __shared__ double tab[kExpTab];
   // nothing to do unless a search of the launch is in the precise tier (decided by the fit,
   // possibly still pending on the host): one early exit per block of the persistent grid
-  bool any = false;
-  for (int i = 0; i < p.S && !any; ++i)
-    any = p.meta[i].mean_tier && (p.meta[i].status == GPBO_OK || p.meta[i].status == GPBO_WDEGENERATE);
-  if (!any) return;
+  if (!any_mean_tier(p)) return;
   for (int e = threadIdx.x; e < kExpTab; e += blockDim.x) tab[e] = etab[e];
   for (int t = tile_lo + (int)blockIdx.x; t < tile_lo + tiles; t += gridDim.x) {
     const int s = search_of(p.tile_first, p.S, t);
@@ -183,10 +192,7 @@ mean64_dmma_kernel(const ScoreLaunch p, const double *__restrict__ Xs64,
   double *qb = xb + kChunk * ld;             // [kChunk]    |x_j / l|^2
   double *ab = qb + kChunk;                  // [kChunk]    alpha_j
   double *qa = ab + kChunk;                  // [128]       |x* / l|^2
-  bool any = false;
-  for (int i = 0; i < p.S && !any; ++i)
-    any = p.meta[i].mean_tier && (p.meta[i].status == GPBO_OK || p.meta[i].status == GPBO_WDEGENERATE);
-  if (!any) return;
+  if (!any_mean_tier(p)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   for (int e = tid; e < kExpTab; e += 32 * kM64Warps) tab[e] = etab[e];
