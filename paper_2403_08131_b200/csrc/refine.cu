@@ -277,6 +277,84 @@ refine_split_kernel(const RefineLaunch p) {
   }
 }
 
+// Argmax-mode refine for n <= 128 (config 3: ~5,000 entries of 64 searches): a WARP per entry
+// instead of a CTA -- lane l owns training points / rows l + 32 q (q < 4): k*_j by direct
+// differences (x* / l broadcast by shuffles), the float64 kernel and alpha_j k*_j, then
+// v_j = sum_{i <= j} (L^-1)_ji k*_i with k*_i broadcast by shuffles (each lane walks its own rows
+// of the row-major L^-1), warp sums for mu~ and |v|^2, lane 0 forms EI, the key and the bracket
+// check -- no block barriers, 8 entries in flight per CTA.
+constexpr int kRwWarps = 8;
+
+__global__ void __launch_bounds__(32 * kRwWarps)
+refine_warp_kernel(const RefineLaunch p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast phase's list is complete
+  const int lane = threadIdx.x & 31;
+  const int64_t nent = (int64_t)*p.list_count;
+  const int64_t wstep = (int64_t)gridDim.x * kRwWarps;
+  for (int64_t e = (int64_t)blockIdx.x * kRwWarps + (threadIdx.x >> 5); e < nent; e += wstep) {
+    const RefineEntry en = p.list[e];
+    const int s = (int)(en.s & ~kEntryAudit);
+    if (!(en.s & kEntryAudit) && en.ei_hi < __uint_as_float(p.thr[s])) continue;  // (warp-uniform)
+    const SearchMeta &m = p.meta[s];
+    const int n = m.n, d = m.d;
+    const float *x = p.Xstar + p.x_off[s] + (int64_t)en.row * d;
+    const float *ls = p.ls32 + m.ls_off;
+    const double *Xj = p.Xs64 + m.x_off;  // column-major x / l
+    const double *alpha = p.alpha64 + m.a_off;
+    const double xa = lane < d ? (double)x[lane] / (double)ls[lane] : 0.0;
+    const double xb = lane + 32 < d ? (double)x[lane + 32] / (double)ls[lane + 32] : 0.0;
+    double r2[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = 0; c < d; ++c) {
+      const double xc = __shfl_sync(0xffffffffu, c < 32 ? xa : xb, c & 31);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = lane + 32 * q;
+        if (j < n) { const double t = xc - Xj[(size_t)c * n + j]; r2[q] = fma(t, t, r2[q]); }
+      }
+    }
+    const double sf2 = (double)m.sf2;
+    double k[4], mu = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = lane + 32 * q;
+      k[q] = j < n ? kernel64(r2[q], sf2, m.kernel) : 0.0;
+      if (j < n) mu = fma(k[q], alpha[j], mu);
+    }
+    const double *Li = p.Linv64 + m.mat_off;  // row-major, lower part
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int qb = 0; qb < 4; ++qb) {
+      if (32 * qb >= n) break;
+      for (int ii = 0; ii < 32; ++ii) {
+        const int i = 32 * qb + ii;
+        if (i >= n) break;
+        const double ki = __shfl_sync(0xffffffffu, k[qb], ii);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = lane + 32 * q;
+          if (i <= j && j < n) v[q] = fma(Li[(size_t)j * n + i], ki, v[q]);
+        }
+      }
+    }
+    double vv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      vv += __shfl_xor_sync(0xffffffffu, vv, o);
+    }
+    if (lane == 0) {
+      const bool fin = isfinite(mu) && isfinite(vv);  // non-finite rows: no key (refine_kernel)
+      const double var64 = fmax(sf2 - vv, 0.0);
+      const double sig = sqrt(var64);
+      const double imp = resolve_best(p.best[s], m) - mu;
+      const double ei = sig > 0.0 ? sig * tau64(imp / sig) : fmax(imp, 0.0);
+      const unsigned long long key = fin ? make_key((float)ei, (uint64_t)(p.m_base[s] + en.row)) : 0ull;
+      if (key) atomicMax(p.keys + s, key);
+      if (fin && bracket_violated(ei, en.ei_lo, en.ei_hi)) atomicAdd(p.viol + s, 1ull);
+    }
+  }
+}
+
 // Small problems (rows x n16^2 small, n <= 64): the whole scoring in float64 -- no operand image,
 // no fast phase, no refine list; exact up to float64 rounding (the oracle's arithmetic).  One
 // warp per candidate: lane j owns training points j and j + 32 (k*_j by direct differences of
@@ -636,6 +714,22 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, refine_split_kernel, p);
+  }
+#ifndef GPBO_REFINE_WARP
+#define GPBO_REFINE_WARP 1
+#endif
+  if (GPBO_REFINE_WARP && p.list && nmax <= 128) {  // a warp per entry (programmatic launch)
+    const int64_t blocks = (max_entries + kRwWarps - 1) / kRwWarps;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms * 8)));
+    cfg.blockDim = dim3(32 * kRwWarps);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, refine_warp_kernel, p);
   }
   const int grid = (int)std::min<int64_t>(max_entries, (int64_t)num_sms * 4);
   refine_kernel<<<grid, kRefineThreads, 0, stream>>>(p);
