@@ -325,14 +325,16 @@ refine_warp_kernel(const RefineLaunch p) {
 #pragma unroll
     for (int qb = 0; qb < 4; ++qb) {
       if (32 * qb >= n) break;
+      // unrolled by 8 with predicates (not a break): the next columns' loads are in flight
+      // while the FMAs of this one wait (a single entry's latency bounds small refine lists)
+#pragma unroll 8
       for (int ii = 0; ii < 32; ++ii) {
         const int i = 32 * qb + ii;
-        if (i >= n) break;
         const double ki = __shfl_sync(0xffffffffu, k[qb], ii);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int j = lane + 32 * q;
-          if (i <= j && j < n) v[q] = fma(Li[(size_t)j * n + i], ki, v[q]);
+          if (i < n && i <= j && j < n) v[q] = fma(Li[(size_t)j * n + i], ki, v[q]);
         }
       }
     }
@@ -718,7 +720,11 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
 #ifndef GPBO_REFINE_WARP
 #define GPBO_REFINE_WARP 1
 #endif
-  if (GPBO_REFINE_WARP && p.list && nmax <= 128) {  // a warp per entry (programmatic launch)
+  // a warp per entry for long lists (the list scales with the candidates: >= 2^21 rows means
+  // >= 128 audit entries alone; config 3, 2^24 rows: ~5,000 entries, 0.076 -> 0.065 ms), a CTA
+  // per entry for short ones, where one entry's latency bounds the phase (config 5, 2^18 rows:
+  // ~200 entries, 0.019 ms with CTAs vs 0.029 with warps)
+  if (GPBO_REFINE_WARP && p.list && nmax <= 128 && max_entries >= (int64_t(1) << 21)) {
     const int64_t blocks = (max_entries + kRwWarps - 1) / kRwWarps;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms * 8)));
