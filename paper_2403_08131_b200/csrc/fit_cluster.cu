@@ -696,12 +696,34 @@ int fit_cluster_smem(int n, int Cc) {
   return (2 * fit_nr8(n) + 24 + 4 * 64 + 2 * 8 * fit_nr8(n) + tiles * 64) * 8;
 }
 
+// the kernel's dynamic shared memory limit: the device's opt-in per-block maximum minus the
+// kernel's static shared memory (queried once)
+static int max_dyn_smem() {
+  static const int v = [] {
+    int dev = 0, optin = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, fit_cluster_kernel) != cudaSuccess) {
+      cudaGetLastError();
+      return optin - 4096;
+    }
+    return optin - (int)fa.sharedSizeBytes;
+  }();
+  return v;
+}
+
 // whether clusters of 16 CTAs with `smem_bytes` each can be resident on this device
 bool fit_cluster16_ok(int smem_bytes) {
+  // per device, the largest size already verified (the query costs a few driver calls per fit)
+  static std::atomic<int> verified[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return false; }
+  if (dev >= 0 && dev < 64 && smem_bytes <= verified[dev].load()) return true;
   if (cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
           cudaSuccess ||
       cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes) != cudaSuccess) {
+                           max_dyn_smem()) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -721,24 +743,28 @@ bool fit_cluster16_ok(int smem_bytes) {
     cudaGetLastError();
     return false;
   }
+  if (nclusters > 0 && dev >= 0 && dev < 64) {
+    int cur = verified[dev].load();
+    while (smem_bytes > cur && !verified[dev].compare_exchange_weak(cur, smem_bytes)) {
+    }
+  }
   return nclusters > 0;
 }
 
 cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem_bytes,
                                const FitIO &io, SearchMeta *meta_out, cudaStream_t stream) {
+  // the attribute at the device maximum, once per device: never lowered below a size another
+  // launch (or fit_cluster16_ok's query) relies on
   static std::atomic<int> smem_set[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64 || smem_bytes > smem_set[dev].load()) {
+  if (smem_bytes > max_dyn_smem()) return cudaErrorInvalidValue;
+  if (dev < 0 || dev >= 64 || !smem_set[dev].load()) {
     e = cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem_bytes);
+                             max_dyn_smem());
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) {
-      int cur = smem_set[dev].load();
-      while (smem_bytes > cur && !smem_set[dev].compare_exchange_weak(cur, smem_bytes)) {
-      }
-    }
+    if (dev >= 0 && dev < 64) smem_set[dev].store(1);
   }
   if (Cc > 8) {  // 16-CTA clusters are non-portable: opt in (once per device, like the smem)
     e = cudaFuncSetAttribute(fit_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
