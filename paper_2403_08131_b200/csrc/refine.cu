@@ -175,8 +175,9 @@ refine_kernel(const RefineLaunch p) {
 // memory (DSMEM) and are summed there in rank order (deterministic), and CTA 0 forms EI and the
 // key.  The fast phase's final threshold is fixed while this runs, so every CTA of a cluster
 // takes the same skip decision.
-constexpr int kSplit = 8;
-
+// kSplit = 4 for n <= 256, 8 above (measured: config 2 refine 0.023 -> 0.020 ms with 4, config
+// 4 0.037 -> 0.046 with 4; 2 slower for both)
+template <int kSplit>
 __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kRefineThreads)
 refine_split_kernel(const RefineLaunch p) {
   namespace cg = cooperative_groups;
@@ -703,6 +704,7 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
   // candidate, 4 CTAs per SM (config 2 refine 23 -> 17 us, config 4 92 -> 41 us).  Small n with
   // many flagged candidates (config 3: ~3.5k) keeps one CTA per candidate (56 vs 371 us).
   if (p.list && nmax > 128) {
+    const int kSplit = nmax <= 256 ? 4 : 8;
     const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(max_entries, num_sms * 4 / kSplit));
     // programmatic dependent launch after the fast phase (griddepcontrol.wait inside); the
     // cluster shape comes from __cluster_dims__
@@ -715,7 +717,8 @@ cudaError_t launch_refine(const RefineLaunch &p, int64_t max_entries, int num_sm
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, refine_split_kernel, p);
+    return kSplit == 4 ? cudaLaunchKernelEx(&cfg, refine_split_kernel<4>, p)
+                       : cudaLaunchKernelEx(&cfg, refine_split_kernel<8>, p);
   }
 #ifndef GPBO_REFINE_WARP
 #define GPBO_REFINE_WARP 1
