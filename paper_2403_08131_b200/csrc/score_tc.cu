@@ -826,7 +826,10 @@ cudaError_t launch_pack_tc(const SearchMeta *meta_d, int S, const double *Linv64
                            unsigned char *img, cudaStream_t stream) {
   // 64 CTAs for one search (config 2: 18.8 -> 16.8 us, config 4: 45 -> 30 us), fewer per search
   // for large batches (config 3: 64 searches x 16)
-  const int per = std::max(4, std::min(64, 1024 / std::max(S, 1)));
+#ifndef GPBO_PACK_PER
+#define GPBO_PACK_PER 128  // measured: 64 -> 128 CTAs per search: config 2 pack 12.6 -> 11.0 us, config 4 26.8 -> 24.9; 256 same as 128
+#endif
+  const int per = std::max(4, std::min(GPBO_PACK_PER, 1024 / std::max(S, 1)));
   pack_tc_kernel<<<dim3(S, per), 256, 0, stream>>>(const_cast<SearchMeta *>(meta_d), Linv64, Xs64,
                                                    alpha64, ls32, img);
   return cudaGetLastError();
