@@ -85,3 +85,37 @@ def test_key_order_is_ei_then_lowest_index():
     assert pack_key(0.5, 3) > pack_key(0.5, 4)       # tie -> lower global index wins
     assert pack_key(0.0, 0) > pack_key(-0.0, 5) > 0  # -0 canonicalised to +0, still > 0
     assert decode_key(pack_key(1.5, 12345)) == (12345, 1.5)
+
+
+def _search_worker(rank, world, port, cfg, S, M, out):
+    """bench.py --shard searches: rank r owns searches r, r + world, ... whole (no collective on
+    the data path); the ranks' argmaxes only meet when gathered for the report."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ids = list(range(rank, S, world))
+    w = gen.make(cfg, n=30, M=M, S=S, search_ids=ids)
+    res = {}
+    for s, srch, Xs in zip(ids, w.searches, w.Xstar):
+        m = gp.fit(srch.X, srch.y, srch.lengthscale, srch.sf2, srch.sn2)
+        ei = gp.expected_improvement(*gp.posterior(m, Xs), m.best).astype(np.float32)
+        top = max(range(len(ei)), key=lambda i: (ei[i], -i))
+        res[s] = (top, float(ei[top]))
+    got = [None] * world
+    dist.all_gather_object(got, res)
+    out[rank] = {k: v for r in got for k, v in r.items()}
+    dist.destroy_process_group()
+
+
+def test_two_rank_search_shard_matches_unsharded():
+    world, cfg, S, M = 2, 3, 5, 700
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_search_worker, args=(world, _free_port(), cfg, S, M, out), nprocs=world, join=True)
+    assert out[0] == out[1] and sorted(out[0]) == list(range(S))
+    full = gen.make(cfg, n=30, M=M, S=S)
+    for s, (srch, Xs) in enumerate(zip(full.searches, full.Xstar)):
+        m = gp.fit(srch.X, srch.y, srch.lengthscale, srch.sf2, srch.sn2)
+        ei = gp.expected_improvement(*gp.posterior(m, Xs), m.best).astype(np.float32)
+        top = max(range(len(ei)), key=lambda i: (ei[i], -i))
+        assert out[0][s] == (top, float(ei[top]))
