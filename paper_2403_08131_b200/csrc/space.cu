@@ -14,6 +14,7 @@
 // Encoding (H0, reading R8): real/int (v - lo)/(hi - lo), ordinal rank/(K-1),
 // categorical one-hot; float64 then one rounding to float32.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -175,12 +176,14 @@ cudaError_t launch_gen(const SpaceView &sp_dev, uint64_t seed, uint32_t search, 
   if (count <= 0) return cudaSuccess;
   if (n > kHashSlots / 2) return cudaErrorInvalidValue;
   const size_t smem = (size_t)kGenThreads * (sp_dev.d | 1) * sizeof(float);
-  static int sms = 0;  // (a benign race: every thread computes the same value)
-  if (sms == 0) {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-      sms = v;
+  static std::atomic<int> sms_of[64];  // SM count per device (0 = not yet queried)
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+    sms = sms_of[dev].load(std::memory_order_relaxed);
+    if (sms == 0) {
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+      sms_of[dev].store(sms, std::memory_order_relaxed);
+    }
   }
   const int64_t tiles = (count + kGenThreads - 1) / kGenThreads;
   gen_kernel<<<(unsigned)std::min<int64_t>(tiles, (int64_t)std::max(sms, 1) * 8), kGenThreads, smem, st>>>(
