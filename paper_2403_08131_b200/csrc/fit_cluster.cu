@@ -35,7 +35,13 @@ namespace gpbo {
 namespace {
 
 namespace cg = cooperative_groups;
-constexpr int kWarps = kFitThreads / 32;
+// 256 threads (255 registers) rather than the one-CTA fit's 384: config 4's 16-CTA fit
+// 0.293 -> 0.266 ms measured (tools/ab_fit.sh); the one-CTA kernel is slower at 256 (0.108 -> 0.117)
+#ifndef GPBO_FITC_THREADS
+#define GPBO_FITC_THREADS 256
+#endif
+constexpr int kFitCThreads = GPBO_FITC_THREADS;
+constexpr int kWarps = kFitCThreads / 32;
 constexpr int kQ = 4;       // tiles of one tile row per trailing-update item
 constexpr int kMaxCc = 16;  // 8 portable, 16 with the non-portable attribute
 
@@ -112,7 +118,7 @@ __host__ __device__ __forceinline__ int own_tiles(int nt, int c, int Cc) {
   return own_rowoff(rows, c, Cc);
 }
 
-__global__ void __launch_bounds__(kFitThreads, 1)
+__global__ void __launch_bounds__(kFitCThreads, 1)
 fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
                    SearchMeta *__restrict__ meta_out) {
   extern __shared__ __align__(16) double sm[];
@@ -159,12 +165,12 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
   // ---- validation (every CTA; CTA 0 copies the caller's device inputs into the model)
   const bool copy = io.X_src != io.X32 && c == 0;
   int bad = 0;
-  for (int i = tid; i < n * d; i += kFitThreads) bad |= !isfinite(X[i]);  // (X: copied by the pre-pass)
-  for (int i = tid; i < n; i += kFitThreads) {
+  for (int i = tid; i < n * d; i += kFitCThreads) bad |= !isfinite(X[i]);  // (X: copied by the pre-pass)
+  for (int i = tid; i < n; i += kFitCThreads) {
     bad |= !isfinite(y[i]);
     if (copy) io.y64[m.y_off + i] = y[i];
   }
-  for (int i = tid; i < d; i += kFitThreads) {
+  for (int i = tid; i < d; i += kFitCThreads) {
     bad |= !(ls[i] > 0.f) || !isfinite(ls[i]);
     if (copy) io.ls32[m.ls_off + i] = ls[i];
   }
@@ -190,16 +196,16 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
     return t;
   };
   double acc = 0.0, amax = 0.0;
-  for (int i = tid; i < n; i += kFitThreads) { acc += y[i]; amax = fmax(amax, fabs(y[i])); }
+  for (int i = tid; i < n; i += kFitCThreads) { acc += y[i]; amax = fmax(amax, fabs(y[i])); }
   const double mean = bred(acc, 0) / n;
   amax = bred(amax, 1);
   acc = 0.0;
-  for (int i = tid; i < n; i += kFitThreads) { const double t = y[i] - mean; acc += t * t; }
+  for (int i = tid; i < n; i += kFitCThreads) { const double t = y[i] - mean; acc += t * t; }
   double stdv = sqrt(bred(acc, 0) / n);
   const bool degenerate = !(stdv > 1e-12 * amax);
   if (degenerate) stdv = 1.0;
   double bmin = INFINITY;
-  for (int i = tid; i < n; i += kFitThreads) {
+  for (int i = tid; i < n; i += kFitCThreads) {
     const double t = degenerate ? 0.0 : (y[i] - mean) / stdv;
     yt[i] = t;
     bmin = fmin(bmin, t);
@@ -387,10 +393,10 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       const int R = c + lr * Cc;
       const double2 *src = reinterpret_cast<const double2 *>(io.Kt64 + m.kt_off + (R * (R + 1) / 2) * 64);
       double2 *dst = reinterpret_cast<double2 *>(at(R, 0));
-      for (int e = tid; e < (R + 1) * 32; e += kFitThreads) dst[e] = src[e];
+      for (int e = tid; e < (R + 1) * 32; e += kFitCThreads) dst[e] = src[e];
     }
     __syncthreads();
-    for (int i = tid; i < n; i += kFitThreads)
+    for (int i = tid; i < n; i += kFitCThreads)
       if (owner(i >> 3) == c) at(i >> 3, i >> 3)[8 * (i & 7) + (i & 7)] += sn2 + jit;
     __syncthreads();
     FCT(0);
@@ -453,7 +459,7 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       FCT(3);
       if (JT + 1 == nt) {  // the last block: its L11 (no rows below, no trailing update)
         if (owner(JT) == c)
-          for (int e = tid; e < 64; e += kFitThreads) {
+          for (int e = tid; e < 64; e += kFitCThreads) {
             const int i = e >> 3, k = e & 7;
             if (k <= i && i < bb) Lg[(size_t)(J + k) * n + J + i] = l11s[e];
           }
@@ -498,12 +504,12 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
       // ---- deferred global writes of panel JT (their latency overlaps T): the L panel of the
       // own rows below the block (= their G entries) and, at the block's owner, the L11 of D(JT)
       for (int R = r0; R < nt; R += Cc)
-        for (int e = tid; e < 64; e += kFitThreads) {
+        for (int e = tid; e < 64; e += kFitCThreads) {
           const int u = e >> 3, i = 8 * R + (e & 7);
           if (i < n) Lg[(size_t)(J + u) * n + i] = GT[gx(i, u)];
         }
       if (owner(JT) == c)
-        for (int e = tid; e < 64; e += kFitThreads) {
+        for (int e = tid; e < 64; e += kFitCThreads) {
           const int i = e >> 3, k = e & 7;
           if (k <= i && i < bb) Lg[(size_t)(J + k) * n + J + i] = l11s[e];
         }
@@ -657,14 +663,14 @@ fit_cluster_kernel(const SearchMeta *__restrict__ meta_in, const FitIO io,
 #endif
   if (c != 0) return;
   double l1 = 0.0, amx = 0.0;
-  for (int k2 = tid; k2 < n; k2 += kFitThreads) {
+  for (int k2 = tid; k2 < n; k2 += kFitCThreads) {
     double a = 0.0;
     for (int r = 0; r < Cc; ++r) a += G[(size_t)r * nr8 + k2];  // rank order: deterministic
     io.alpha64[m.a_off + k2] = a;
     l1 += fabs(a);
     amx = fmax(amx, fabs(a));
   }
-  for (int kk = n + tid; kk < m.n_pad; kk += kFitThreads) io.alpha64[m.a_off + kk] = 0.0;
+  for (int kk = n + tid; kk < m.n_pad; kk += kFitCThreads) io.alpha64[m.a_off + kk] = 0.0;
   l1 = bred(l1, 0);
   amx = bred(amx, 1);
   if (tid == 0) {
@@ -729,7 +735,7 @@ bool fit_cluster16_ok(int smem_bytes) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(16);
-  cfg.blockDim = dim3(kFitThreads);
+  cfg.blockDim = dim3(kFitCThreads);
   cfg.dynamicSmemBytes = (size_t)smem_bytes;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -772,7 +778,7 @@ cudaError_t launch_fit_cluster(const SearchMeta *meta_d, int S, int Cc, int smem
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S * Cc);
-  cfg.blockDim = dim3(kFitThreads);
+  cfg.blockDim = dim3(kFitCThreads);
   cfg.dynamicSmemBytes = (size_t)smem_bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
